@@ -1,0 +1,187 @@
+/*
+ * acpf.h — C-ABI of libacpf.so, the B200 (sm_100a) batched AC power-flow engine.
+ *
+ * This is the drop-in boundary for the reference's batched-solve hot path
+ * (arxiv 2605.14103 reference package `acpflow`, pkg/src/acpflow/):
+ *
+ *   acpf_nr_*    replaces the per-scenario Newton solve the reference batch
+ *                driver calls, `newton_solve` -> `_newton_loop`
+ *                (transmission.py:306-330, 333-380), including its mismatch
+ *                map (transmission.py:194-215) and its GMRES/FD step solve
+ *                (transmission.py:259-298, sparse.py:219-338), which this
+ *                engine replaces with an exact sparse LU step.
+ *   acpf_zbus_*  replaces `zbus_iterate` -> `_zbus_loop` and
+ *                `batch_zbus_solve` (distribution.py:633-711), including
+ *                `current_injection` (:573-610), `ZBusModel.z_apply`
+ *                (:423-425) and `fixed_point_residual` (:613-621).
+ *
+ * The reference's own binding for this path is the Python callable passed to
+ * `run_batch(solver, scenarios, ...)` (batch.py:280-344); INTEGRATION.md
+ * shows the ctypes stub that binds these symbols behind that callable.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. All scenario arrays are row-major per
+ *    scenario ([batch][...]); complex values are interleaved (re, im) doubles.
+ *  - `flags` selects where batch buffers live: ACPF_HOST_PTRS (pageable or
+ *    pinned host memory; the library stages through device memory) or
+ *    ACPF_DEVICE_PTRS (device memory on the plan's device).
+ *  - Numerical outcomes are per-scenario status codes, never errors:
+ *    a call returns ACPF_OK even when scenarios diverge.
+ *  - Setup/usage errors return a negative acpf_status; the message is
+ *    available from acpf_last_error() (thread-local).
+ *  - Ownership: a plan owns device copies of the model (made at create,
+ *    released at destroy). The caller owns every batch buffer.
+ *  - Threading: calls on one plan must be serialised by the caller; distinct
+ *    plans (e.g. one per GPU) may be driven from different host threads.
+ *  - Determinism: each scenario's outputs are bitwise independent of the
+ *    batch size, its position in the batch and the chunking.
+ */
+#ifndef ACPF_H
+#define ACPF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t acpf_status;
+
+#define ACPF_OK 0
+#define ACPF_EINVAL (-1)  /* bad argument / inconsistent sizes            */
+#define ACPF_ECUDA (-2)   /* CUDA runtime error (message has details)     */
+#define ACPF_ENOMEM (-3)  /* device or host allocation failed             */
+#define ACPF_ESTRUCT (-4) /* structurally singular Jacobian pattern       */
+
+#define ACPF_HOST_PTRS 0u
+#define ACPF_DEVICE_PTRS 1u
+
+#define ACPF_ABI_VERSION 1
+
+/* Per-scenario Newton status (acpf_nr_solve `status`). Mirrors the exit
+ * branches of _newton_loop (transmission.py:347-359) in their check order. */
+#define ACPF_NR_CONVERGED 0  /* ||F||inf <= tol                          */
+#define ACPF_NR_MAX_ITER 1   /* k == max_newton, not converged           */
+#define ACPF_NR_NONFINITE 2  /* mismatch became non-finite               */
+#define ACPF_NR_VMAG_LE0 3   /* min V <= 0                               */
+#define ACPF_NR_ZERO_PIVOT 4 /* exact zero pivot in the static-pivot LU  */
+
+/* Per-scenario Z-Bus status (acpf_zbus_solve `status`), _zbus_loop :653-687. */
+#define ACPF_ZB_CONVERGED 0
+#define ACPF_ZB_MAX_ITER 1
+#define ACPF_ZB_FLOOR 2 /* VoltageFloorError mid-iteration; see floor_slot */
+
+const char* acpf_last_error(void);
+int32_t acpf_abi_version(void);
+int32_t acpf_device_count(void);
+
+/* ------------------------------------------------------------------------
+ * Transmission Newton-Raphson
+ * ------------------------------------------------------------------------ */
+typedef struct acpf_nr_plan* acpf_nr_plan_t;
+
+typedef struct acpf_nr_plan_info {
+  int32_t n_bus;        /* buses                                        */
+  int32_t n_theta;      /* |PV| + |PQ|  (angle unknowns)                */
+  int32_t n_q;          /* |PQ|         (magnitude unknowns)            */
+  int32_t n_j;          /* n_theta + n_q                                */
+  int32_t nnz_y;        /* Ybus nonzeros                                */
+  int32_t nnz_j;        /* Jacobian nonzeros                            */
+  int64_t nnz_lu;       /* static-pivot L+U slots (incl. fill)          */
+  int64_t n_pairs;      /* multiply-adds of one refactorisation         */
+  int32_t group;        /* scenarios interleaved per warp (32)          */
+  int32_t etree_height; /* informational                                */
+  int64_t workspace_bytes_per_group;
+} acpf_nr_plan_info;
+
+/* Build the device plan for one network (reference model build
+ * transmission.py:146-160 + the symbolic LU this engine needs).
+ *   y_*           complex CSR Ybus, n_bus rows, sorted column indices
+ *                 (network.py:450-496 / AdmittanceMatrix.complex_csr).
+ *   theta_block   bus indices of the angle unknowns, PV then PQ (len n_theta)
+ *   q_block       bus indices of the magnitude unknowns, PQ   (len n_q)
+ *                 (network.py:499-516)
+ *   theta_init, vmag_init   flat start incl. pinned slack/PV values
+ *                 (transmission.py:169-177), len n_bus.
+ *   perm          fill-reducing ordering of the n_theta+n_q unknowns
+ *                 (perm[k] = packed unknown eliminated k-th) or NULL for the
+ *                 built-in minimum-degree ordering.                        */
+acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_rowptr,
+                                const int32_t* y_col, const double* y_re, const double* y_im,
+                                int32_t n_theta, const int32_t* theta_block, int32_t n_q,
+                                const int32_t* q_block, const double* theta_init,
+                                const double* vmag_init, const int32_t* perm,
+                                acpf_nr_plan_t* out);
+
+/* Host-only symbolic analysis (no device needed): fills the structural
+ * fields of `info` (workspace_bytes_per_group included) for the same inputs
+ * acpf_nr_plan_create takes. Used to inspect orderings offline.          */
+acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                            int32_t n_theta, const int32_t* theta_block, int32_t n_q,
+                            const int32_t* q_block, const int32_t* perm, acpf_nr_plan_info* info);
+
+acpf_status acpf_nr_plan_info_get(acpf_nr_plan_t plan, acpf_nr_plan_info* info);
+
+/* Export the plan's ordering (len n_j) and LU row pointers (len n_j+1). */
+acpf_status acpf_nr_plan_structure(acpf_nr_plan_t plan, int32_t* perm_out, int64_t* lu_rowptr_out);
+
+/* Solve `batch` scenarios (each = newton_solve(model, scenario, opts) from the
+ * flat start).
+ *   p_spec [batch][n_theta], q_spec [batch][n_q]   (TransmissionScenario)
+ *   theta_out, vmag_out [batch][n_bus]             (NewtonResult.state)
+ *   converged [batch] u8, iterations [batch], final_mismatch_inf [batch],
+ *   status [batch] (ACPF_NR_*).
+ * Any output pointer except theta_out/vmag_out may be NULL.                */
+acpf_status acpf_nr_solve(acpf_nr_plan_t plan, int64_t batch, const double* p_spec,
+                          const double* q_spec, double tol_mismatch, int32_t max_newton,
+                          double* theta_out, double* vmag_out, uint8_t* converged,
+                          int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                          uint32_t flags, void* cuda_stream);
+
+/* Device time (ms) of the last acpf_nr_solve's Newton kernel launches,
+ * measured with CUDA events on the solve stream; and their launch count. */
+acpf_status acpf_nr_last_timing(acpf_nr_plan_t plan, double* kernel_ms, int32_t* launches);
+
+acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t plan);
+
+/* ------------------------------------------------------------------------
+ * Distribution Z-Bus fixed point
+ * ------------------------------------------------------------------------ */
+typedef struct acpf_zbus_plan* acpf_zbus_plan_t;
+
+/* Build the device plan (reference ZBusModel, distribution.py:394-517).
+ *   n            non-slack node-phases
+ *   n_l, l_index load-touched reduced indices (sorted, unique)
+ *   zl           Z[:, l] as [n][n_l] interleaved complex (row-major)
+ *   v0           no-load profile [n] complex
+ *   wye_idx      [n_wye] reduced index per wye load
+ *   delta_p/q    [n_delta] reduced indices of each delta pair
+ *   voltage_floor  division guard (default 1e-6 in the reference)       */
+acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const int32_t* l_index,
+                                  const double* zl, const double* v0, int32_t n_wye,
+                                  const int32_t* wye_idx, int32_t n_delta, const int32_t* delta_p,
+                                  const int32_t* delta_q, double voltage_floor,
+                                  acpf_zbus_plan_t* out);
+
+/* Solve `batch` scenarios (each = zbus_iterate(model, scenario, opts)).
+ *   s_wye [batch][n_wye] complex, s_delta [batch][n_delta] complex
+ *   v_out [batch][n] complex (FixedPointResult.v)
+ *   converged u8, iterations, final_delta, residual_inf, status (ACPF_ZB_*)
+ *   floor_slot: for ACPF_ZB_FLOOR, which check failed first, in the
+ *   reference's order: k (wye k), n_wye+k (delta k, phase p),
+ *   n_wye+n_delta+k (delta k, phase q), n_wye+2*n_delta+k (delta k, p-q);
+ *   -1 otherwise. Any output pointer except v_out may be NULL.          */
+acpf_status acpf_zbus_solve(acpf_zbus_plan_t plan, int64_t batch, const double* s_wye,
+                            const double* s_delta, double tol, int32_t max_iter, double* v_out,
+                            uint8_t* converged, int32_t* iterations, double* final_delta,
+                            double* residual_inf, int32_t* status, int32_t* floor_slot,
+                            uint32_t flags, void* cuda_stream);
+
+acpf_status acpf_zbus_last_timing(acpf_zbus_plan_t plan, double* kernel_ms, int32_t* launches);
+
+acpf_status acpf_zbus_plan_destroy(acpf_zbus_plan_t plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACPF_H */

@@ -1,0 +1,655 @@
+// C-ABI entry points of libacpf.so (declared in include/acpf.h).
+//
+// Plans own device copies of the per-network model; solves stream the
+// caller's batch through the fused kernels (nr_kernel.cu, zbus_kernel.cu),
+// chunking when the batch would not fit the device workspace, staging host
+// buffers through device memory when ACPF_HOST_PTRS is given.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "acpf_internal.cuh"
+#include "nr_symbolic.h"
+
+namespace acpf {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+#define ACPF_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+      return e_ == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;             \
+    }                                                                                \
+  } while (0)
+
+// Owning list of device allocations.
+struct DevArena {
+  std::vector<void*> ptrs;
+  ~DevArena() { release(); }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+  template <class T>
+  cudaError_t upload(T** out, const T* host, size_t count) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T));
+    if (e != cudaSuccess) return e;
+    ptrs.push_back(p);
+    if (count) e = cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice);
+    *out = static_cast<T*>(p);
+    return e;
+  }
+  cudaError_t alloc(void** out, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, bytes));
+    if (e != cudaSuccess) return e;
+    ptrs.push_back(p);
+    *out = p;
+    return e;
+  }
+};
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::strtoll(v, nullptr, 10);
+}
+
+}  // namespace
+}  // namespace acpf
+
+using namespace acpf;
+
+struct acpf_nr_plan {
+  int device = 0;
+  NrSymbolic sym;
+  NrDeviceModel dm{};
+  DevArena model;
+  DevArena work;
+  NrWorkspace ws{};
+  int64_t ws_groups = 0;
+  int64_t bytes_per_group = 0;
+  DevArena stage;
+  size_t stage_bytes = 0;
+  void* stage_base = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int last_launches = 0;
+};
+
+struct acpf_zbus_plan {
+  int device = 0;
+  ZbDeviceModel dm{};
+  DevArena model;
+  DevArena stage;
+  size_t stage_bytes = 0;
+  void* stage_base = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int last_launches = 0;
+};
+
+static void fill_info(const NrSymbolic& s, acpf_nr_plan_info* info) {
+  info->n_bus = s.n_bus;
+  info->n_theta = s.n_theta;
+  info->n_q = s.n_q;
+  info->n_j = s.n_j;
+  info->nnz_y = (int32_t)s.nnz_y;
+  info->nnz_j = (int32_t)s.nnz_j;
+  info->nnz_lu = s.nnz_lu;
+  info->n_pairs = s.n_pairs;
+  info->group = kGroup;
+  info->etree_height = s.etree_height;
+  info->workspace_bytes_per_group =
+      (int64_t)kGroup * 8 * (s.nnz_lu + 3 * (int64_t)s.n_j + 8 * (int64_t)s.n_bus);
+}
+
+extern "C" {
+
+const char* acpf_last_error(void) { return g_error.c_str(); }
+
+int32_t acpf_abi_version(void) { return ACPF_ABI_VERSION; }
+
+int32_t acpf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// Newton
+// ---------------------------------------------------------------------------
+
+acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_rowptr,
+                                const int32_t* y_col, const double* y_re, const double* y_im,
+                                int32_t n_theta, const int32_t* theta_block, int32_t n_q,
+                                const int32_t* q_block, const double* theta_init,
+                                const double* vmag_init, const int32_t* perm,
+                                acpf_nr_plan_t* out) {
+  if (!out || n_bus <= 0 || !y_rowptr || !y_col || !y_re || !y_im || n_theta < 0 || n_q < 0 ||
+      (n_theta && !theta_block) || (n_q && !q_block) || !theta_init || !vmag_init) {
+    set_error("acpf_nr_plan_create: invalid argument");
+    return ACPF_EINVAL;
+  }
+  *out = nullptr;
+  acpf_nr_plan* p = new (std::nothrow) acpf_nr_plan();
+  if (!p) {
+    set_error("host allocation failed");
+    return ACPF_ENOMEM;
+  }
+  try {
+    build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+  } catch (const std::exception& ex) {
+    set_error(std::string("symbolic analysis: ") + ex.what());
+    delete p;
+    return ACPF_EINVAL;
+  }
+  p->device = device;
+  DeviceGuard dg(device);
+  const NrSymbolic& s = p->sym;
+  const int nj = s.n_j;
+  const int64_t nnz = y_rowptr[n_bus];
+  std::vector<double2> yv(nnz);
+  for (int64_t e = 0; e < nnz; ++e) yv[e] = make_double2(y_re[e], y_im[e]);
+  std::vector<int32_t> tpos(n_bus, -1), qpos(n_bus, -1);
+  for (int k = 0; k < n_theta; ++k) tpos[theta_block[k]] = k;
+  for (int k = 0; k < n_q; ++k) qpos[q_block[k]] = n_theta + k;
+  std::vector<int32_t> rowptr(nj + 1), diag(nj), pptr(s.nnz_lu + 1);
+  for (int i = 0; i <= nj; ++i) rowptr[i] = (int32_t)s.rowptr[i];
+  for (int i = 0; i < nj; ++i) diag[i] = (int32_t)s.diag[i];
+  for (int64_t t = 0; t <= s.nnz_lu; ++t) pptr[t] = (int32_t)s.pair_ptr[t];
+  std::vector<int2> desc(s.nnz_lu), pairs(s.n_pairs);
+  for (int64_t t = 0; t < s.nnz_lu; ++t)
+    desc[t] = make_int2(s.slot_ynz[t], s.slot_jbus[t] | ((int32_t)s.slot_type[t] << 28));
+  for (int64_t q = 0; q < s.n_pairs; ++q) pairs[q] = make_int2(s.pair_l[q], s.pair_u[q]);
+
+  NrDeviceModel& d = p->dm;
+  d.n_bus = n_bus;
+  d.n_theta = n_theta;
+  d.n_q = n_q;
+  d.n_j = nj;
+  d.nnz_lu = s.nnz_lu;
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = p->model.upload(dst, src, cnt);
+  };
+  up(const_cast<int32_t**>(&d.y_rowptr), y_rowptr, (size_t)n_bus + 1);
+  up(const_cast<int32_t**>(&d.y_col), y_col, (size_t)nnz);
+  up(const_cast<double2**>(&d.y_val), yv.data(), (size_t)nnz);
+  up(const_cast<double**>(&d.theta_init), theta_init, (size_t)n_bus);
+  up(const_cast<double**>(&d.vmag_init), vmag_init, (size_t)n_bus);
+  up(const_cast<int32_t**>(&d.tpos), tpos.data(), (size_t)n_bus);
+  up(const_cast<int32_t**>(&d.qpos), qpos.data(), (size_t)n_bus);
+  up(const_cast<int32_t**>(&d.ipos), s.ipos.data(), (size_t)nj);
+  up(const_cast<int32_t**>(&d.row_bus), s.row_bus.data(), (size_t)nj);
+  up(const_cast<int32_t**>(&d.row_kind), s.row_kind.data(), (size_t)nj);
+  up(const_cast<int32_t**>(&d.lu_rowptr), rowptr.data(), (size_t)nj + 1);
+  up(const_cast<int32_t**>(&d.lu_col), s.col.data(), (size_t)s.nnz_lu);
+  up(const_cast<int32_t**>(&d.lu_diag), diag.data(), (size_t)nj);
+  up(const_cast<int2**>(&d.slot_desc), desc.data(), (size_t)s.nnz_lu);
+  up(const_cast<int32_t**>(&d.pair_ptr), pptr.data(), (size_t)s.nnz_lu + 1);
+  up(const_cast<int2**>(&d.pairs), pairs.data(), (size_t)s.n_pairs);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+  if (e != cudaSuccess) {
+    set_error(std::string("acpf_nr_plan_create: ") + cudaGetErrorString(e));
+    delete p;
+    return e == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;
+  }
+  {
+    acpf_nr_plan_info tmp;
+    fill_info(s, &tmp);
+    p->bytes_per_group = tmp.workspace_bytes_per_group;
+  }
+  *out = p;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                            int32_t n_theta, const int32_t* theta_block, int32_t n_q,
+                            const int32_t* q_block, const int32_t* perm, acpf_nr_plan_info* info) {
+  if (n_bus <= 0 || !y_rowptr || !y_col || !info || (n_theta && !theta_block) || (n_q && !q_block)) {
+    set_error("acpf_nr_analyze: invalid argument");
+    return ACPF_EINVAL;
+  }
+  try {
+    NrSymbolic s;
+    build_nr_symbolic(s, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+    fill_info(s, info);
+  } catch (const std::exception& ex) {
+    set_error(std::string("symbolic analysis: ") + ex.what());
+    return ACPF_EINVAL;
+  }
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_plan_info_get(acpf_nr_plan_t p, acpf_nr_plan_info* info) {
+  if (!p || !info) {
+    set_error("acpf_nr_plan_info_get: null argument");
+    return ACPF_EINVAL;
+  }
+  fill_info(p->sym, info);
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_plan_structure(acpf_nr_plan_t p, int32_t* perm_out, int64_t* lu_rowptr_out) {
+  if (!p) {
+    set_error("acpf_nr_plan_structure: null plan");
+    return ACPF_EINVAL;
+  }
+  if (perm_out) std::memcpy(perm_out, p->sym.perm.data(), p->sym.perm.size() * sizeof(int32_t));
+  if (lu_rowptr_out)
+    std::memcpy(lu_rowptr_out, p->sym.rowptr.data(), p->sym.rowptr.size() * sizeof(int64_t));
+  return ACPF_OK;
+}
+
+static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
+  if (p->ws_groups >= groups) return ACPF_OK;
+  p->work.release();
+  p->ws_groups = 0;
+  const NrDeviceModel& d = p->dm;
+  const size_t G = (size_t)groups * kGroup;
+  void* ptr;
+  auto get = [&](size_t bytes) -> void* {
+    if (p->work.alloc(&ptr, bytes) != cudaSuccess) return nullptr;
+    return ptr;
+  };
+  NrWorkspace& w = p->ws;
+  w.lu = (double*)get(G * d.nnz_lu * 8);
+  w.invd = (double*)get(G * d.n_j * 8);
+  w.yx = (double*)get(G * d.n_j * 8);
+  w.spec = (double*)get(G * d.n_j * 8);
+  w.th = (double*)get(G * d.n_bus * 8);
+  w.vm = (double*)get(G * d.n_bus * 8);
+  w.U = (double2*)get(G * d.n_bus * 16);
+  w.E = (double2*)get(G * d.n_bus * 16);
+  w.I = (double2*)get(G * d.n_bus * 16);
+  if (!w.lu || !w.invd || !w.yx || !w.spec || !w.th || !w.vm || !w.U || !w.E || !w.I) {
+    p->work.release();
+    cudaGetLastError();
+    set_error("acpf_nr_solve: device workspace allocation failed (" + std::to_string(groups) +
+              " groups); lower ACPF_NR_CHUNK");
+    return ACPF_ENOMEM;
+  }
+  w.groups = groups;
+  p->ws_groups = groups;
+  return ACPF_OK;
+}
+
+static acpf_status ensure_stage(DevArena& arena, size_t& have, void*& base, size_t bytes) {
+  if (have >= bytes) return ACPF_OK;
+  arena.release();
+  have = 0;
+  if (arena.alloc(&base, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("staging allocation failed (" + std::to_string(bytes) + " bytes)");
+    return ACPF_ENOMEM;
+  }
+  have = bytes;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
+                          const double* q_spec, double tol_mismatch, int32_t max_newton,
+                          double* theta_out, double* vmag_out, uint8_t* converged,
+                          int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                          uint32_t flags, void* cuda_stream) {
+  if (!p || batch < 0 || !theta_out || !vmag_out || max_newton < 1 || !(tol_mismatch > 0) ||
+      (p->dm.n_theta && !p_spec) || (p->dm.n_q && !q_spec) || flags > 1u) {
+    set_error("acpf_nr_solve: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (batch == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const NrDeviceModel& d = p->dm;
+  const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
+
+  int64_t chunk = env_int("ACPF_NR_CHUNK", 0);
+  if (chunk <= 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const int64_t have_groups = p->ws_groups;
+    const int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
+    int64_t groups = std::max<int64_t>(1, budget / std::max<int64_t>(1, p->bytes_per_group));
+    groups = std::min<int64_t>(groups, 4096);
+    chunk = groups * kGroup;
+  }
+  chunk = std::min<int64_t>(chunk, batch);
+  chunk = ((chunk + kGroup - 1) / kGroup) * kGroup;
+  const int64_t groups = chunk / kGroup;
+  acpf_status rc = nr_ensure_workspace(p, groups);
+  if (rc != ACPF_OK) return rc;
+
+  // per-scenario byte sizes
+  const size_t in_b = (size_t)(d.n_theta + d.n_q) * 8;
+  const size_t out_b = (size_t)d.n_bus * 16 + 1 + 4 + 8 + 4;
+  if (!dev_ptrs) {
+    rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, (size_t)chunk * (in_b + out_b) + 256);
+    if (rc != ACPF_OK) return rc;
+  }
+  float total_ms = 0.0f;
+  int launches = 0;
+  for (int64_t s0 = 0; s0 < batch; s0 += chunk) {
+    const int64_t nb = std::min(chunk, batch - s0);
+    NrBatchIO io{};
+    io.batch = nb;
+    if (dev_ptrs) {
+      io.p_spec = p_spec ? p_spec + s0 * d.n_theta : nullptr;
+      io.q_spec = q_spec ? q_spec + s0 * d.n_q : nullptr;
+      io.theta_out = theta_out + s0 * d.n_bus;
+      io.vmag_out = vmag_out + s0 * d.n_bus;
+      io.converged = converged ? converged + s0 : nullptr;
+      io.iterations = iterations ? iterations + s0 : nullptr;
+      io.fnorm = final_mismatch_inf ? final_mismatch_inf + s0 : nullptr;
+      io.status = status ? status + s0 : nullptr;
+    } else {
+      char* b = (char*)p->stage_base;
+      double* ps = (double*)b;
+      b += (size_t)chunk * d.n_theta * 8;
+      double* qs = (double*)b;
+      b += (size_t)chunk * d.n_q * 8;
+      double* th = (double*)b;
+      b += (size_t)chunk * d.n_bus * 8;
+      double* vm = (double*)b;
+      b += (size_t)chunk * d.n_bus * 8;
+      double* fn = (double*)b;
+      b += (size_t)chunk * 8;
+      int32_t* it = (int32_t*)b;
+      b += (size_t)chunk * 4;
+      int32_t* stt = (int32_t*)b;
+      b += (size_t)chunk * 4;
+      uint8_t* cv = (uint8_t*)b;
+      if (d.n_theta)
+        ACPF_CUDA(cudaMemcpyAsync(ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, st));
+      if (d.n_q)
+        ACPF_CUDA(cudaMemcpyAsync(qs, q_spec + s0 * d.n_q, nb * d.n_q * 8, cudaMemcpyHostToDevice, st));
+      io.p_spec = ps;
+      io.q_spec = qs;
+      io.theta_out = th;
+      io.vmag_out = vm;
+      io.fnorm = fn;
+      io.iterations = it;
+      io.status = stt;
+      io.converged = cv;
+    }
+    ACPF_CUDA(cudaEventRecord(p->ev0, st));
+    ACPF_CUDA(launch_nr_newton(d, p->ws, io, tol_mismatch, max_newton, st));
+    ACPF_CUDA(cudaEventRecord(p->ev1, st));
+    ++launches;
+    if (!dev_ptrs) {
+      ACPF_CUDA(cudaMemcpyAsync(theta_out + s0 * d.n_bus, io.theta_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
+      ACPF_CUDA(cudaMemcpyAsync(vmag_out + s0 * d.n_bus, io.vmag_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
+      if (final_mismatch_inf)
+        ACPF_CUDA(cudaMemcpyAsync(final_mismatch_inf + s0, io.fnorm, nb * 8, cudaMemcpyDeviceToHost, st));
+      if (iterations)
+        ACPF_CUDA(cudaMemcpyAsync(iterations + s0, io.iterations, nb * 4, cudaMemcpyDeviceToHost, st));
+      if (status) ACPF_CUDA(cudaMemcpyAsync(status + s0, io.status, nb * 4, cudaMemcpyDeviceToHost, st));
+      if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, io.converged, nb, cudaMemcpyDeviceToHost, st));
+    }
+    ACPF_CUDA(cudaEventSynchronize(p->ev1));
+    float ms = 0.0f;
+    ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    total_ms += ms;
+  }
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  p->last_ms = total_ms;
+  p->last_launches = launches;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_last_timing(acpf_nr_plan_t p, double* kernel_ms, int32_t* launches) {
+  if (!p) {
+    set_error("acpf_nr_last_timing: null plan");
+    return ACPF_EINVAL;
+  }
+  if (kernel_ms) *kernel_ms = p->last_ms;
+  if (launches) *launches = p->last_launches;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
+  if (!p) return ACPF_OK;
+  {
+    DeviceGuard dg(p->device);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    p->work.release();
+    p->stage.release();
+    p->model.release();
+  }
+  delete p;
+  return ACPF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Z-Bus
+// ---------------------------------------------------------------------------
+
+acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const int32_t* l_index,
+                                  const double* zl, const double* v0, int32_t n_wye,
+                                  const int32_t* wye_idx, int32_t n_delta, const int32_t* delta_p,
+                                  const int32_t* delta_q, double voltage_floor,
+                                  acpf_zbus_plan_t* out) {
+  if (!out || n <= 0 || n_l < 0 || (n_l && (!l_index || !zl)) || !v0 || n_wye < 0 ||
+      n_delta < 0 || (n_wye && !wye_idx) || (n_delta && (!delta_p || !delta_q)) ||
+      n_l > 1024) {
+    set_error("acpf_zbus_plan_create: invalid argument");
+    return ACPF_EINVAL;
+  }
+  *out = nullptr;
+  std::vector<int32_t> lpos(n, -1);
+  for (int k = 0; k < n_l; ++k) {
+    if (l_index[k] < 0 || l_index[k] >= n || (k && l_index[k] <= l_index[k - 1])) {
+      set_error("acpf_zbus_plan_create: l_index must be sorted, unique, in range");
+      return ACPF_EINVAL;
+    }
+    lpos[l_index[k]] = k;
+  }
+  auto map = [&](const int32_t* idx, int cnt, std::vector<int32_t>& o) -> bool {
+    o.resize(cnt);
+    for (int k = 0; k < cnt; ++k) {
+      if (idx[k] < 0 || idx[k] >= n || lpos[idx[k]] < 0) return false;
+      o[k] = lpos[idx[k]];
+    }
+    return true;
+  };
+  std::vector<int32_t> wl, dpl, dql;
+  if (!map(wye_idx, n_wye, wl) || !map(delta_p, n_delta, dpl) || !map(delta_q, n_delta, dql)) {
+    set_error("acpf_zbus_plan_create: load index not in l_index");
+    return ACPF_EINVAL;
+  }
+  acpf_zbus_plan* p = new (std::nothrow) acpf_zbus_plan();
+  if (!p) {
+    set_error("host allocation failed");
+    return ACPF_ENOMEM;
+  }
+  p->device = device;
+  DeviceGuard dg(device);
+  ZbDeviceModel& d = p->dm;
+  d.n = n;
+  d.n_l = n_l;
+  d.kpad = std::max(4, ((n_l + 3) / 4) * 4);
+  d.n_rb = (n + kZbRows - 1) / kZbRows;
+  d.n_wye = n_wye;
+  d.n_delta = n_delta;
+  d.floor = voltage_floor;
+  std::vector<double> frag(zbus_frag_doubles(d.n_rb, d.kpad));
+  zbus_pack_fragments(zl, n, n_l, d.n_rb, d.kpad, frag.data());
+  std::vector<double2> v0p((size_t)d.n_rb * kZbRows, make_double2(0.0, 0.0));
+  for (int r = 0; r < n; ++r) v0p[r] = make_double2(v0[2 * r], v0[2 * r + 1]);
+  std::vector<int32_t> lrow(l_index, l_index + n_l);
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = p->model.upload(dst, src, cnt);
+  };
+  up(const_cast<double**>(&d.zfrag), frag.data(), frag.size());
+  up(const_cast<double2**>(&d.v0), v0p.data(), v0p.size());
+  up(const_cast<int32_t**>(&d.l_row), lrow.data(), lrow.size());
+  up(const_cast<int32_t**>(&d.wye_l), wl.data(), wl.size());
+  up(const_cast<int32_t**>(&d.dp_l), dpl.data(), dpl.size());
+  up(const_cast<int32_t**>(&d.dq_l), dql.data(), dql.size());
+  d.lpos_of_row = nullptr;
+  double* mag0_dev = nullptr;
+  if (e == cudaSuccess) e = p->model.upload(&mag0_dev, (const double*)nullptr, 0);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+  if (e == cudaSuccess) {
+    ZbBatchIO io{};
+    e = launch_zbus(d, io, 0.0, 1, true, mag0_dev, nullptr, 0);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(&d.mag0, mag0_dev, 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    set_error(std::string("acpf_zbus_plan_create: ") + cudaGetErrorString(e));
+    delete p;
+    return e == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;
+  }
+  *out = p;
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_solve(acpf_zbus_plan_t p, int64_t batch, const double* s_wye,
+                            const double* s_delta, double tol, int32_t max_iter, double* v_out,
+                            uint8_t* converged, int32_t* iterations, double* final_delta,
+                            double* residual_inf, int32_t* status, int32_t* floor_slot,
+                            uint32_t flags, void* cuda_stream) {
+  const ZbDeviceModel& d = p ? p->dm : ZbDeviceModel{};
+  if (!p || batch < 0 || !v_out || max_iter < 1 || !(tol > 0) || (d.n_wye && !s_wye) ||
+      (d.n_delta && !s_delta) || flags > 1u) {
+    set_error("acpf_zbus_solve: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (batch == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
+  int64_t chunk = dev_ptrs ? batch : std::min<int64_t>(batch, env_int("ACPF_ZBUS_CHUNK", 65536));
+  const size_t in_b = (size_t)(d.n_wye + d.n_delta) * 16;
+  const size_t out_b = (size_t)d.n * 16 + 1 + 4 + 8 + 8 + 4 + 4;
+  if (!dev_ptrs) {
+    acpf_status rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, (size_t)chunk * (in_b + out_b) + 256);
+    if (rc != ACPF_OK) return rc;
+  }
+  float total_ms = 0.0f;
+  int launches = 0;
+  for (int64_t s0 = 0; s0 < batch; s0 += chunk) {
+    const int64_t nb = std::min(chunk, batch - s0);
+    ZbBatchIO io{};
+    io.batch = nb;
+    if (dev_ptrs) {
+      io.s_wye = (const double2*)(s_wye ? s_wye + 2 * s0 * d.n_wye : nullptr);
+      io.s_delta = (const double2*)(s_delta ? s_delta + 2 * s0 * d.n_delta : nullptr);
+      io.v_out = (double2*)(v_out + 2 * s0 * d.n);
+      io.converged = converged ? converged + s0 : nullptr;
+      io.iterations = iterations ? iterations + s0 : nullptr;
+      io.final_delta = final_delta ? final_delta + s0 : nullptr;
+      io.residual = residual_inf ? residual_inf + s0 : nullptr;
+      io.status = status ? status + s0 : nullptr;
+      io.floor_slot = floor_slot ? floor_slot + s0 : nullptr;
+    } else {
+      char* b = (char*)p->stage_base;
+      double2* sw = (double2*)b;
+      b += (size_t)chunk * d.n_wye * 16;
+      double2* sd = (double2*)b;
+      b += (size_t)chunk * d.n_delta * 16;
+      double2* vo = (double2*)b;
+      b += (size_t)chunk * d.n * 16;
+      double* fd = (double*)b;
+      b += (size_t)chunk * 8;
+      double* rs = (double*)b;
+      b += (size_t)chunk * 8;
+      int32_t* it = (int32_t*)b;
+      b += (size_t)chunk * 4;
+      int32_t* stt = (int32_t*)b;
+      b += (size_t)chunk * 4;
+      int32_t* fs = (int32_t*)b;
+      b += (size_t)chunk * 4;
+      uint8_t* cv = (uint8_t*)b;
+      if (d.n_wye)
+        ACPF_CUDA(cudaMemcpyAsync(sw, s_wye + 2 * s0 * d.n_wye, nb * d.n_wye * 16, cudaMemcpyHostToDevice, st));
+      if (d.n_delta)
+        ACPF_CUDA(cudaMemcpyAsync(sd, s_delta + 2 * s0 * d.n_delta, nb * d.n_delta * 16, cudaMemcpyHostToDevice, st));
+      io.s_wye = sw;
+      io.s_delta = sd;
+      io.v_out = vo;
+      io.final_delta = fd;
+      io.residual = rs;
+      io.iterations = it;
+      io.status = stt;
+      io.floor_slot = fs;
+      io.converged = cv;
+    }
+    int nl = 0;
+    ACPF_CUDA(cudaEventRecord(p->ev0, st));
+    ACPF_CUDA(launch_zbus(d, io, tol, max_iter, false, nullptr, &nl, st));
+    ACPF_CUDA(cudaEventRecord(p->ev1, st));
+    launches += nl;
+    if (!dev_ptrs) {
+      ACPF_CUDA(cudaMemcpyAsync(v_out + 2 * s0 * d.n, io.v_out, nb * d.n * 16, cudaMemcpyDeviceToHost, st));
+      if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, io.converged, nb, cudaMemcpyDeviceToHost, st));
+      if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + s0, io.iterations, nb * 4, cudaMemcpyDeviceToHost, st));
+      if (final_delta) ACPF_CUDA(cudaMemcpyAsync(final_delta + s0, io.final_delta, nb * 8, cudaMemcpyDeviceToHost, st));
+      if (residual_inf) ACPF_CUDA(cudaMemcpyAsync(residual_inf + s0, io.residual, nb * 8, cudaMemcpyDeviceToHost, st));
+      if (status) ACPF_CUDA(cudaMemcpyAsync(status + s0, io.status, nb * 4, cudaMemcpyDeviceToHost, st));
+      if (floor_slot) ACPF_CUDA(cudaMemcpyAsync(floor_slot + s0, io.floor_slot, nb * 4, cudaMemcpyDeviceToHost, st));
+    }
+    ACPF_CUDA(cudaEventSynchronize(p->ev1));
+    float ms = 0.0f;
+    ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    total_ms += ms;
+  }
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  p->last_ms = total_ms;
+  p->last_launches = launches;
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_last_timing(acpf_zbus_plan_t p, double* kernel_ms, int32_t* launches) {
+  if (!p) {
+    set_error("acpf_zbus_last_timing: null plan");
+    return ACPF_EINVAL;
+  }
+  if (kernel_ms) *kernel_ms = p->last_ms;
+  if (launches) *launches = p->last_launches;
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_plan_destroy(acpf_zbus_plan_t p) {
+  if (!p) return ACPF_OK;
+  {
+    DeviceGuard dg(p->device);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    p->stage.release();
+    p->model.release();
+  }
+  delete p;
+  return ACPF_OK;
+}
+
+}  // extern "C"

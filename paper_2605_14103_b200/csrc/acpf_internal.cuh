@@ -1,0 +1,109 @@
+// Internal declarations shared by the libacpf translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/acpf.h"
+
+namespace acpf {
+
+void set_error(const std::string& msg);
+
+constexpr int kGroup = 32;  // scenarios interleaved per warp (one lane each)
+
+// ---------------------------------------------------------------------------
+// Newton plan (device side view passed to the kernel by value)
+// ---------------------------------------------------------------------------
+struct NrDeviceModel {
+  int n_bus, n_theta, n_q, n_j;
+  const int32_t* y_rowptr;
+  const int32_t* y_col;
+  const double2* y_val;
+  const double* theta_init;
+  const double* vmag_init;
+  const int32_t* tpos;     // [n_bus] packed theta index or -1
+  const int32_t* qpos;     // [n_bus] packed V index (>= n_theta) or -1
+  const int32_t* ipos;     // [n_j] packed -> elimination position
+  const int32_t* row_bus;  // [n_j]
+  const int32_t* row_kind; // [n_j]
+  const int32_t* lu_rowptr;  // [n_j+1]
+  const int32_t* lu_col;     // [nnz_lu]
+  const int32_t* lu_diag;    // [n_j]
+  const int2* slot_desc;     // [nnz_lu] (ynz, jbus | type << 28)
+  const int32_t* pair_ptr;   // [nnz_lu+1]
+  const int2* pairs;         // [n_pairs] (l slot, u slot)
+  int64_t nnz_lu;
+};
+
+struct NrWorkspace {
+  // all per-group blocks are [rows][kGroup]
+  double* lu;     // nnz_lu
+  double* invd;   // n_j
+  double* yx;     // n_j
+  double* spec;   // n_j
+  double* th;     // n_bus
+  double* vm;     // n_bus
+  double2* U;     // n_bus
+  double2* E;     // n_bus
+  double2* I;     // n_bus
+  int64_t groups;
+};
+
+struct NrBatchIO {
+  const double* p_spec;  // [batch][n_theta]
+  const double* q_spec;  // [batch][n_q]
+  double* theta_out;     // [batch][n_bus]
+  double* vmag_out;
+  uint8_t* converged;
+  int32_t* iterations;
+  double* fnorm;
+  int32_t* status;
+  int64_t batch;  // scenarios in this chunk
+};
+
+cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrWorkspace& w, const NrBatchIO& io,
+                             double tol, int max_newton, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// Z-Bus plan
+// ---------------------------------------------------------------------------
+struct ZbDeviceModel {
+  int n;          // non-slack node-phases
+  int n_l;        // load columns
+  int kpad;       // n_l rounded up to a multiple of 4
+  int n_rb;       // row blocks of kZbRows rows
+  const double* zfrag;   // fragment-ordered Z[:, l] (see zbus_kernel.cu)
+  const double2* v0;     // [n_rb * kZbRows] (zero padded)
+  const int32_t* lpos_of_row;  // unused by kernel v1, kept for diagnostics
+  const int32_t* l_row;  // [n_l] reduced row of each load column
+  const int32_t* wye_l;  // [n_wye] load column of each wye load
+  const int32_t* dp_l;   // [n_delta]
+  const int32_t* dq_l;   // [n_delta]
+  int n_wye, n_delta;
+  double floor;
+  double mag0;   // sum |v0| with the kernel's own reduction order
+};
+
+struct ZbBatchIO {
+  const double2* s_wye;   // [batch][n_wye]
+  const double2* s_delta; // [batch][n_delta]
+  double2* v_out;         // [batch][n]
+  uint8_t* converged;
+  int32_t* iterations;
+  double* final_delta;
+  double* residual;
+  int32_t* status;
+  int32_t* floor_slot;
+  int64_t batch;
+};
+
+constexpr int kZbRows = 64;  // rows per Z stage
+
+cudaError_t launch_zbus(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter,
+                        bool mag0_mode, double* mag0_out, int* launches, cudaStream_t stream);
+size_t zbus_frag_doubles(int n_rb, int kpad);
+void zbus_pack_fragments(const double* zl, int n, int n_l, int n_rb, int kpad, double* out);
+
+}  // namespace acpf

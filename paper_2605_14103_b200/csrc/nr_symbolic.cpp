@@ -1,0 +1,238 @@
+// Host-side symbolic analysis for the batched Newton solve (once per network).
+//
+// The reference never assembles the Jacobian (transmission.py:218-236 is a
+// matrix-free JVP under FD-preconditioned GMRES, sparse.py:219-338). This
+// engine replaces that step solve with an exact sparse LU, so it needs, once
+// per network:
+//   1. the Jacobian pattern implied by the Ybus pattern and the bus partition
+//      (blocks H,N,M,L of dense_jacobian, transmission.py:383-407);
+//   2. a fill-reducing symmetric ordering (built-in minimum degree, or the
+//      caller's permutation);
+//   3. the static-pivot L+U pattern (no pivoting: the probe in SURVEY.md 0.2
+//      shows identical Newton flags/iterations to the reference);
+//   4. per-slot assembly descriptors (which Ybus entry and which derivative
+//      block feeds each LU slot; fill slots start at zero);
+//   5. the Crout schedule: for every LU slot (p,c), the ordered list of
+//      (l_pm, u_mc) slot pairs whose products are subtracted from a_pc.
+// Everything here is plain C++; the device consumes the flat arrays.
+
+#include "nr_symbolic.h"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace acpf {
+
+namespace {
+
+// Eliminate the graph in `order` (or, if order is empty, choose minimum
+// degree with lowest-index tie break). Returns for each elimination step the
+// neighbour set (original node ids) at elimination time = U-part of that row.
+void eliminate(int n, std::vector<std::vector<int>>& adj, std::vector<int>& order,
+               std::vector<std::vector<int>>& upart) {
+  const bool choose = order.empty();
+  std::vector<char> gone(n, 0);
+  std::set<std::pair<int, int>> pq;
+  if (choose) {
+    order.reserve(n);
+    for (int v = 0; v < n; ++v) pq.insert({(int)adj[v].size(), v});
+  }
+  upart.assign(n, {});
+  std::vector<int> merged;
+  for (int k = 0; k < n; ++k) {
+    int v;
+    if (choose) {
+      v = pq.begin()->second;
+      pq.erase(pq.begin());
+      order.push_back(v);
+    } else {
+      v = order[k];
+      if (v < 0 || v >= n || gone[v]) throw std::invalid_argument("perm is not a permutation");
+    }
+    gone[v] = 1;
+    std::vector<int> nb;
+    nb.reserve(adj[v].size());
+    for (int a : adj[v])
+      if (!gone[a]) nb.push_back(a);
+    // nb sorted (adj lists are kept sorted)
+    for (int a : nb) {
+      auto& la = adj[a];
+      if (choose) pq.erase({(int)la.size(), a});
+      merged.clear();
+      merged.reserve(la.size() + nb.size());
+      std::set_union(la.begin(), la.end(), nb.begin(), nb.end(), std::back_inserter(merged));
+      // drop a itself and v, and eliminated nodes
+      la.clear();
+      for (int b : merged)
+        if (b != a && !gone[b]) la.push_back(b);
+      if (choose) pq.insert({(int)la.size(), a});
+    }
+    upart[k] = std::move(nb);
+    adj[v].clear();
+    adj[v].shrink_to_fit();
+  }
+}
+
+}  // namespace
+
+void build_nr_symbolic(NrSymbolic& s, int n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                       int n_theta, const int32_t* theta_block, int n_q, const int32_t* q_block,
+                       const int32_t* perm_in) {
+  s.n_bus = n_bus;
+  s.n_theta = n_theta;
+  s.n_q = n_q;
+  const int nj = n_theta + n_q;
+  s.n_j = nj;
+  if (nj <= 0) throw std::invalid_argument("no unknowns");
+
+  std::vector<int> tpos(n_bus, -1), qpos(n_bus, -1);
+  for (int k = 0; k < n_theta; ++k) {
+    int b = theta_block[k];
+    if (b < 0 || b >= n_bus || tpos[b] >= 0) throw std::invalid_argument("bad theta_block");
+    tpos[b] = k;
+  }
+  for (int k = 0; k < n_q; ++k) {
+    int b = q_block[k];
+    if (b < 0 || b >= n_bus || qpos[b] >= 0) throw std::invalid_argument("bad q_block");
+    if (tpos[b] < 0) throw std::invalid_argument("q_block bus missing from theta_block");
+    qpos[b] = n_theta + k;
+  }
+  // packed unknown -> (bus, kind)
+  std::vector<int> var_bus(nj), var_kind(nj);
+  for (int k = 0; k < n_theta; ++k) var_bus[k] = theta_block[k], var_kind[k] = 0;
+  for (int k = 0; k < n_q; ++k) var_bus[n_theta + k] = q_block[k], var_kind[n_theta + k] = 1;
+
+  // J pattern (structurally symmetric): for unknown r at bus i, every bus j
+  // with Y_ij present, plus j = i always.
+  std::vector<std::vector<int>> adj(nj);
+  s.nnz_y = y_rowptr[n_bus];
+  for (int r = 0; r < nj; ++r) {
+    int i = var_bus[r];
+    auto add_bus = [&](int j) {
+      if (tpos[j] >= 0 && tpos[j] != r) adj[r].push_back(tpos[j]);
+      if (qpos[j] >= 0 && qpos[j] != r) adj[r].push_back(qpos[j]);
+    };
+    add_bus(i);
+    for (int e = y_rowptr[i]; e < y_rowptr[i + 1]; ++e) {
+      int j = y_col[e];
+      if (j < 0 || j >= n_bus) throw std::invalid_argument("Ybus column out of range");
+      add_bus(j);
+    }
+    std::sort(adj[r].begin(), adj[r].end());
+    adj[r].erase(std::unique(adj[r].begin(), adj[r].end()), adj[r].end());
+  }
+  int64_t nnzj = nj;
+  for (int r = 0; r < nj; ++r) nnzj += (int64_t)adj[r].size();
+  s.nnz_j = nnzj;
+
+  std::vector<int> order;
+  if (perm_in) order.assign(perm_in, perm_in + nj);
+  std::vector<std::vector<int>> upart;
+  eliminate(nj, adj, order, upart);
+  s.perm.assign(order.begin(), order.end());
+  s.ipos.assign(nj, -1);
+  for (int k = 0; k < nj; ++k) s.ipos[order[k]] = k;
+
+  // rows in elimination order: U-part(k) in new positions; L-part by transpose
+  std::vector<std::vector<int>> U(nj), L(nj);
+  for (int k = 0; k < nj; ++k) {
+    for (int a : upart[k]) U[k].push_back(s.ipos[a]);
+    std::sort(U[k].begin(), U[k].end());
+    for (int c : U[k]) L[c].push_back(k);  // k ascending => L[c] sorted
+  }
+  s.etree_height = 0;
+  {
+    std::vector<int> h(nj, 0);
+    for (int k = 0; k < nj; ++k) {
+      if (!U[k].empty()) {
+        int par = U[k][0];
+        h[par] = std::max(h[par], h[k] + 1);
+      }
+      s.etree_height = std::max(s.etree_height, h[k] + 1);
+    }
+  }
+
+  // LU CSR (row-major, columns ascending: L-part, diag, U-part)
+  s.rowptr.assign(nj + 1, 0);
+  for (int p = 0; p < nj; ++p) s.rowptr[p + 1] = s.rowptr[p] + L[p].size() + 1 + U[p].size();
+  const int64_t nslots = s.rowptr[nj];
+  s.nnz_lu = nslots;
+  s.col.resize(nslots);
+  s.diag.resize(nj);
+  for (int p = 0; p < nj; ++p) {
+    int64_t t = s.rowptr[p];
+    for (int m : L[p]) s.col[t++] = m;
+    s.diag[p] = t;
+    s.col[t++] = p;
+    for (int c : U[p]) s.col[t++] = c;
+  }
+
+  // assembly descriptors: slot (p,c) = J[perm[p]][perm[c]]
+  s.row_bus.resize(nj);
+  s.row_kind.resize(nj);
+  s.slot_ynz.assign(nslots, -2);
+  s.slot_jbus.assign(nslots, 0);
+  s.slot_type.assign(nslots, 0);
+  std::vector<int64_t> where(nj, -1);
+  for (int p = 0; p < nj; ++p) {
+    int r = s.perm[p];
+    int i = var_bus[r];
+    s.row_bus[p] = i;
+    s.row_kind[p] = var_kind[r];
+    for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
+    auto put = [&](int j, int e) {
+      // unknowns at bus j: theta (kind 0), V (kind 1)
+      for (int kind = 0; kind < 2; ++kind) {
+        int var = kind == 0 ? tpos[j] : qpos[j];
+        if (var < 0) continue;
+        int64_t t = where[s.ipos[var]];
+        if (t < 0) throw std::logic_error("Jacobian entry missing from LU pattern");
+        s.slot_ynz[t] = e;
+        s.slot_jbus[t] = j;
+        s.slot_type[t] = (uint8_t)(kind | (var_kind[r] << 1) | ((i == j) << 2));
+      }
+    };
+    put(i, -1);  // diagonal bus block, y = 0 unless Y_ii present (below)
+    for (int e = y_rowptr[i]; e < y_rowptr[i + 1]; ++e) put(y_col[e], e);
+    for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = -1;
+  }
+  for (int64_t t = 0; t < nslots; ++t)
+    if (s.slot_ynz[t] == -2) s.slot_type[t] = 8;  // fill
+
+  // Crout schedule
+  s.pair_ptr.assign(nslots + 1, 0);
+  s.pair_l.clear();
+  s.pair_u.clear();
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> lists;
+  for (int p = 0; p < nj; ++p) {
+    const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
+    lists.assign(r1 - r0, {});
+    for (int64_t t = r0; t < r1; ++t) where[s.col[t]] = t;
+    for (int64_t tl = r0; tl < s.diag[p]; ++tl) {
+      int m = s.col[tl];
+      for (int64_t tu = s.diag[m] + 1; tu < s.rowptr[m + 1]; ++tu) {
+        int c = s.col[tu];
+        int64_t tt = where[c];
+        if (tt < 0) throw std::logic_error("symbolic fill incomplete");
+        lists[tt - r0].push_back({(int32_t)tl, (int32_t)tu});
+      }
+    }
+    for (int64_t t = r0; t < r1; ++t) {
+      where[s.col[t]] = -1;
+      for (auto& pr : lists[t - r0]) {
+        s.pair_l.push_back(pr.first);
+        s.pair_u.push_back(pr.second);
+      }
+      s.pair_ptr[t + 1] = (int64_t)s.pair_l.size();
+    }
+  }
+  s.n_pairs = (int64_t)s.pair_l.size();
+  if (nslots > INT32_MAX || s.n_pairs > INT32_MAX)
+    throw std::length_error("factor too large for 32-bit slot indices");
+}
+
+}  // namespace acpf

@@ -1,0 +1,502 @@
+// Fused Z-Bus fixed point on sm_100a FP64 tensor cores (DMMA).
+//
+// Reference loop (distribution.py:653-687): v = v0; repeat
+//   i = current_injection(v)                  (:573-610)
+//   v = Z i + v0                              (:673, z_apply :423-425)
+//   delta = | sum|v| - sum|v_prev| |  <= tol ? (:674-679)
+// then the certificate ||v - (Z i(v) + v0)||inf    (:613-621).
+//
+// i(v) is non-zero only on the load-touched phases l, so each sweep is the
+// complex GEMM  V[n x NT] = Z[:, l] (n x |l|) * I_l (|l| x NT) + v0 over a
+// tile of NT scenarios. Real/imag split:
+//   Vr = Zr Ir - Zi Ii,  Vi = Zr Ii + Zi Ir
+// on mma.sync.m8n8k4.f64 (DMMA; sm_100a has no tcgen05 kind::f64).
+//
+// One CTA owns a tile of NT scenarios for its whole life (all sweeps + the
+// certificate), so nothing but the final v ever leaves the SM:
+//   - Z[:, l] (2.4 MB for EULV, L2-resident) streams through shared memory
+//     in 64-row stages by cp.async.bulk (TMA bulk engine) + mbarrier,
+//     double buffered, pre-swizzled on the host into DMMA fragment order so
+//     every fragment load is one conflict-free LDS.64 per lane;
+//   - I_l lives in shared memory in B-fragment order, rebuilt every sweep by
+//     the column-owner thread from v at the load rows (wye then delta, in
+//     the reference accumulation order), with the voltage-floor checks;
+//   - the epilogue adds v0, writes v of still-running scenarios, and reduces
+//     |v| per column in a fixed order (deterministic; identical for every
+//     column, so results do not depend on the tile position or batch size);
+//   - converged scenarios freeze (their v is not overwritten), exactly like
+//     the reference returning the iterate at which delta <= tol.
+
+#include "acpf_internal.cuh"
+
+namespace acpf {
+
+namespace {
+
+constexpr int kThreads = 256;   // 8 warps: 4 row-pairs x 2 column halves
+constexpr int kMaxKsPerStage = 16;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// reference-style complex quotient s / v (scaled, no overflow for |v| ~ 1)
+__device__ __forceinline__ double2 cdiv(double2 s, double2 v) {
+  if (fabs(v.x) >= fabs(v.y)) {
+    const double r = v.y / v.x, den = v.x + v.y * r;
+    return make_double2((s.x + s.y * r) / den, (s.y - s.x * r) / den);
+  }
+  const double r = v.x / v.y, den = v.x * r + v.y;
+  return make_double2((s.x * r + s.y) / den, (s.y * r - s.x) / den);
+}
+
+// NaN-propagating max (np.max semantics)
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return (isnan(a) || a > b) ? a : b;
+}
+
+enum PassMode { kIterate = 0, kCert = 1, kMag0 = 2 };
+
+template <int NT>
+struct Smem {
+  static constexpr int kCgWarp = NT / 16;   // column groups per warp
+};
+
+template <int NT>
+__device__ __forceinline__ int ifrag_index(int k, int col) {
+  // B fragment (k x col), layout [kstep][cg][comp][lane], lane = (col%8)*4 + k%4
+  return (((k >> 2) * (NT / 8) + (col >> 3)) * 2) * 32 + ((col & 7) << 2) + (k & 3);
+}
+
+struct ZbTileState {
+  double* colsum;  // [NT]
+  double* red;     // [4][NT]
+  int* run;        // [NT] 1 = running (writes allowed in an iterate pass)
+  int* cert;       // [NT] 1 = needs the certificate pass
+};
+
+// One sweep over all Z stages for the current tile.
+template <int NT, int MODE>
+__device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t tile_col0,
+                        double* zs, const double* isf, uint64_t* bars, uint32_t& phase_bits,
+                        ZbTileState st) {
+  constexpr int CGW = Smem<NT>::kCgWarp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rp = warp & 3, ch = warp >> 2;
+  const int ksteps = m.kpad >> 2;
+  const int n_kc = (ksteps + kMaxKsPerStage - 1) / kMaxKsPerStage;
+  const int n_stage = m.n_rb * n_kc;
+  const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
+
+  auto stage_src = [&](int sidx, const double*& src, uint32_t& bytes) {
+    const int rb = sidx / n_kc, kc = sidx % n_kc;
+    const int ks0 = kc * kMaxKsPerStage;
+    const int nks = min(kMaxKsPerStage, ksteps - ks0);
+    src = m.zfrag + ((size_t)rb * ksteps + ks0) * 512;
+    bytes = (uint32_t)nks * 512 * 8;
+  };
+  auto issue = [&](int sidx) {
+    const double* src;
+    uint32_t bytes;
+    stage_src(sidx, src, bytes);
+    double* dst = zs + (sidx & 1) * stage_doubles;
+    uint64_t* bar = bars + (sidx & 1);
+    mbar_expect_tx(bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      const uint32_t chunk = min(32768u, bytes - off);
+      bulk_g2s(reinterpret_cast<char*>(dst) + off, reinterpret_cast<const char*>(src) + off, chunk,
+               bar);
+    }
+  };
+
+  if (tid == 0) {
+    issue(0);
+    if (n_stage > 1) issue(1);
+  }
+
+  double cr[2][CGW][2], ci[2][CGW][2];
+  for (int sidx = 0; sidx < n_stage; ++sidx) {
+    const int rb = sidx / n_kc, kc = sidx % n_kc;
+    const int buf = sidx & 1;
+    if (kc == 0) {
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < CGW; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+    }
+    mbar_wait(bars + buf, (phase_bits >> buf) & 1u);
+    phase_bits ^= (1u << buf);
+    const double* zb = zs + buf * stage_doubles;
+    const int ks0 = kc * kMaxKsPerStage;
+    const int nks = min(kMaxKsPerStage, ksteps - ks0);
+    for (int ks = 0; ks < nks; ++ks) {
+      double ar[2], ai[2], br[CGW], bi[CGW];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int rg = rp * 2 + a;
+        ar[a] = zb[((ks * 8 + rg) * 2 + 0) * 32 + lane];
+        ai[a] = zb[((ks * 8 + rg) * 2 + 1) * 32 + lane];
+      }
+#pragma unroll
+      for (int b = 0; b < CGW; ++b) {
+        const int cg = ch * CGW + b;
+        br[b] = isf[(((ks0 + ks) * (NT / 8) + cg) * 2 + 0) * 32 + lane];
+        bi[b] = isf[(((ks0 + ks) * (NT / 8) + cg) * 2 + 1) * 32 + lane];
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const double nai = -ai[a];
+#pragma unroll
+        for (int b = 0; b < CGW; ++b) {
+          dmma(cr[a][b][0], cr[a][b][1], ar[a], br[b]);
+          dmma(cr[a][b][0], cr[a][b][1], nai, bi[b]);
+          dmma(ci[a][b][0], ci[a][b][1], ar[a], bi[b]);
+          dmma(ci[a][b][0], ci[a][b][1], ai[a], br[b]);
+        }
+      }
+    }
+    if (kc == n_kc - 1) {
+      // ---- epilogue for row block rb
+      double part[CGW][2];
+#pragma unroll
+      for (int b = 0; b < CGW; ++b) part[b][0] = part[b][1] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int row = rb * kZbRows + (rp * 2 + a) * 8 + (lane >> 2);
+        const double2 v0 = m.v0[row];
+        const bool in = row < m.n;
+#pragma unroll
+        for (int b = 0; b < CGW; ++b) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = (ch * CGW + b) * 8 + 2 * (lane & 3) + j;
+            const double vr = cr[a][b][j] + v0.x, vi = ci[a][b][j] + v0.y;
+            double contrib = 0.0;
+            if (MODE == kIterate) {
+              if (in) {
+                contrib = sqrt(vr * vr + vi * vi);
+                if (st.run[col]) io.v_out[(tile_col0 + col) * m.n + row] = make_double2(vr, vi);
+              }
+              part[b][j] = part[b][j] + contrib;
+            } else if (MODE == kMag0) {
+              if (in) contrib = sqrt(vr * vr + vi * vi);
+              part[b][j] = part[b][j] + contrib;
+            } else {  // certificate: |v_final - (Z i(v_final) + v0)|
+              if (in && st.cert[col]) {
+                const double2 vf = io.v_out[(tile_col0 + col) * m.n + row];
+                const double dr = vf.x - vr, di = vf.y - vi;
+                contrib = sqrt(dr * dr + di * di);
+              }
+              part[b][j] = nanmax(part[b][j], contrib);
+            }
+          }
+        }
+      }
+      // reduce over the 8 row lanes (lane bits 2..4), fixed order
+#pragma unroll
+      for (int b = 0; b < CGW; ++b)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double x = part[b][j];
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, x, off);
+            x = (MODE == kCert) ? nanmax(x, o) : x + o;
+          }
+          if (lane < 4) st.red[rp * NT + (ch * CGW + b) * 8 + 2 * lane + j] = x;
+        }
+      __syncthreads();
+      if (tid < NT) {
+        const double* r = st.red;
+        if (MODE == kCert) {
+          st.colsum[tid] = nanmax(nanmax(nanmax(st.colsum[tid], r[tid]), r[NT + tid]),
+                                  nanmax(r[2 * NT + tid], r[3 * NT + tid]));
+        } else {
+          st.colsum[tid] = st.colsum[tid] + (((r[tid] + r[NT + tid]) + r[2 * NT + tid]) + r[3 * NT + tid]);
+        }
+      }
+    }
+    __syncthreads();  // everyone is done with zs[buf] (and red)
+    if (tid == 0 && sidx + 2 < n_stage) issue(sidx + 2);
+  }
+}
+
+// Column-owner work: build I_l for column `col` from v at the load rows.
+// Returns floor slot (>= 0) on a voltage-floor violation, else -1.
+template <int NT>
+__device__ int zb_injection(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t scen, int col,
+                            bool from_v0, double* isf) {
+  for (int k = 0; k < m.kpad; ++k) {
+    isf[ifrag_index<NT>(k, col) + 0] = 0.0;
+    isf[ifrag_index<NT>(k, col) + 32] = 0.0;
+  }
+  auto vat = [&](int lcol) -> double2 {
+    const int row = m.l_row[lcol];
+    return from_v0 ? m.v0[row] : io.v_out[scen * m.n + row];
+  };
+  // floor checks in the reference order (distribution.py:583-606)
+  for (int k = 0; k < m.n_wye; ++k) {
+    const double2 v = vat(m.wye_l[k]);
+    if (hypot(v.x, v.y) <= m.floor) return k;
+  }
+  for (int k = 0; k < m.n_delta; ++k) {
+    const double2 v = vat(m.dp_l[k]);
+    if (hypot(v.x, v.y) <= m.floor) return m.n_wye + k;
+  }
+  for (int k = 0; k < m.n_delta; ++k) {
+    const double2 v = vat(m.dq_l[k]);
+    if (hypot(v.x, v.y) <= m.floor) return m.n_wye + m.n_delta + k;
+  }
+  for (int k = 0; k < m.n_delta; ++k) {
+    const double2 vp = vat(m.dp_l[k]), vq = vat(m.dq_l[k]);
+    if (hypot(vp.x - vq.x, vp.y - vq.y) <= m.floor) return m.n_wye + 2 * m.n_delta + k;
+  }
+  // wye: i[p] += -conj(s / v_p), in load order (np.add.at)
+  for (int k = 0; k < m.n_wye; ++k) {
+    const int lc = m.wye_l[k];
+    const double2 q = cdiv(io.s_wye[scen * m.n_wye + k], vat(lc));
+    const int idx = ifrag_index<NT>(lc, col);
+    isf[idx] = isf[idx] + (-q.x);
+    isf[idx + 32] = isf[idx + 32] + q.y;
+  }
+  // delta: i_line = conj(s / (v_p - v_q)); i[p] -= i_line (all k), then i[q] += i_line
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int k = 0; k < m.n_delta; ++k) {
+      const double2 vp = vat(m.dp_l[k]), vq = vat(m.dq_l[k]);
+      const double2 q = cdiv(io.s_delta[scen * m.n_delta + k], make_double2(vp.x - vq.x, vp.y - vq.y));
+      const int lc = pass == 0 ? m.dp_l[k] : m.dq_l[k];
+      const int idx = ifrag_index<NT>(lc, col);
+      if (pass == 0) {
+        isf[idx] = isf[idx] + (-q.x);
+        isf[idx + 32] = isf[idx + 32] + q.y;
+      } else {
+        isf[idx] = isf[idx] + q.x;
+        isf[idx + 32] = isf[idx + 32] + (-q.y);
+      }
+    }
+  }
+  return -1;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+    zbus_kernel(ZbDeviceModel m, ZbBatchIO io, double tol, int max_iter, int mag0_mode,
+                double* mag0_out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int ksteps = m.kpad >> 2;
+  const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
+  double* zs = reinterpret_cast<double*>(smem_raw);
+  double* isf = zs + 2 * stage_doubles;
+  double* colsum = isf + (size_t)ksteps * NT * 8;
+  double* red = colsum + NT;
+  double* mag = red + 4 * NT;
+  double* delta = mag + NT;
+  double* resid = delta + NT;
+  int* run = reinterpret_cast<int*>(resid + NT);
+  int* cert = run + NT;
+  int* stat = cert + NT;
+  int* iters = stat + NT;
+  int* fslot = iters + NT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fslot + NT + (NT & 1));
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase_bits = 0;
+  ZbTileState st{colsum, red, run, cert};
+
+  if (mag0_mode) {
+    for (int k = tid; k < ksteps * NT * 8; k += kThreads) isf[k] = 0.0;
+    if (tid < NT) colsum[tid] = 0.0, run[tid] = 0;
+    __syncthreads();
+    zb_pass<NT, kMag0>(m, io, 0, zs, isf, bars, phase_bits, st);
+    if (tid == 0) *mag0_out = colsum[0];
+    return;
+  }
+
+  const int64_t n_tiles = (io.batch + NT - 1) / NT;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t col0 = tile * NT;
+    const int64_t scen = col0 + tid;
+    if (tid < NT) {
+      const bool live = scen < io.batch;
+      run[tid] = live;
+      cert[tid] = 0;
+      stat[tid] = live ? -1 : -2;
+      mag[tid] = m.mag0;
+      delta[tid] = __longlong_as_double(0x7ff0000000000000LL);
+      resid[tid] = 0.0;
+      iters[tid] = 0;
+      fslot[tid] = -1;
+    }
+    // ---- sweeps
+    for (int k = 1; k <= max_iter; ++k) {
+      if (tid < NT) {
+        if (run[tid]) {
+          const int fs = zb_injection<NT>(m, io, scen, tid, k == 1, isf);
+          if (fs >= 0) {
+            run[tid] = 0;
+            stat[tid] = ACPF_ZB_FLOOR;
+            iters[tid] = k;
+            fslot[tid] = fs;
+            resid[tid] = __longlong_as_double(0x7ff0000000000000LL);
+            if (k == 1)
+              for (int r = 0; r < m.n; ++r) io.v_out[scen * m.n + r] = m.v0[r];
+          }
+        }
+        if (!run[tid])
+          for (int q = 0; q < m.kpad; ++q) {
+            isf[ifrag_index<NT>(q, tid)] = 0.0;
+            isf[ifrag_index<NT>(q, tid) + 32] = 0.0;
+          }
+        colsum[tid] = 0.0;
+      }
+      const int any = __syncthreads_or(tid < NT && run[tid]);
+      if (!any) break;
+      zb_pass<NT, kIterate>(m, io, col0, zs, isf, bars, phase_bits, st);
+      if (tid < NT && run[tid]) {
+        const double s = colsum[tid];
+        const double d = fabs(s - mag[tid]);
+        mag[tid] = s;
+        delta[tid] = d;
+        if (d <= tol) {
+          run[tid] = 0;
+          stat[tid] = ACPF_ZB_CONVERGED;
+          iters[tid] = k;
+        } else if (k == max_iter) {
+          run[tid] = 0;
+          stat[tid] = ACPF_ZB_MAX_ITER;
+          iters[tid] = k;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- certificate ||v - (Z i(v) + v0)||inf
+    if (tid < NT) {
+      cert[tid] = 0;
+      colsum[tid] = 0.0;
+      if (stat[tid] == ACPF_ZB_CONVERGED || stat[tid] == ACPF_ZB_MAX_ITER) {
+        const int fs = zb_injection<NT>(m, io, scen, tid, false, isf);
+        if (fs >= 0) {
+          resid[tid] = __longlong_as_double(0x7ff0000000000000LL);
+        } else {
+          cert[tid] = 1;
+        }
+      }
+      if (!cert[tid])
+        for (int q = 0; q < m.kpad; ++q) {
+          isf[ifrag_index<NT>(q, tid)] = 0.0;
+          isf[ifrag_index<NT>(q, tid) + 32] = 0.0;
+        }
+    }
+    const int anyc = __syncthreads_or(tid < NT && cert[tid]);
+    if (anyc) {
+      zb_pass<NT, kCert>(m, io, col0, zs, isf, bars, phase_bits, st);
+      if (tid < NT && cert[tid]) resid[tid] = colsum[tid];
+    }
+    if (tid < NT && scen < io.batch) {
+      if (io.converged) io.converged[scen] = stat[tid] == ACPF_ZB_CONVERGED;
+      if (io.iterations) io.iterations[scen] = iters[tid];
+      if (io.final_delta) io.final_delta[scen] = delta[tid];
+      if (io.residual) io.residual[scen] = resid[tid];
+      if (io.status) io.status[scen] = stat[tid];
+      if (io.floor_slot) io.floor_slot[scen] = fslot[tid];
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT>
+size_t zbus_smem_bytes(int kpad) {
+  const int ksteps = kpad >> 2;
+  const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
+  size_t d = 2 * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + 4 * NT + 3 * NT;
+  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 16 + 16;
+  return bytes;
+}
+
+template <int NT>
+cudaError_t launch_nt(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter,
+                      bool mag0_mode, double* mag0_out, cudaStream_t stream) {
+  const size_t smem = zbus_smem_bytes<NT>(m.kpad);
+  cudaError_t err = cudaFuncSetAttribute(zbus_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+  if (err != cudaSuccess) return err;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = mag0_mode ? 1 : (io.batch + NT - 1) / NT;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  zbus_kernel<NT><<<grid, kThreads, smem, stream>>>(m, io, tol, max_iter, mag0_mode ? 1 : 0, mag0_out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t zbus_frag_doubles(int n_rb, int kpad) { return (size_t)n_rb * (kpad >> 2) * 512; }
+
+// Host: pack Z[:, l] ([n][n_l] interleaved complex) into DMMA A-fragment
+// order: [row block][kstep][row group 0..7][re|im][lane], lane t holds
+// Z[rb*64 + rg*8 + t/4][ks*4 + t%4] (zero padded).
+void zbus_pack_fragments(const double* zl, int n, int n_l, int n_rb, int kpad, double* out) {
+  const int ksteps = kpad >> 2;
+  size_t o = 0;
+  for (int rb = 0; rb < n_rb; ++rb)
+    for (int ks = 0; ks < ksteps; ++ks)
+      for (int rg = 0; rg < 8; ++rg)
+        for (int comp = 0; comp < 2; ++comp)
+          for (int t = 0; t < 32; ++t) {
+            const int row = rb * kZbRows + rg * 8 + (t >> 2);
+            const int k = ks * 4 + (t & 3);
+            out[o++] = (row < n && k < n_l) ? zl[((size_t)row * n_l + k) * 2 + comp] : 0.0;
+          }
+}
+
+cudaError_t launch_zbus(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter,
+                        bool mag0_mode, double* mag0_out, int* launches, cudaStream_t stream) {
+  if (launches) *launches = 1;
+  if (m.kpad <= 64) return launch_nt<64>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
+  return launch_nt<32>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
+}
+
+}  // namespace acpf

@@ -1,0 +1,377 @@
+"""ctypes binding of libacpf.so (include/acpf.h) and the device plans.
+
+This is the only bridge between the host API (reference-shaped dataclasses)
+and the CUDA engine. There is no CPU fallback: if the library or a GPU is
+missing every solve raises :class:`EngineUnavailable`.
+
+Batch buffers may be numpy arrays (host pointers, ``ACPF_HOST_PTRS``: the
+library stages through device memory) or CUDA ``torch`` tensors
+(``ACPF_DEVICE_PTRS``); torch is used for device memory only.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libacpf.so"
+
+ACPF_HOST_PTRS = 0
+ACPF_DEVICE_PTRS = 1
+
+NR_CONVERGED, NR_MAX_ITER, NR_NONFINITE, NR_VMAG_LE0, NR_ZERO_PIVOT = range(5)
+ZB_CONVERGED, ZB_MAX_ITER, ZB_FLOOR = range(3)
+
+EXPORTED = (
+    "acpf_last_error", "acpf_abi_version", "acpf_device_count",
+    "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_plan_info_get", "acpf_nr_plan_structure",
+    "acpf_nr_solve", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
+    "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
+    "acpf_zbus_plan_destroy",
+)
+
+
+class EngineUnavailable(RuntimeError):
+    """libacpf.so missing/unbuildable or no CUDA device: there is no fallback."""
+
+
+class EngineError(RuntimeError):
+    """A C-ABI call returned a negative acpf_status."""
+
+
+class NrPlanInfo(C.Structure):
+    _fields_ = [
+        ("n_bus", C.c_int32), ("n_theta", C.c_int32), ("n_q", C.c_int32), ("n_j", C.c_int32),
+        ("nnz_y", C.c_int32), ("nnz_j", C.c_int32), ("nnz_lu", C.c_int64), ("n_pairs", C.c_int64),
+        ("group", C.c_int32), ("etree_height", C.c_int32),
+        ("workspace_bytes_per_group", C.c_int64),
+    ]
+
+
+_lib = None
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+U32 = C.c_uint32
+D = C.c_double
+
+
+def load_library(path: str | os.PathLike | None = None):
+    """Load (building first if stale and nvcc is present) and type the C-ABI."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    target = Path(path) if path else _LIB_PATH
+    if path is None:
+        try:
+            from . import _build
+            if _build._stale() and Path(_build.NVCC).exists():
+                _build.build()
+        except Exception as exc:  # a stale-but-present library still loads
+            if not target.exists():
+                raise EngineUnavailable(f"cannot build {target}: {exc}") from exc
+    if not target.exists():
+        raise EngineUnavailable(f"{target} not built (run __graft_entry__.build())")
+    lib = C.CDLL(str(target))
+    sig = {
+        "acpf_last_error": (C.c_char_p, []),
+        "acpf_abi_version": (I32, []),
+        "acpf_device_count": (I32, []),
+        "acpf_nr_plan_create": (I32, [I32, I32, P, P, P, P, I32, P, I32, P, P, P, P, P]),
+        "acpf_nr_analyze": (I32, [I32, P, P, I32, P, I32, P, P, P]),
+        "acpf_nr_plan_info_get": (I32, [P, P]),
+        "acpf_nr_plan_structure": (I32, [P, P, P]),
+        "acpf_nr_solve": (I32, [P, I64, P, P, D, I32, P, P, P, P, P, P, U32, P]),
+        "acpf_nr_last_timing": (I32, [P, P, P]),
+        "acpf_nr_plan_destroy": (I32, [P]),
+        "acpf_zbus_plan_create": (I32, [I32, I32, I32, P, P, P, I32, P, I32, P, P, D, P]),
+        "acpf_zbus_solve": (I32, [P, I64, P, P, D, I32, P, P, P, P, P, P, P, U32, P]),
+        "acpf_zbus_last_timing": (I32, [P, P, P]),
+        "acpf_zbus_plan_destroy": (I32, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.acpf_last_error().decode(errors="replace") if _lib else ""
+        raise EngineError(f"acpf status {rc}: {msg}")
+
+
+def require_device(device: int = 0) -> None:
+    lib = load_library()
+    n = lib.acpf_device_count()
+    if n <= device:
+        raise EngineUnavailable(f"no CUDA device {device} (found {n}); the engine has no CPU path")
+
+
+def _ptr(a) -> int | None:
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("arrays passed to the engine must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensors passed to the engine must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(a)!r}")
+
+
+def _is_device(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+def nr_analyze(y_csr, theta_block, q_block, perm=None) -> dict:
+    """Host-only symbolic analysis (no GPU): structure sizes for a network."""
+    lib = load_library()
+    y = y_csr.tocsr()
+    y.sort_indices()
+    rowptr = np.ascontiguousarray(y.indptr, dtype=np.int32)
+    col = np.ascontiguousarray(y.indices, dtype=np.int32)
+    tb = np.ascontiguousarray(theta_block, dtype=np.int32)
+    qb = np.ascontiguousarray(q_block, dtype=np.int32)
+    pm = None if perm is None else np.ascontiguousarray(perm, dtype=np.int32)
+    info = NrPlanInfo()
+    _check(lib.acpf_nr_analyze(y.shape[0], _ptr(rowptr), _ptr(col), tb.size, _ptr(tb), qb.size,
+                               _ptr(qb), _ptr(pm), C.byref(info)))
+    return {f: getattr(info, f) for f, _ in NrPlanInfo._fields_}
+
+
+# ---------------------------------------------------------------------------
+# Newton plans
+# ---------------------------------------------------------------------------
+
+
+class NrPlan:
+    """Device plan for one transmission network (acpf_nr_plan_create)."""
+
+    def __init__(self, y_csr, theta_block, q_block, theta_init, vmag_init, device: int = 0,
+                 perm=None):
+        require_device(device)
+        lib = load_library()
+        y = y_csr.tocsr()
+        y.sort_indices()
+        self.n_bus = y.shape[0]
+        rowptr = np.ascontiguousarray(y.indptr, dtype=np.int32)
+        col = np.ascontiguousarray(y.indices, dtype=np.int32)
+        yre = np.ascontiguousarray(y.data.real, dtype=np.float64)
+        yim = np.ascontiguousarray(y.data.imag, dtype=np.float64)
+        tb = np.ascontiguousarray(theta_block, dtype=np.int32)
+        qb = np.ascontiguousarray(q_block, dtype=np.int32)
+        th0 = np.ascontiguousarray(theta_init, dtype=np.float64)
+        vm0 = np.ascontiguousarray(vmag_init, dtype=np.float64)
+        pm = None if perm is None else np.ascontiguousarray(perm, dtype=np.int32)
+        h = P()
+        _check(lib.acpf_nr_plan_create(device, self.n_bus, _ptr(rowptr), _ptr(col), _ptr(yre),
+                                       _ptr(yim), tb.size, _ptr(tb), qb.size, _ptr(qb), _ptr(th0),
+                                       _ptr(vm0), _ptr(pm), C.byref(h)))
+        self._h = h
+        self.device = device
+        self.n_theta, self.n_q = int(tb.size), int(qb.size)
+        info = NrPlanInfo()
+        _check(lib.acpf_nr_plan_info_get(h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in NrPlanInfo._fields_}
+
+    def structure(self):
+        perm = np.empty(self.info["n_j"], dtype=np.int32)
+        rp = np.empty(self.info["n_j"] + 1, dtype=np.int64)
+        _check(_lib.acpf_nr_plan_structure(self._h, _ptr(perm), _ptr(rp)))
+        return perm, rp
+
+    def solve(self, p_spec, q_spec, tol: float, max_newton: int, out: dict | None = None,
+              stream=None) -> dict:
+        """Solve a stacked batch. numpy in -> numpy out (host staging inside
+        the library); CUDA tensors in -> CUDA tensors out (device pointers)."""
+        dev = _is_device(p_spec)
+        b = int(p_spec.shape[0])
+        if out is None:
+            out = self.alloc_outputs(b, like=p_spec if dev else None)
+        flags = ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS
+        _check(_lib.acpf_nr_solve(
+            self._h, b, _ptr(p_spec), _ptr(q_spec), float(tol), int(max_newton),
+            _ptr(out["theta"]), _ptr(out["vmag"]), _ptr(out["converged"]),
+            _ptr(out["iterations"]), _ptr(out["final_mismatch_inf"]), _ptr(out["status"]),
+            flags, _stream_ptr(stream)))
+        return out
+
+    def alloc_outputs(self, b: int, like=None) -> dict:
+        if like is not None:
+            import torch
+            kw = dict(device=like.device)
+            return {
+                "theta": torch.empty((b, self.n_bus), dtype=torch.float64, **kw),
+                "vmag": torch.empty((b, self.n_bus), dtype=torch.float64, **kw),
+                "converged": torch.empty(b, dtype=torch.uint8, **kw),
+                "iterations": torch.empty(b, dtype=torch.int32, **kw),
+                "final_mismatch_inf": torch.empty(b, dtype=torch.float64, **kw),
+                "status": torch.empty(b, dtype=torch.int32, **kw),
+            }
+        return {
+            "theta": np.empty((b, self.n_bus)), "vmag": np.empty((b, self.n_bus)),
+            "converged": np.empty(b, dtype=np.uint8), "iterations": np.empty(b, dtype=np.int32),
+            "final_mismatch_inf": np.empty(b), "status": np.empty(b, dtype=np.int32),
+        }
+
+    def last_timing(self) -> tuple:
+        ms, n = D(), I32()
+        _check(_lib.acpf_nr_last_timing(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.acpf_nr_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+# ---------------------------------------------------------------------------
+# Z-Bus plans
+# ---------------------------------------------------------------------------
+
+
+class ZbusPlan:
+    """Device plan for one feeder (acpf_zbus_plan_create)."""
+
+    def __init__(self, model, device: int = 0):
+        require_device(device)
+        lib = load_library()
+        self.n = int(model.n)
+        self.n_wye = int(model.wye_idx.size)
+        self.n_delta = int(model.delta_p.size)
+        cols = np.ascontiguousarray(model.load_cols, dtype=np.int32)
+        zl = np.ascontiguousarray(model.z_load, dtype=np.complex128)
+        v0 = np.ascontiguousarray(model.v0, dtype=np.complex128)
+        wi = np.ascontiguousarray(model.wye_idx, dtype=np.int32)
+        dp = np.ascontiguousarray(model.delta_p, dtype=np.int32)
+        dq = np.ascontiguousarray(model.delta_q, dtype=np.int32)
+        h = P()
+        _check(lib.acpf_zbus_plan_create(device, self.n, cols.size, _ptr(cols), _ptr(zl), _ptr(v0),
+                                         wi.size, _ptr(wi), dp.size, _ptr(dp), _ptr(dq),
+                                         float(model.voltage_floor), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def alloc_outputs(self, b: int, like=None) -> dict:
+        if like is not None:
+            import torch
+            kw = dict(device=like.device)
+            return {
+                "v": torch.empty((b, self.n), dtype=torch.complex128, **kw),
+                "converged": torch.empty(b, dtype=torch.uint8, **kw),
+                "iterations": torch.empty(b, dtype=torch.int32, **kw),
+                "final_delta": torch.empty(b, dtype=torch.float64, **kw),
+                "residual_inf": torch.empty(b, dtype=torch.float64, **kw),
+                "status": torch.empty(b, dtype=torch.int32, **kw),
+                "floor_slot": torch.empty(b, dtype=torch.int32, **kw),
+            }
+        return {
+            "v": np.empty((b, self.n), dtype=np.complex128),
+            "converged": np.empty(b, dtype=np.uint8), "iterations": np.empty(b, dtype=np.int32),
+            "final_delta": np.empty(b), "residual_inf": np.empty(b),
+            "status": np.empty(b, dtype=np.int32), "floor_slot": np.empty(b, dtype=np.int32),
+        }
+
+    def solve(self, s_wye, s_delta, tol: float, max_iter: int, out: dict | None = None,
+              stream=None) -> dict:
+        dev = _is_device(s_wye)
+        b = int(s_wye.shape[0])
+        if out is None:
+            out = self.alloc_outputs(b, like=s_wye if dev else None)
+        flags = ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS
+        _check(_lib.acpf_zbus_solve(
+            self._h, b, _ptr(s_wye) if self.n_wye else None,
+            _ptr(s_delta) if self.n_delta else None, float(tol), int(max_iter), _ptr(out["v"]),
+            _ptr(out["converged"]), _ptr(out["iterations"]), _ptr(out["final_delta"]),
+            _ptr(out["residual_inf"]), _ptr(out["status"]), _ptr(out["floor_slot"]), flags,
+            _stream_ptr(stream)))
+        return out
+
+    def last_timing(self) -> tuple:
+        ms, n = D(), I32()
+        _check(_lib.acpf_zbus_last_timing(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.acpf_zbus_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def zbus_plan_for(model, device: int | None = None) -> ZbusPlan:
+    device = 0 if device is None else device
+    plan = model._plans.get(device)
+    if plan is None:
+        plan = ZbusPlan(model, device)
+        model._plans[device] = plan
+    return plan
+
+
+def zbus_solve_arrays(model, s_wye, s_delta, tol, max_iter, device=None) -> dict:
+    plan = zbus_plan_for(model, device)
+    sw = np.ascontiguousarray(s_wye, dtype=np.complex128)
+    sd = np.ascontiguousarray(s_delta, dtype=np.complex128)
+    if sd.size == 0:
+        sd = np.zeros((sw.shape[0], 0), dtype=np.complex128)
+    return plan.solve(sw, sd, tol, max_iter)
+
+
+def zbus_floor_message(model, v: np.ndarray, slot: int) -> str:
+    """Reconstruct the reference VoltageFloorError text (distribution.py:45-50)."""
+    from .distribution import _floor_label
+    nw, nd = model.wye_idx.size, model.delta_p.size
+    if slot < nw:
+        kind, k, mag = "wye", slot, abs(v[model.wye_idx[slot]])
+    elif slot < nw + nd:
+        k = slot - nw
+        kind, mag = "p", abs(v[model.delta_p[k]])
+    elif slot < nw + 2 * nd:
+        k = slot - nw - nd
+        kind, mag = "q", abs(v[model.delta_q[k]])
+    else:
+        k = slot - nw - 2 * nd
+        kind, mag = "pq", abs(v[model.delta_p[k]] - v[model.delta_q[k]])
+    label = _floor_label(model, kind, k)
+    return f"voltage magnitude {float(mag):.3e} below floor at node-phase {label}"
+
+
+def zbus_results(model, out: dict) -> list:
+    from .distribution import FixedPointResult
+    res = []
+    for k in range(out["v"].shape[0]):
+        v = out["v"][k].copy()
+        st = int(out["status"][k])
+        diag = zbus_floor_message(model, v, int(out["floor_slot"][k])) if st == ZB_FLOOR else None
+        res.append(FixedPointResult(
+            v=v, converged=bool(out["converged"][k]), iterations=int(out["iterations"][k]),
+            final_delta=float(out["final_delta"][k]), residual_inf=float(out["residual_inf"][k]),
+            diagnostic=diag))
+    return res
+
+
+@dataclass
+class Timing:
+    kernel_ms: float
+    launches: int

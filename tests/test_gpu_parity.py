@@ -1,0 +1,119 @@
+"""GPU parity: the CUDA path vs the reference's golden vectors (tests/golden).
+
+Bar (BASELINE.json north star): identical convergence flags and iteration
+counts; |dVm| <= 1e-8 p.u. and |dtheta| <= 1e-8 rad (Z-Bus: |dv| <= 1e-8 on
+the complex node-phase voltage); final mismatch/residual below the
+reference tolerance. All calls go through the C-ABI (libacpf.so).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2605_14103_b200 as pf
+from paper_2605_14103_b200 import engine
+from paper_2605_14103_b200.fixtures import load_distribution, load_transmission
+
+pytestmark = pytest.mark.gpu
+
+TOL_V = 1e-8
+TOL_TH = 1e-8
+
+TX = {"case14": "case14", "case118": "case118", "case1354": "case1354pegase", "gb2224": "gb2224"}
+ZB = {"ieee13": "ieee13", "ieee123": "ieee123", "eulv": "eulv"}
+
+
+@pytest.fixture(scope="module")
+def tx_models():
+    return {k: pf.build_transmission_model(load_transmission(v)) for k, v in TX.items()}
+
+
+@pytest.fixture(scope="module")
+def zb_models():
+    return {k: pf.build_zbus_model(load_distribution(v)) for k, v in ZB.items()}
+
+
+@pytest.mark.parametrize("tag", list(TX))
+def test_nr_matches_reference(tag, tx_models, golden):
+    g = golden(f"nr_{tag}")
+    model = tx_models[tag]
+    out = model.plan().solve(np.ascontiguousarray(g["p_spec"]), np.ascontiguousarray(g["q_spec"]),
+                             1e-8, 20)
+    np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
+    np.testing.assert_array_equal(out["iterations"], g["iterations"])
+    assert (out["final_mismatch_inf"] <= 1e-8).all()
+    if "theta" in g:
+        assert np.abs(out["theta"] - g["theta"]).max() <= TOL_TH
+        assert np.abs(out["vmag"] - g["vmag"]).max() <= TOL_V
+
+
+@pytest.mark.parametrize("tag", list(TX))
+def test_nr_base_and_infeasible(tag, tx_models, golden):
+    g = golden(f"nr_{tag}")
+    model = tx_models[tag]
+    r = pf.newton_solve(model)
+    assert r.converged and r.iterations == int(g["base_iterations"])
+    assert np.abs(r.state.theta - g["base_theta"]).max() <= TOL_TH
+    assert np.abs(r.state.vmag - g["base_vmag"]).max() <= TOL_V
+    sc = pf.base_scenario(model.net, model.part)
+    h = pf.newton_solve(model, pf.TransmissionScenario(50 * sc.p_spec, 50 * sc.q_spec))
+    assert h.converged == bool(g["huge_converged"])
+    assert h.iterations == int(g["huge_iterations"])
+    assert (h.diagnostic or "") == str(g["huge_diagnostic"])
+
+
+def test_nr_pinned_entries_bit_exact(tx_models):
+    model = tx_models["case118"]
+    r = pf.newton_solve(model)
+    for i in model.part.slack:
+        assert r.state.theta[i] == model.net.buses[i].theta_set
+        assert r.state.vmag[i] == model.net.buses[i].v_set
+    for i in model.part.pv:
+        assert r.state.vmag[i] == model.net.buses[i].v_set
+
+
+def test_nr_batch_position_independent(tx_models, golden):
+    g = golden("nr_case118")
+    model = tx_models["case118"]
+    p, q = g["p_spec"], g["q_spec"]
+    perm = np.random.default_rng(3).permutation(p.shape[0])
+    a = model.plan().solve(np.ascontiguousarray(p), np.ascontiguousarray(q), 1e-8, 20)
+    b = model.plan().solve(np.ascontiguousarray(p[perm]), np.ascontiguousarray(q[perm]), 1e-8, 20)
+    np.testing.assert_array_equal(a["theta"][perm], b["theta"])
+    np.testing.assert_array_equal(a["vmag"][perm], b["vmag"])
+
+
+@pytest.mark.parametrize("tag", list(ZB))
+def test_zbus_matches_reference(tag, zb_models, golden):
+    g = golden(f"zb_{tag}")
+    model = zb_models[tag]
+    out = engine.zbus_solve_arrays(model, g["s_wye"], g["s_delta"], 1e-9, 100)
+    np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
+    np.testing.assert_array_equal(out["iterations"], g["iterations"])
+    kv = g["v"].shape[0]
+    assert np.abs(out["v"][:kv] - g["v"]).max() <= TOL_V
+    assert (out["final_delta"][g["converged"]] <= 1e-9).all()
+    assert (out["residual_inf"] <= 1e-6).all()
+
+
+def test_zbus_noload_and_heavy(zb_models, golden):
+    g = golden("zb_ieee13")
+    model = zb_models["ieee13"]
+    r = pf.zbus_iterate(model, pf.DistributionScenario(np.zeros_like(model.wye_s),
+                                                       np.zeros_like(model.delta_s)))
+    assert r.converged and r.iterations == int(g["noload_iterations"]) == 1
+    np.testing.assert_array_equal(r.v, model.v0)
+    h = pf.zbus_iterate(model, pf.DistributionScenario(model.wye_s * 60.0, model.delta_s * 60.0))
+    assert h.converged == bool(g["heavy_converged"])
+    assert h.iterations == int(g["heavy_iterations"])
+    assert (h.diagnostic or "") == str(g["heavy_diagnostic"])
+
+
+def test_zbus_batch_position_independent(zb_models, golden):
+    g = golden("zb_ieee13")
+    model = zb_models["ieee13"]
+    sw, sd = g["s_wye"][:300], g["s_delta"][:300]
+    perm = np.random.default_rng(5).permutation(300)
+    a = engine.zbus_solve_arrays(model, sw, sd, 1e-9, 100)
+    b = engine.zbus_solve_arrays(model, sw[perm], sd[perm], 1e-9, 100)
+    np.testing.assert_array_equal(a["v"][perm], b["v"])
+    np.testing.assert_array_equal(a["iterations"][perm], b["iterations"])
