@@ -88,6 +88,7 @@ using namespace acpf;
 struct acpf_nr_plan {
   int device = 0;
   NrSymbolic sym;
+  NrSchedule sch;
   NrDeviceModel dm{};
   DevArena model;
   DevArena work;
@@ -114,7 +115,7 @@ struct acpf_zbus_plan {
   int last_launches = 0;
 };
 
-static void fill_info(const NrSymbolic& s, acpf_nr_plan_info* info) {
+static void fill_info(const NrSymbolic& s, acpf_nr_plan_info* info, int64_t ws_bytes = -1) {
   info->n_bus = s.n_bus;
   info->n_theta = s.n_theta;
   info->n_q = s.n_q;
@@ -126,7 +127,8 @@ static void fill_info(const NrSymbolic& s, acpf_nr_plan_info* info) {
   info->group = kGroup;
   info->etree_height = s.etree_height;
   info->workspace_bytes_per_group =
-      (int64_t)kGroup * 8 * (s.nnz_lu + 3 * (int64_t)s.n_j + 8 * (int64_t)s.n_bus);
+      ws_bytes >= 0 ? ws_bytes
+                    : (int64_t)kGroup * 8 * (s.nnz_lu + 3 * (int64_t)s.n_j + 9 * (int64_t)s.n_bus);
 }
 
 extern "C" {
@@ -163,7 +165,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     return ACPF_ENOMEM;
   }
   try {
-    build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+    NrSymbolic first;
+    build_nr_symbolic(first, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+    const std::vector<int32_t> lperm = level_sorted_perm(first);
+    build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block,
+                      lperm.data());
+    build_nr_schedule(p->sym, y_rowptr, y_re, y_im, (int)env_int("ACPF_NR_CAP", 320), p->sch);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;
@@ -172,6 +179,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   p->device = device;
   DeviceGuard dg(device);
   const NrSymbolic& s = p->sym;
+  const NrSchedule& sc = p->sch;
   const int nj = s.n_j;
   const int64_t nnz = y_rowptr[n_bus];
   std::vector<double2> yv(nnz);
@@ -179,14 +187,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   std::vector<int32_t> tpos(n_bus, -1), qpos(n_bus, -1);
   for (int k = 0; k < n_theta; ++k) tpos[theta_block[k]] = k;
   for (int k = 0; k < n_q; ++k) qpos[q_block[k]] = n_theta + k;
-  std::vector<int32_t> rowptr(nj + 1), diag(nj), pptr(s.nnz_lu + 1);
-  for (int i = 0; i <= nj; ++i) rowptr[i] = (int32_t)s.rowptr[i];
-  for (int i = 0; i < nj; ++i) diag[i] = (int32_t)s.diag[i];
-  for (int64_t t = 0; t <= s.nnz_lu; ++t) pptr[t] = (int32_t)s.pair_ptr[t];
-  std::vector<int2> desc(s.nnz_lu), pairs(s.n_pairs);
-  for (int64_t t = 0; t < s.nnz_lu; ++t)
-    desc[t] = make_int2(s.slot_ynz[t], s.slot_jbus[t] | ((int32_t)s.slot_type[t] << 28));
-  for (int64_t q = 0; q < s.n_pairs; ++q) pairs[q] = make_int2(s.pair_l[q], s.pair_u[q]);
+  std::vector<double2> sy(s.nnz_lu);
+  for (int64_t t = 0; t < s.nnz_lu; ++t) sy[t] = make_double2(sc.slot_yr[t], sc.slot_yi[t]);
 
   NrDeviceModel& d = p->dm;
   d.n_bus = n_bus;
@@ -194,6 +196,21 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.n_q = n_q;
   d.n_j = nj;
   d.nnz_lu = s.nnz_lu;
+  d.n_seg = sc.n_seg;
+  d.n_elem = sc.n_elem;
+  d.off_lu = sc.off_lu;
+  d.off_invd = sc.off_invd;
+  d.off_yx = sc.off_yx;
+  d.off_u = sc.off_u;
+  d.off_e = sc.off_e;
+  d.off_i = sc.off_i;
+  d.off_spec = sc.off_spec;
+  d.off_th = sc.off_th;
+  d.off_vm = sc.off_vm;
+  d.off_spill = sc.off_spill;
+  d.cap = sc.cap;
+  d.max_l = sc.max_l;
+  d.n_levels = sc.n_levels;
   cudaError_t e = cudaSuccess;
   auto up = [&](auto** dst, const auto* src, size_t cnt) {
     if (e == cudaSuccess) e = p->model.upload(dst, src, cnt);
@@ -206,14 +223,11 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<int32_t**>(&d.tpos), tpos.data(), (size_t)n_bus);
   up(const_cast<int32_t**>(&d.qpos), qpos.data(), (size_t)n_bus);
   up(const_cast<int32_t**>(&d.ipos), s.ipos.data(), (size_t)nj);
-  up(const_cast<int32_t**>(&d.row_bus), s.row_bus.data(), (size_t)nj);
-  up(const_cast<int32_t**>(&d.row_kind), s.row_kind.data(), (size_t)nj);
-  up(const_cast<int32_t**>(&d.lu_rowptr), rowptr.data(), (size_t)nj + 1);
-  up(const_cast<int32_t**>(&d.lu_col), s.col.data(), (size_t)s.nnz_lu);
-  up(const_cast<int32_t**>(&d.lu_diag), diag.data(), (size_t)nj);
-  up(const_cast<int2**>(&d.slot_desc), desc.data(), (size_t)s.nnz_lu);
-  up(const_cast<int32_t**>(&d.pair_ptr), pptr.data(), (size_t)s.nnz_lu + 1);
-  up(const_cast<int2**>(&d.pairs), pairs.data(), (size_t)s.n_pairs);
+  up(const_cast<double2**>(&d.slot_y), sy.data(), sy.size());
+  up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
+  up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
+  up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());
+  up(const_cast<uint32_t**>(&d.segmeta), sc.segmeta.data(), sc.segmeta.size());
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
   if (e != cudaSuccess) {
@@ -221,11 +235,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     delete p;
     return e == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;
   }
-  {
-    acpf_nr_plan_info tmp;
-    fill_info(s, &tmp);
-    p->bytes_per_group = tmp.workspace_bytes_per_group;
-  }
+  p->bytes_per_group = sc.n_elem * kGroup * 8;
   *out = p;
   return ACPF_OK;
 }
@@ -253,7 +263,7 @@ acpf_status acpf_nr_plan_info_get(acpf_nr_plan_t p, acpf_nr_plan_info* info) {
     set_error("acpf_nr_plan_info_get: null argument");
     return ACPF_EINVAL;
   }
-  fill_info(p->sym, info);
+  fill_info(p->sym, info, p->bytes_per_group);
   return ACPF_OK;
 }
 
@@ -272,31 +282,16 @@ static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
   if (p->ws_groups >= groups) return ACPF_OK;
   p->work.release();
   p->ws_groups = 0;
-  const NrDeviceModel& d = p->dm;
-  const size_t G = (size_t)groups * kGroup;
-  void* ptr;
-  auto get = [&](size_t bytes) -> void* {
-    if (p->work.alloc(&ptr, bytes) != cudaSuccess) return nullptr;
-    return ptr;
-  };
-  NrWorkspace& w = p->ws;
-  w.lu = (double*)get(G * d.nnz_lu * 8);
-  w.invd = (double*)get(G * d.n_j * 8);
-  w.yx = (double*)get(G * d.n_j * 8);
-  w.spec = (double*)get(G * d.n_j * 8);
-  w.th = (double*)get(G * d.n_bus * 8);
-  w.vm = (double*)get(G * d.n_bus * 8);
-  w.U = (double2*)get(G * d.n_bus * 16);
-  w.E = (double2*)get(G * d.n_bus * 16);
-  w.I = (double2*)get(G * d.n_bus * 16);
-  if (!w.lu || !w.invd || !w.yx || !w.spec || !w.th || !w.vm || !w.U || !w.E || !w.I) {
+  void* ptr = nullptr;
+  if (p->work.alloc(&ptr, (size_t)groups * p->bytes_per_group) != cudaSuccess) {
     p->work.release();
     cudaGetLastError();
     set_error("acpf_nr_solve: device workspace allocation failed (" + std::to_string(groups) +
               " groups); lower ACPF_NR_CHUNK");
     return ACPF_ENOMEM;
   }
-  w.groups = groups;
+  p->ws.arena = (double*)ptr;
+  p->ws.groups = groups;
   p->ws_groups = groups;
   return ACPF_OK;
 }
@@ -337,7 +332,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     const int64_t have_groups = p->ws_groups;
     const int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
     int64_t groups = std::max<int64_t>(1, budget / std::max<int64_t>(1, p->bytes_per_group));
-    groups = std::min<int64_t>(groups, 4096);
+    groups = std::min<int64_t>(groups, 16384);
     chunk = groups * kGroup;
   }
   chunk = std::min<int64_t>(chunk, batch);

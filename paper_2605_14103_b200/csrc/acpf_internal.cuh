@@ -6,12 +6,13 @@
 #include <string>
 
 #include "../../include/acpf.h"
+#include "nr_symbolic.h"
 
 namespace acpf {
 
 void set_error(const std::string& msg);
 
-constexpr int kGroup = 32;  // scenarios interleaved per warp (one lane each)
+constexpr int kGroup = 8;  // NR: scenarios per warp (a quad of lanes each)
 
 // ---------------------------------------------------------------------------
 // Newton plan (device side view passed to the kernel by value)
@@ -23,31 +24,26 @@ struct NrDeviceModel {
   const double2* y_val;
   const double* theta_init;
   const double* vmag_init;
-  const int32_t* tpos;     // [n_bus] packed theta index or -1
-  const int32_t* qpos;     // [n_bus] packed V index (>= n_theta) or -1
-  const int32_t* ipos;     // [n_j] packed -> elimination position
-  const int32_t* row_bus;  // [n_j]
-  const int32_t* row_kind; // [n_j]
-  const int32_t* lu_rowptr;  // [n_j+1]
-  const int32_t* lu_col;     // [nnz_lu]
-  const int32_t* lu_diag;    // [n_j]
-  const int2* slot_desc;     // [nnz_lu] (ynz, jbus | type << 28)
-  const int32_t* pair_ptr;   // [nnz_lu+1]
-  const int2* pairs;         // [n_pairs] (l slot, u slot)
+  const int32_t* tpos;  // [n_bus] packed theta index or -1
+  const int32_t* qpos;  // [n_bus] packed V index (>= n_theta) or -1
+  const int32_t* ipos;  // [n_j] packed -> elimination position
+  // streaming-Crout schedule (nr_symbolic.h NrSchedule)
+  const double2* slot_y;      // [nnz_lu] Ybus value feeding the slot
+  const uint32_t* slot_info;  // [nnz_lu]
+  const uint32_t* brow;       // [n_j]
+  const uint32_t* stream;     // [(n_seg+1)*32]
+  const uint32_t* segmeta;    // [n_seg+1]
+  int64_t n_seg;
   int64_t nnz_lu;
+  int64_t n_elem;
+  int64_t off_lu, off_invd, off_yx, off_u, off_e, off_i, off_spec, off_th, off_vm, off_spill;
+  int cap;
+  int max_l;
+  int n_levels;
 };
 
 struct NrWorkspace {
-  // all per-group blocks are [rows][kGroup]
-  double* lu;     // nnz_lu
-  double* invd;   // n_j
-  double* yx;     // n_j
-  double* spec;   // n_j
-  double* th;     // n_bus
-  double* vm;     // n_bus
-  double2* U;     // n_bus
-  double2* E;     // n_bus
-  double2* I;     // n_bus
+  double* arena;  // [groups][n_elem][kGroup]
   int64_t groups;
 };
 
@@ -63,6 +59,7 @@ struct NrBatchIO {
   int64_t batch;  // scenarios in this chunk
 };
 
+size_t nr_smem_bytes(int cap);
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrWorkspace& w, const NrBatchIO& io,
                              double tol, int max_newton, cudaStream_t stream);
 

@@ -1,23 +1,36 @@
-// Batched polar Newton-Raphson on sm_100a: one warp = 32 scenarios in
-// lock-step, lane = scenario, every per-scenario array interleaved
-// [row][32] so each warp access is one coalesced 256-byte transaction and
-// the shared schedule (Ybus, LU pattern, Crout pairs) is a warp-uniform
-// broadcast load.
+// Batched polar Newton-Raphson on sm_100a, streaming-Crout formulation.
+//
+// Layout: one warp = one group of kGroup = 8 scenarios; each scenario owns a
+// quad of lanes (lane = r*8 + sc, sub-lane r = 0..3, scenario sc = 0..7).
+// Every per-scenario quantity lives in a per-group arena of "elements":
+// element e of scenario sc at arena[e*8 + sc], so one element of a group is
+// 64 contiguous bytes and a warp instruction touching 4 elements is four
+// fully used 64-byte segments. The schedule (LU pattern, Crout updates,
+// Ybus values) is shared by all groups and read as warp-uniform data.
 //
 // One launch runs the whole Newton loop of the reference `_newton_loop`
-// (transmission.py:333-380) for its warp's scenarios, with no host round
-// trip:
-//   A  phasors      u = V e^{j theta}                  (transmission.py:196)
-//   B  mismatch     I = Y u, S = u conj(I), F, ||F||inf (transmission.py:194-215)
+// (transmission.py:333-380) for its group with no host round trip:
+//   A  phasors      u = V e^{j theta}                     (transmission.py:196)
+//   B  mismatch     I = Y u, S = u conj(I), F, ||F||inf    (transmission.py:194-215)
 //      exit checks in the reference order: non-finite -> converged ->
-//      min V <= 0 -> k == max_newton                  (transmission.py:347-359)
-//   C  Jacobian assembly fused into a Crout (row-by-row, dot-product form)
-//      static-pivot LU refactorisation, forward substitution fused
-//      (replaces the GMRES/FD step of transmission.py:361-369)
-//   D  back substitution and x += dx                   (transmission.py:378)
-// Jacobian entries are produced on the fly from the Ybus entry that feeds
-// each LU slot (the block formulas of dense_jacobian, transmission.py:383-407),
-// so the factor storage is written exactly once per slot per Newton step.
+//      min V <= 0 -> k == max_newton                     (transmission.py:347-359)
+//   C  Jacobian assembly fused into a row-by-row (Crout, dot-product form)
+//      static-pivot sparse LU refactorisation with the forward substitution
+//      fused in (replaces the GMRES/FD step solve, transmission.py:361-369);
+//   D  back substitution, x += dx                         (transmission.py:378)
+// A, B and D split buses/updates over the four sub-lanes of a scenario.
+//
+// C and D are driven by one precomputed *gather stream*: every operand not
+// produced inside the current row (earlier U rows, pivots, y/x entries,
+// phasors) is an element index in the stream. The warp prefetches the stream
+// ahead of use with cp.async (LDGSTS, 8 B per lane, 4 elements per warp
+// instruction) into a shared-memory ring; completion is tracked by one
+// mbarrier per 32-element segment. Rows are level-sorted (same fill), so
+// prefetch runs across row boundaries and only drains where a level starts.
+// The Crout updates of one LU slot are split over the quad (4 partial dot
+// products, combined by a fixed butterfly), and the current row's L part
+// never leaves shared memory (later rows only read U), so global traffic is
+// the gathers of earlier U rows plus one write per U slot.
 
 #include "acpf_internal.cuh"
 
@@ -25,46 +38,232 @@ namespace acpf {
 
 namespace {
 
+constexpr int kNSeg = 4;                      // ring segments (kNSeg*32 elements in flight)
+constexpr int kElemBytes = kGroup * 8;        // 64
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// u_i * conj(a)
+// u * conj(a)
 __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
   return make_double2(u.x * a.x + u.y * a.y, u.y * a.x - u.x * a.y);
 }
 
-__global__ void __launch_bounds__(128) nr_newton_kernel(NrDeviceModel m, NrWorkspace w,
-                                                        NrBatchIO io, double tol,
-                                                        int max_newton) {
-  const int lane = threadIdx.x & 31;
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (g >= w.groups) return;
-  const int64_t s = g * kGroup + lane;
-  const bool valid = s < io.batch;
+// sum over the quad (sub-lanes r = 0..3 of one scenario), fixed order
+__device__ __forceinline__ double quad_sum(double x) {
+  x = x + __shfl_xor_sync(kFull, x, 8);
+  x = x + __shfl_xor_sync(kFull, x, 16);
+  return x;
+}
 
-  const int64_t ws_lu = g * m.nnz_lu * kGroup;
-  double* __restrict__ lu = w.lu + ws_lu + lane;
-  double* __restrict__ invd = w.invd + g * m.n_j * kGroup + lane;
-  double* __restrict__ yx = w.yx + g * m.n_j * kGroup + lane;
-  double* __restrict__ spec = w.spec + g * m.n_j * kGroup + lane;
-  double* __restrict__ th = w.th + g * m.n_bus * kGroup + lane;
-  double* __restrict__ vm = w.vm + g * m.n_bus * kGroup + lane;
-  double2* __restrict__ U = w.U + g * m.n_bus * kGroup + lane;
-  double2* __restrict__ E = w.E + g * m.n_bus * kGroup + lane;
-  double2* __restrict__ I = w.I + g * m.n_bus * kGroup + lane;
+// Warp-level gather streamer; every lane executes every call.
+struct Streamer {
+  const uint32_t* stream;  // [n_seg + 1][32]  gidx | lpos << 22
+  const uint32_t* meta;    // [n_seg + 1]      len | epoch << 6
+  const double* arena;     // group arena (element e, scenario sc at arena[e*8 + sc])
+  uint32_t ring;           // smem [kNSeg*32 elements][8] doubles
+  uint32_t rlpos;          // smem [kNSeg*32] u16
+  uint32_t rlen;           // smem [kNSeg] u32
+  uint32_t bar;            // smem [kNSeg] mbarriers (count 32)
+  int lane, r, sc;
+  int64_t n_seg;
+  int64_t k_iss, iss_total;
+  uint32_t winA, winB, metaA, metaB;
+  int64_t k_cur, cur_total;
+  int slot, off, len;
+  uint32_t phase;
+  int epoch;
 
-  // flat start + interleave this lane's specified injections
-  for (int i = 0; i < m.n_bus; ++i) {
-    th[i * kGroup] = m.theta_init[i];
-    vm[i * kGroup] = m.vmag_init[i];
+  __device__ __forceinline__ void preload(int64_t k, uint32_t& win, uint32_t& mt) {
+    win = stream[k * 32 + lane];
+    mt = meta[k];
   }
-  for (int r = 0; r < m.n_j; ++r) {
+
+  __device__ void begin_step() {
+    k_iss = 0;
+    k_cur = -1;
+    off = len = 0;
+    epoch = 0;
+    preload(0, winA, metaA);
+    preload(n_seg > 0 ? 1 : 0, winB, metaB);
+  }
+
+  __device__ void issue_one() {
+    const int s = (int)(iss_total % kNSeg);
+    const int n = (int)(metaA & 63u);
+    const uint32_t seg_base = ring + (uint32_t)s * 32 * kElemBytes;
+    __syncwarp();
+    if (lane < n)
+      asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(rlpos + (s * 32 + lane) * 2),
+                   "h"((unsigned short)(winA >> 22))
+                   : "memory");
+    if (lane == 0)
+      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(rlen + s * 4), "r"(n) : "memory");
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = 4 * j + r;
+      const uint32_t w = __shfl_sync(kFull, winA, e);
+      if (e < n)
+        cp_async8(seg_base + (uint32_t)e * kElemBytes + sc * 8, arena + (size_t)(w & 0x3fffffu) * kGroup + sc);
+    }
+    cp_async_arrive(bar + s * 8);
+    __syncwarp();
+    ++k_iss;
+    ++iss_total;
+    winA = winB;
+    metaA = metaB;
+    const int64_t nk = k_iss + 1 <= n_seg ? k_iss + 1 : n_seg;
+    preload(nk, winB, metaB);
+  }
+
+  __device__ void try_issue() {
+    while (k_iss < n_seg && (k_iss - k_cur) <= kNSeg - (k_cur >= 0 ? 1 : 0) &&
+           (int)(metaA >> 6) <= epoch)
+      issue_one();
+  }
+
+  __device__ void new_epoch(int e) {
+    epoch = e;
+    // rows finished so far were written by this warp's lanes with st.global;
+    // make them visible to the other lanes' cp.async reads
+    __syncwarp();
+    __threadfence_block();
+    try_issue();
+  }
+
+  __device__ void advance() {
+    ++k_cur;
+    if (k_cur > 0) ++cur_total;
+    try_issue();
+    if (k_iss <= k_cur) __trap();  // schedule bug: segment never issuable
+    slot = (int)(cur_total % kNSeg);
+    mbar_wait(bar + slot * 8, (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    len = (int)lds_u32(rlen + slot * 4);
+    off = 0;
+  }
+
+  __device__ __forceinline__ uint32_t elem(int o) const {
+    return ring + (uint32_t)(slot * 32 + o) * kElemBytes + sc * 8;
+  }
+
+  // scalar element (all four sub-lanes read their scenario's value)
+  __device__ __forceinline__ double get() {
+    if (off == len) advance();
+    const double v = lds_f64(elem(off));
+    ++off;
+    return v;
+  }
+
+  __device__ void end_step() { ++cur_total; }
+};
+
+__global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io,
+                                                       double tol, int max_newton) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const int r = lane >> 3, sc = lane & 7;
+  const int64_t g = blockIdx.x;
+  if (g >= w.groups) return;
+  const int64_t s = g * kGroup + sc;
+  const bool valid = s < io.batch;
+  double* __restrict__ A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+#define EL(e) A[(size_t)(e) * kGroup]
+
+  const uint32_t sbase = su32(smem);
+  const uint32_t ring = sbase;                                   // kNSeg*32 elements
+  const uint32_t lbuf = ring + kNSeg * 32 * kElemBytes;          // cap elements
+  const uint32_t bar = lbuf + (uint32_t)m.cap * kElemBytes;      // kNSeg mbarriers
+  const uint32_t rlpos = bar + kNSeg * 8;                        // kNSeg*32 u16
+  const uint32_t rlen = rlpos + kNSeg * 32 * 2;                  // kNSeg u32
+  const uint32_t lbuf_sc = lbuf + sc * 8;
+  if (lane == 0) {
+    for (int k = 0; k < kNSeg; ++k) mbar_init(bar + k * 8, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
+  Streamer st;
+  st.stream = m.stream;
+  st.meta = m.segmeta;
+  st.arena = w.arena + (size_t)g * m.n_elem * kGroup;
+  st.ring = ring;
+  st.rlpos = rlpos;
+  st.rlen = rlen;
+  st.bar = bar;
+  st.lane = lane;
+  st.r = r;
+  st.sc = sc;
+  st.n_seg = m.n_seg;
+  st.iss_total = 0;
+  st.cur_total = 0;
+  st.phase = 0;
+  const bool no_spill = m.cap >= m.max_l;
+
+  // flat start + this scenario's specified injections (buses/entries split over the quad)
+  for (int i = r; i < m.n_bus; i += 4) {
+    EL(m.off_th + i) = m.theta_init[i];
+    EL(m.off_vm + i) = m.vmag_init[i];
+  }
+  for (int k = r; k < m.n_j; k += 4) {
     double v = 0.0;
     if (valid)
-      v = r < m.n_theta ? io.p_spec[s * m.n_theta + r] : io.q_spec[s * m.n_q + (r - m.n_theta)];
-    spec[r * kGroup] = v;
+      v = k < m.n_theta ? io.p_spec[s * m.n_theta + k] : io.q_spec[s * m.n_q + (k - m.n_theta)];
+    EL(m.off_spec + k) = v;
   }
+  __syncwarp();
 
   bool done = !valid;
   int status = 0, iters = 0;
@@ -72,164 +271,289 @@ __global__ void __launch_bounds__(128) nr_newton_kernel(NrDeviceModel m, NrWorks
 
   for (int k = 0; k <= max_newton; ++k) {
     // ---- A: phasors, min V
-    double vmin = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-    for (int i = 0; i < m.n_bus; ++i) {
-      const double t = th[i * kGroup], v = vm[i * kGroup];
+    double vmin = __longlong_as_double(0x7ff0000000000000LL);
+    for (int i = r; i < m.n_bus; i += 4) {
+      const double t = EL(m.off_th + i), v = EL(m.off_vm + i);
       double sn, cs;
       sincos(t, &sn, &cs);
-      E[i * kGroup] = make_double2(cs, sn);
-      U[i * kGroup] = make_double2(v * cs, v * sn);
+      EL(m.off_e + 2 * i) = cs;
+      EL(m.off_e + 2 * i + 1) = sn;
+      EL(m.off_u + 2 * i) = v * cs;
+      EL(m.off_u + 2 * i + 1) = v * sn;
       vmin = fmin(vmin, v);
     }
+    __syncwarp();
     // ---- B: injections and mismatch
-    double fmax = 0.0;
-    bool anynan = false, anyinf = false;
-    for (int i = 0; i < m.n_bus; ++i) {
+    double fmx = 0.0;
+    int bad = 0;  // bit0 NaN, bit1 Inf
+    for (int i = r; i < m.n_bus; i += 4) {
       double2 acc = make_double2(0.0, 0.0);
       const int e1 = m.y_rowptr[i + 1];
       for (int e = m.y_rowptr[i]; e < e1; ++e) {
         const double2 y = m.y_val[e];
-        const double2 u = U[m.y_col[e] * kGroup];
-        acc.x += y.x * u.x - y.y * u.y;
-        acc.y += y.x * u.y + y.y * u.x;
+        const int c = m.y_col[e];
+        const double ur = EL(m.off_u + 2 * c), ui = EL(m.off_u + 2 * c + 1);
+        acc.x += y.x * ur - y.y * ui;
+        acc.y += y.x * ui + y.y * ur;
       }
-      I[i * kGroup] = acc;
-      const double2 ui = U[i * kGroup];
-      const double2 sc = mul_conj(ui, acc);  // S_i = u_i conj(I_i)
+      EL(m.off_i + 2 * i) = acc.x;
+      EL(m.off_i + 2 * i + 1) = acc.y;
+      const double2 u = make_double2(EL(m.off_u + 2 * i), EL(m.off_u + 2 * i + 1));
+      const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
       const int tp = m.tpos[i], qp = m.qpos[i];
       if (tp >= 0) {
-        const double f = sc.x - spec[tp * kGroup];
-        anynan |= isnan(f);
-        anyinf |= isinf(f);
-        fmax = fmax < fabs(f) ? fabs(f) : fmax;
-        yx[m.ipos[tp] * kGroup] = -f;
+        const double f = sv.x - EL(m.off_spec + tp);
+        bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
+        fmx = fmx < fabs(f) ? fabs(f) : fmx;
+        EL(m.off_yx + m.ipos[tp]) = -f;
       }
       if (qp >= 0) {
-        const double f = sc.y - spec[qp * kGroup];
-        anynan |= isnan(f);
-        anyinf |= isinf(f);
-        fmax = fmax < fabs(f) ? fabs(f) : fmax;
-        yx[m.ipos[qp] * kGroup] = -f;
+        const double f = sv.y - EL(m.off_spec + qp);
+        bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
+        fmx = fmx < fabs(f) ? fabs(f) : fmx;
+        EL(m.off_yx + m.ipos[qp]) = -f;
       }
     }
+    // quad reductions (order independent: max / min / or)
+    fmx = fmax(fmx, __shfl_xor_sync(kFull, fmx, 8));
+    fmx = fmax(fmx, __shfl_xor_sync(kFull, fmx, 16));
+    vmin = fmin(vmin, __shfl_xor_sync(kFull, vmin, 8));
+    vmin = fmin(vmin, __shfl_xor_sync(kFull, vmin, 16));
+    bad |= __shfl_xor_sync(kFull, bad, 8);
+    bad |= __shfl_xor_sync(kFull, bad, 16);
     if (!done) {
-      if (anynan || anyinf) {
+      if (bad) {
         done = true;
         status = ACPF_NR_NONFINITE;
         iters = k;
-        fout = anynan ? __longlong_as_double(0x7ff8000000000000LL) : fmax;
-      } else if (fmax <= tol) {
+        fout = (bad & 1) ? __longlong_as_double(0x7ff8000000000000LL) : fmx;
+      } else if (fmx <= tol) {
         done = true;
         status = ACPF_NR_CONVERGED;
         iters = k;
-        fout = fmax;
+        fout = fmx;
       } else if (vmin <= 0.0) {
         done = true;
         status = ACPF_NR_VMAG_LE0;
         iters = k;
-        fout = fmax;
+        fout = fmx;
       } else if (k == max_newton) {
         done = true;
         status = ACPF_NR_MAX_ITER;
         iters = max_newton;
-        fout = fmax;
+        fout = fmx;
       }
     }
-    if (__all_sync(0xffffffffu, done)) break;
+    if (__all_sync(kFull, done)) break;
 
     // ---- C: assembly + Crout refactorisation + forward substitution
+    st.begin_step();
+    st.new_epoch(0);
     bool zero_pivot = false;
+    int64_t t = 0;  // LU slot
+    // slot descriptor windows (lane j holds slot w0 + j), double buffered
+    int64_t w0 = 0;
+    double wyr = 0, wyi = 0, nyr = 0, nyi = 0;
+    uint32_t winfo = 0, ninfo = 0;
+    if (lane < m.nnz_lu) {
+      wyr = m.slot_y[lane].x;
+      wyi = m.slot_y[lane].y;
+      winfo = m.slot_info[lane];
+    }
+    if (32 + lane < m.nnz_lu) {
+      nyr = m.slot_y[32 + lane].x;
+      nyi = m.slot_y[32 + lane].y;
+      ninfo = m.slot_info[32 + lane];
+    }
+    int epoch = 0;
     for (int p = 0; p < m.n_j; ++p) {
-      const int bi = m.row_bus[p];
-      const double2 ui = U[bi * kGroup];
-      const double2 Ii = I[bi * kGroup];
-      const int t0 = m.lu_rowptr[p], t1 = m.lu_rowptr[p + 1], td = m.lu_diag[p];
-      double yacc = yx[p * kGroup];
-      for (int t = t0; t < t1; ++t) {
-        const int2 d = m.slot_desc[t];
-        const int type = (unsigned)d.y >> 28;
-        double a = 0.0;
-        if (type < 8) {
-          const int j = d.y & 0x0fffffff;
-          const double2 y = d.x >= 0 ? m.y_val[d.x] : make_double2(0.0, 0.0);
-          const bool diag = type & 4, qrow = type & 2;
-          if (type & 1) {  // d/dV_j: u_i conj(y E_j) [+ conj(I_i) E_i]
-            const double2 ej = E[j * kGroup];
-            const double2 wv = mul_conj(ui, cmul(y, ej));
-            if (!diag) {
-              a = qrow ? wv.y : wv.x;
-            } else {
-              a = qrow ? wv.y + (Ii.x * ej.y - Ii.y * ej.x) : wv.x + (Ii.x * ej.x + Ii.y * ej.y);
-            }
-          } else {  // d/dtheta_j
-            if (!diag) {  // -j u_i conj(y u_j)
-              const double2 wv = mul_conj(ui, cmul(y, U[j * kGroup]));
-              a = qrow ? -wv.x : wv.y;
-            } else {  // j u_i conj(I_i - y u_i)
-              const double2 yu = cmul(y, ui);
-              const double2 wv = mul_conj(ui, make_double2(Ii.x - yu.x, Ii.y - yu.y));
-              a = qrow ? wv.x : -wv.y;
-            }
+      double ur = 0, ui = 0, Ir = 0, Ii = 0, yacc = 0;
+      int pos = 0;  // position within the row
+      for (;;) {
+        if (t - w0 == 32) {
+          w0 += 32;
+          wyr = nyr;
+          wyi = nyi;
+          winfo = ninfo;
+          const int64_t nt = w0 + 32 + lane;
+          if (nt < m.nnz_lu) {
+            nyr = m.slot_y[nt].x;
+            nyi = m.slot_y[nt].y;
+            ninfo = m.slot_info[nt];
           }
         }
-        const int q1 = m.pair_ptr[t + 1];
-#pragma unroll 4
-        for (int q = m.pair_ptr[t]; q < q1; ++q) {
-          const int2 pr = m.pairs[q];
-          a = fma(-lu[pr.x * kGroup], lu[pr.y * kGroup], a);
+        const int j = (int)(t - w0);
+        const uint32_t info = __shfl_sync(kFull, winfo, j);
+        if (info & kSlotRowStart) {
+          if (info & kSlotNewEpoch) st.new_epoch(++epoch);
+          ur = st.get();
+          ui = st.get();
+          Ir = st.get();
+          Ii = st.get();
+          yacc = st.get();
         }
-        if (t < td) {
-          const int c = m.lu_col[t];
-          a *= invd[c * kGroup];
-          yacc = fma(-a, yx[c * kGroup], yacc);
-        } else if (t == td) {
-          zero_pivot |= (a == 0.0);
-          invd[p * kGroup] = 1.0 / a;
+        const int type = info & 15u;
+        double a = 0.0;
+        if (type < 8) {
+          const double yr = __shfl_sync(kFull, wyr, j);
+          const double yi = __shfl_sync(kFull, wyi, j);
+          const double xr = st.get(), xi = st.get();  // u_j (theta col) or E_j (V col)
+          const double2 y = make_double2(yr, yi);
+          const double2 ui2 = make_double2(ur, ui);
+          const bool diag = type & 4, qrow = type & 2;
+          if (type & 1) {  // d/dV_j: u_i conj(y E_j) [+ conj(I_i) E_i]
+            const double2 wv = mul_conj(ui2, cmul(y, make_double2(xr, xi)));
+            if (!diag)
+              a = qrow ? wv.y : wv.x;
+            else
+              a = qrow ? wv.y + (Ir * xi - Ii * xr) : wv.x + (Ir * xr + Ii * xi);
+          } else if (!diag) {  // -j u_i conj(y u_j)
+            const double2 wv = mul_conj(ui2, cmul(y, make_double2(xr, xi)));
+            a = qrow ? -wv.x : wv.y;
+          } else {  // j u_i conj(I_i - y u_i)
+            const double2 yu = cmul(y, ui2);
+            const double2 wv = mul_conj(ui2, make_double2(Ir - yu.x, Ii - yu.y));
+            a = qrow ? wv.x : -wv.y;
+          }
         }
-        lu[t * kGroup] = a;
+        int cnt = (int)(info >> 16);
+        if (cnt) {
+          double part = 0.0;
+          while (cnt > 0) {
+            if (st.off == st.len) st.advance();
+            const int nb = min(cnt, st.len - st.off);
+            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off) * 2;
+            const uint32_t ra = st.elem(st.off);
+            if (no_spill) {
+#pragma unroll 2
+              for (int q = r; q < nb; q += 4) {
+                const uint32_t lp = lds_u16(la + 2 * q);
+                part = fma(-lds_f64(lbuf_sc + lp * kElemBytes), lds_f64(ra + q * kElemBytes), part);
+              }
+            } else {
+              for (int q = r; q < nb; q += 4) {
+                const int lp = (int)lds_u16(la + 2 * q);
+                const double l = lp < m.cap ? lds_f64(lbuf_sc + lp * kElemBytes)
+                                            : EL(m.off_spill + (lp - m.cap));
+                part = fma(-l, lds_f64(ra + q * kElemBytes), part);
+              }
+            }
+            st.off += nb;
+            cnt -= nb;
+          }
+          a = a + quad_sum(part);
+        }
+        if (info & kSlotL) {
+          const double inv = st.get();
+          const double yc = st.get();
+          a *= inv;
+          yacc = fma(-a, yc, yacc);
+          // every quad lane holds the same value: each writes it, so each
+          // lane's later reads depend only on its own store
+          if (pos < m.cap)
+            sts_f64(lbuf_sc + pos * kElemBytes, a);
+          else
+            EL(m.off_spill + (pos - m.cap)) = a;
+        } else {
+          if (info & kSlotDiag) {
+            zero_pivot |= (a == 0.0);
+            if (r == 0) EL(m.off_invd + p) = 1.0 / a;
+          }
+          if (r == 0) EL(m.off_lu + t) = a;
+        }
+        ++t;
+        ++pos;
+        if (info & kSlotRowEnd) break;
       }
-      yx[p * kGroup] = yacc;
+      if (r == 0) EL(m.off_yx + p) = yacc;
     }
-    // ---- D: back substitution
-    for (int p = m.n_j - 1; p >= 0; --p) {
-      double acc = yx[p * kGroup];
-      const int t1 = m.lu_rowptr[p + 1];
-      for (int t = m.lu_diag[p] + 1; t < t1; ++t) acc = fma(-lu[t * kGroup], yx[m.lu_col[t] * kGroup], acc);
-      yx[p * kGroup] = acc * invd[p * kGroup];
+    // ---- D: back substitution (rows by back level)
+    st.new_epoch(m.n_levels);
+    epoch = m.n_levels;
+    uint32_t bwin = 0, bnext = 0;
+    if (lane < m.n_j) bwin = m.brow[lane];
+    if (32 + lane < m.n_j) bnext = m.brow[32 + lane];
+    for (int rr = 0; rr < m.n_j; ++rr) {
+      if (rr && (rr & 31) == 0) {
+        bwin = bnext;
+        if (rr + 32 + lane < m.n_j) bnext = m.brow[rr + 32 + lane];
+      }
+      const uint32_t b = __shfl_sync(kFull, bwin, rr & 31);
+      if (b >> 31) st.new_epoch(++epoch);
+      const int p = (int)(b & 0xfffffu);
+      int rem = (int)((b >> 20) & 0x7ffu);
+      const double y0 = st.get();
+      const double inv = st.get();
+      double part = 0.0;
+      while (rem > 0) {
+        if (st.off == st.len) st.advance();
+        const int nb = min(rem, (st.len - st.off) >> 1);
+        if (nb == 0) {  // a (u, x) pair straddles two segments
+          const double u = st.get();
+          const double x = st.get();
+          if (r == 0) part = fma(-u, x, part);
+          --rem;
+          continue;
+        }
+        const uint32_t ra = st.elem(st.off);
+        for (int q = r; q < nb; q += 4)
+          part = fma(-lds_f64(ra + 2 * q * kElemBytes), lds_f64(ra + (2 * q + 1) * kElemBytes), part);
+        st.off += 2 * nb;
+        rem -= nb;
+      }
+      const double x = (y0 + quad_sum(part)) * inv;
+      if (r == 0) EL(m.off_yx + p) = x;
     }
+    st.end_step();
+    __syncwarp();
+    // per scenario: every lane of a quad saw the same pivots
+    zero_pivot = zero_pivot || __shfl_xor_sync(kFull, (int)zero_pivot, 8) ||
+                 __shfl_xor_sync(kFull, (int)zero_pivot, 16);
     if (!done && zero_pivot) {
       done = true;
       status = ACPF_NR_ZERO_PIVOT;
       iters = k;
-      fout = fmax;
+      fout = fmx;
     }
     if (!done) {
-      for (int i = 0; i < m.n_bus; ++i) {
+      for (int i = r; i < m.n_bus; i += 4) {
         const int tp = m.tpos[i], qp = m.qpos[i];
-        if (tp >= 0) th[i * kGroup] = th[i * kGroup] + yx[m.ipos[tp] * kGroup];
-        if (qp >= 0) vm[i * kGroup] = vm[i * kGroup] + yx[m.ipos[qp] * kGroup];
+        if (tp >= 0) EL(m.off_th + i) = EL(m.off_th + i) + EL(m.off_yx + m.ipos[tp]);
+        if (qp >= 0) EL(m.off_vm + i) = EL(m.off_vm + i) + EL(m.off_yx + m.ipos[qp]);
       }
     }
+    __syncwarp();
   }
 
   if (!valid) return;
-  for (int i = 0; i < m.n_bus; ++i) {
-    io.theta_out[s * m.n_bus + i] = th[i * kGroup];
-    io.vmag_out[s * m.n_bus + i] = vm[i * kGroup];
+  for (int i = r; i < m.n_bus; i += 4) {
+    io.theta_out[s * m.n_bus + i] = EL(m.off_th + i);
+    io.vmag_out[s * m.n_bus + i] = EL(m.off_vm + i);
   }
-  if (io.converged) io.converged[s] = status == ACPF_NR_CONVERGED;
-  if (io.iterations) io.iterations[s] = iters;
-  if (io.fnorm) io.fnorm[s] = fout;
-  if (io.status) io.status[s] = status;
+  if (r == 0) {
+    if (io.converged) io.converged[s] = status == ACPF_NR_CONVERGED;
+    if (io.iterations) io.iterations[s] = iters;
+    if (io.fnorm) io.fnorm[s] = fout;
+    if (io.status) io.status[s] = status;
+  }
+#undef EL
 }
 
 }  // namespace
 
+size_t nr_smem_bytes(int cap) {
+  return (size_t)kNSeg * 32 * kElemBytes + (size_t)cap * kElemBytes + kNSeg * 8 + kNSeg * 32 * 2 +
+         kNSeg * 4 + 16;
+}
+
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrWorkspace& w, const NrBatchIO& io,
                              double tol, int max_newton, cudaStream_t stream) {
-  const int warps_per_block = 4;
-  const int64_t blocks = (w.groups + warps_per_block - 1) / warps_per_block;
-  nr_newton_kernel<<<(unsigned)blocks, 32 * warps_per_block, 0, stream>>>(m, w, io, tol, max_newton);
+  const size_t smem = nr_smem_bytes(m.cap);
+  cudaError_t e = cudaFuncSetAttribute(nr_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t groups = (io.batch + kGroup - 1) / kGroup;
+  nr_stream_kernel<<<(unsigned)groups, 32, smem, stream>>>(m, w, io, tol, max_newton);
   return cudaGetLastError();
 }
 

@@ -236,3 +236,161 @@ void build_nr_symbolic(NrSymbolic& s, int n_bus, const int32_t* y_rowptr, const 
 }
 
 }  // namespace acpf
+
+namespace acpf {
+
+namespace {
+std::vector<int> factor_levels(const NrSymbolic& s) {
+  std::vector<int> lev(s.n_j, 0);
+  for (int p = 0; p < s.n_j; ++p) {
+    int l = 0;
+    for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) l = std::max(l, lev[s.col[t]] + 1);
+    lev[p] = l;
+  }
+  return lev;
+}
+}  // namespace
+
+std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
+  // rows of equal level never reference each other, and sorting by level is
+  // a topological order of the elimination tree, so the filled pattern (and
+  // nnz) is unchanged while rows that can be prefetched together become
+  // contiguous.
+  const std::vector<int> lev = factor_levels(s);
+  std::vector<int32_t> idx(s.n_j);
+  for (int p = 0; p < s.n_j; ++p) idx[p] = p;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return lev[a] < lev[b]; });
+  std::vector<int32_t> perm(s.n_j);
+  for (int k = 0; k < s.n_j; ++k) perm[k] = s.perm[idx[k]];
+  return perm;
+}
+
+void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const double* y_re,
+                       const double* y_im, int cap_limit, NrSchedule& o) {
+  (void)y_rowptr;
+  const int nj = s.n_j, nb = s.n_bus;
+  // ---- arena layout
+  int64_t e = 0;
+  o.off_lu = e;    e += s.nnz_lu;
+  o.off_invd = e;  e += nj;
+  o.off_yx = e;    e += nj;
+  o.off_u = e;     e += 2 * (int64_t)nb;
+  o.off_e = e;     e += 2 * (int64_t)nb;
+  o.off_i = e;     e += 2 * (int64_t)nb;
+  o.off_spec = e;  e += nj;
+  o.off_th = e;    e += nb;
+  o.off_vm = e;    e += nb;
+  o.max_l = 0;
+  for (int p = 0; p < nj; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
+  o.cap = std::min(o.max_l, cap_limit);
+  o.off_spill = e; e += std::max(0, o.max_l - o.cap);
+  o.n_elem = e;
+  if (o.n_elem >= (1 << 22)) throw std::length_error("arena exceeds 22-bit gather index");
+  if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 entries");
+
+  // ---- levels
+  const std::vector<int> lev = factor_levels(s);
+  std::vector<int> blev(nj, 0);
+  for (int p = nj - 1; p >= 0; --p) {
+    int l = 0;
+    for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) l = std::max(l, blev[s.col[t]] + 1);
+    blev[p] = l;
+  }
+  o.n_levels = 0;
+  o.n_blevels = 0;
+  for (int p = 0; p < nj; ++p) {
+    o.n_levels = std::max(o.n_levels, lev[p] + 1);
+    o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
+    if (p && lev[p] < lev[p - 1]) throw std::logic_error("rows not level-sorted");
+  }
+
+  // ---- stream construction
+  std::vector<uint32_t> flat;     // gidx | lpos << 22
+  std::vector<int> flat_epoch;
+  auto push = [&](int64_t gidx, int lpos, int epoch) {
+    flat.push_back((uint32_t)gidx | ((uint32_t)lpos << 22));
+    flat_epoch.push_back(epoch);
+  };
+  o.slot_yr.assign(s.nnz_lu, 0.0);
+  o.slot_yi.assign(s.nnz_lu, 0.0);
+  o.slot_info.assign(s.nnz_lu, 0);
+  for (int p = 0; p < nj; ++p) {
+    const int ep = lev[p];
+    const int bi = s.row_bus[p];
+    push(o.off_u + 2 * bi, 0, ep);
+    push(o.off_u + 2 * bi + 1, 0, ep);
+    push(o.off_i + 2 * bi, 0, ep);
+    push(o.off_i + 2 * bi + 1, 0, ep);
+    push(o.off_yx + p, 0, ep);
+    const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
+    for (int64_t t = r0; t < r1; ++t) {
+      uint32_t info = s.slot_type[t];
+      if (t == r0) info |= kSlotRowStart;
+      if (t == r0 && p > 0 && lev[p] != lev[p - 1]) info |= kSlotNewEpoch;
+      if (t == s.diag[p]) info |= kSlotDiag;
+      if (t == r1 - 1) info |= kSlotRowEnd;
+      if (t < s.diag[p]) info |= kSlotL;
+      const int64_t cnt = s.pair_ptr[t + 1] - s.pair_ptr[t];
+      if (cnt >= 65536) throw std::length_error("too many updates for one slot");
+      info |= (uint32_t)cnt << 16;
+      o.slot_info[t] = info;
+      if (s.slot_type[t] < 8) {
+        const int j = s.slot_jbus[t];
+        if (s.slot_ynz[t] >= 0) {
+          o.slot_yr[t] = y_re[s.slot_ynz[t]];
+          o.slot_yi[t] = y_im[s.slot_ynz[t]];
+        }
+        const int64_t base = (s.slot_type[t] & 1) ? o.off_e : o.off_u;
+        push(base + 2 * j, 0, ep);
+        push(base + 2 * j + 1, 0, ep);
+      }
+      for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
+        push(o.off_lu + s.pair_u[q], (int)(s.pair_l[q] - r0), ep);
+      if (t < s.diag[p]) {
+        push(o.off_invd + s.col[t], 0, ep);
+        push(o.off_yx + s.col[t], 0, ep);
+      }
+    }
+  }
+  // back rows: by back level, descending p within a level
+  std::vector<int32_t> border(nj);
+  for (int p = 0; p < nj; ++p) border[p] = p;
+  std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
+    return blev[a] != blev[b] ? blev[a] < blev[b] : a > b;
+  });
+  o.brow.resize(nj);
+  for (int r = 0; r < nj; ++r) {
+    const int p = border[r];
+    const int ep = o.n_levels + blev[p];
+    const int64_t cnt = s.rowptr[p + 1] - s.diag[p] - 1;
+    if (p >= (1 << 20) || cnt >= 2048) throw std::length_error("back row too large");
+    o.brow[r] = (uint32_t)p | ((uint32_t)cnt << 20) |
+                ((r > 0 && blev[p] != blev[border[r - 1]]) ? (1u << 31) : 0u);
+    push(o.off_yx + p, 0, ep);
+    push(o.off_invd + p, 0, ep);
+    for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
+      push(o.off_lu + t, 0, ep);
+      push(o.off_yx + s.col[t], 0, ep);
+    }
+  }
+  o.n_stream = (int64_t)flat.size();
+  // ---- segment: at most kSeg words, never across an epoch change
+  o.stream.clear();
+  o.segmeta.clear();
+  size_t i = 0;
+  while (i < flat.size()) {
+    const int ep = flat_epoch[i];
+    size_t j = i;
+    while (j < flat.size() && j - i < (size_t)kSeg && flat_epoch[j] == ep) ++j;
+    for (size_t k = i; k < j; ++k) o.stream.push_back(flat[k]);
+    for (size_t k = j - i; k < (size_t)kSeg; ++k) o.stream.push_back(0u);
+    o.segmeta.push_back((uint32_t)(j - i) | ((uint32_t)ep << 6));
+    i = j;
+  }
+  o.n_seg = (int64_t)o.segmeta.size();
+  // sentinel segment (never issued): epoch beyond every consumer epoch
+  for (int k = 0; k < kSeg; ++k) o.stream.push_back(0u);
+  o.segmeta.push_back(0u | (0x3ffffffu << 6));
+}
+
+}  // namespace acpf

@@ -25,6 +25,42 @@ struct NrSymbolic {
   std::vector<int32_t> pair_l, pair_u;
 };
 
+// Per-step gather stream for the streaming Crout kernel (see nr_kernel.cu).
+// Arena: one contiguous block of elements per scenario group; element e of
+// lane l lives at arena[e * 32 + l].
+struct NrSchedule {
+  int64_t off_lu = 0, off_invd = 0, off_yx = 0, off_u = 0, off_e = 0, off_i = 0, off_spec = 0,
+          off_th = 0, off_vm = 0, off_spill = 0, n_elem = 0;
+  int cap = 0;       // L entries kept in shared memory per row
+  int max_l = 0;     // longest L part of any row
+  int n_levels = 0;  // factor levels (etree height)
+  int n_blevels = 0; // back-substitution levels
+  // factor slots in slot order
+  std::vector<double> slot_yr, slot_yi;
+  std::vector<uint32_t> slot_info;  // type(4) | flags(4) | cnt << 16
+  // back rows in back order: p | cnt << 20 | new_epoch << 31
+  std::vector<uint32_t> brow;
+  // segmented stream: 32 words per segment, word = gidx | lpos << 22
+  std::vector<uint32_t> stream;
+  std::vector<uint32_t> segmeta;  // len | epoch << 6
+  int64_t n_seg = 0;
+  int64_t n_stream = 0;  // live elements (without padding)
+};
+
+// slot_info flag bits
+constexpr uint32_t kSlotRowStart = 1u << 4;
+constexpr uint32_t kSlotDiag = 1u << 5;
+constexpr uint32_t kSlotRowEnd = 1u << 6;
+constexpr uint32_t kSlotNewEpoch = 1u << 7;
+constexpr uint32_t kSlotL = 1u << 8;
+constexpr int kSeg = 32;
+
+void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const double* y_re,
+                       const double* y_im, int cap_limit, NrSchedule& out);
+
+// Level-sorted topological reordering of an elimination order (same fill).
+std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
+
 void build_nr_symbolic(NrSymbolic& s, int n_bus, const int32_t* y_rowptr, const int32_t* y_col,
                        int n_theta, const int32_t* theta_block, int n_q, const int32_t* q_block,
                        const int32_t* perm_in);

@@ -238,7 +238,7 @@ class NrPlan:
         return ms.value, n.value
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.acpf_nr_plan_destroy(self._h)
             self._h = None
 
@@ -313,7 +313,7 @@ class ZbusPlan:
         return ms.value, n.value
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.acpf_zbus_plan_destroy(self._h)
             self._h = None
 
