@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""Benchmark: converged power flows/sec on B200 (GBnetwork NR headline, EULV Z-Bus secondary).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A *step* is one pass of the hot path over one batch of synthetic scenarios
+(BASELINE.json configs[2] GBnetwork NR, configs[3] EULV Z-Bus; per-GPU batch
+fixed, so scaling is weak). Scenarios come from the reference's own seeded
+generator (Philox multipliers U[0.8, 1.2], batch.py:45-60) on the reference
+fixtures. ``value`` is measured with inputs resident in HBM (CUDA events on
+the solve stream, barrier + synchronize around the K timed steps, max over
+ranks); ``e2e`` is the same metric through the C-ABI with pinned host
+buffers, H2D of the inputs and D2H of voltages/flags inside the timed
+region. Inputs exceed L2 (2.1 GB NR, 0.23 GB Z-Bus), so no explicit flush.
+
+``--impl reference`` times the reference algorithm's CPU path (the pinned
+oracle restatement, oracle/, GMRES-FD Newton / LU Z-Bus) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NR_CASE, NR_SEED = "gb2224", 10010
+ZB_CASE, ZB_SEED = "eulv", 10011
+METRIC = "converged power flows/sec (GBnetwork NR, EULV Z-Bus) at 1/2/4/8 B200 vs CPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--nr-batch", type=int, default=65536, help="NR scenarios per GPU per step")
+    ap.add_argument("--zb-batch", type=int, default=262144, help="Z-Bus scenarios per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="scenarios per CPU-baseline step")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+def build_nr(rank, world, batch):
+    import paper_2605_14103_b200 as pf
+    from paper_2605_14103_b200.fixtures import load_transmission
+
+    net = load_transmission(NR_CASE)
+    model = pf.build_transmission_model(net)
+    base = pf.transmission_base(net, model.part)
+    spec = pf.ScenarioSpec(count=batch * world, seed=NR_SEED)
+    p, q = pf.make_scenario_arrays(base, spec, start=rank * batch, count=batch)
+    return model, p, q
+
+
+def build_zb(rank, world, batch):
+    import paper_2605_14103_b200 as pf
+    from paper_2605_14103_b200.fixtures import load_distribution
+
+    model = pf.build_zbus_model(load_distribution(ZB_CASE))
+    base = pf.distribution_base(model)
+    spec = pf.ScenarioSpec(count=batch * world, seed=ZB_SEED, target="distribution")
+    sw, sd = pf.make_scenario_arrays(base, spec, start=rank * batch, count=batch)
+    return model, sw, sd
+
+
+def pinned_like(a: np.ndarray):
+    import torch
+    t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+    t.numpy()[...] = a
+    return t
+
+
+def pinned_outputs(outs: dict) -> dict:
+    import torch
+    res = {}
+    for k, v in outs.items():
+        t = torch.empty(v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True)
+        res[k] = t.numpy()
+    return res
+
+
+def time_device(fn, steps, warmup, stream, dev):
+    """K timed steps bracketed by barrier + synchronize; CUDA events on `stream`."""
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    if dist.is_initialized():
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist.is_initialized():
+        dist.barrier()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def time_host(fn, steps, warmup, dev):
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    if dist.is_initialized():
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fn()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter() - t0
+    if dist.is_initialized():
+        dist.barrier()
+    return t
+
+
+def traffic_from_profiles(kernel: str, batch: int):
+    """dram bytes per launch from a committed ncu --set full summary, if one
+    matches this kernel and batch (profiles/ncu_traffic.json)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        e = d.get(kernel)
+        if e and int(e.get("batch", -1)) == batch:
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+def run_ours(args, rank, local, world):
+    import torch
+    from paper_2605_14103_b200 import engine, peaks, roofline, shard
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    res = {}
+
+    # ---------------- NR (headline)
+    model, p, q = build_nr(rank, world, args.nr_batch)
+    plan = model.plan(local)
+    pt, qt = torch.from_numpy(p).to(dev), torch.from_numpy(q).to(dev)
+    out = plan.alloc_outputs(args.nr_batch, like=pt)
+    launches = [0, 0.0]
+
+    def nr_step():
+        plan.solve(pt, qt, 1e-8, 20, out=out, stream=stream)
+        ms, nl = plan.last_timing()
+        launches[0] += nl
+        launches[1] += ms
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            nr_step()
+        launches[:] = [0, 0.0]
+        t = time_device(nr_step, args.steps, 0, stream, dev)
+    t = shard.max_over_ranks(t, dev)
+    conv = int(out["converged"].sum().item())
+    its = out["iterations"].cpu().numpy()
+    n_conv_all = shard.sum_over_ranks(conv, dev)
+    info = plan.info
+    value = n_conv_all * args.steps / t
+    kern_s = launches[1] / 1e3 / max(1, launches[0])  # avg launch duration
+    per_launch_scen = args.nr_batch / max(1, launches[0] / args.steps)
+    alg_bytes = float(roofline.nr_bytes_per_scenario(its, info["n_bus"], info["n_j"],
+                                                     info["nnz_lu"]).mean()) * per_launch_scen
+    hbm, hbm_src = peaks.hbm_gbs()
+    achieved = alg_bytes / kern_s / 1e9
+    traffic = traffic_from_profiles("nr_stream_kernel", args.nr_batch)
+    res["nr"] = dict(value=value, t=t, steps=args.steps, launches=launches[0], clocks=clk.summary(),
+                     iterations=np.unique(its).tolist(), conv_frac=conv / args.nr_batch,
+                     roofline={"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                               "frac": achieved / hbm, "traffic": traffic,
+                               "kernel": "nr_stream_kernel",
+                               "algorithmic_bytes_per_launch": alg_bytes,
+                               "avg_launch_ms": kern_s * 1e3, "peak_source": hbm_src})
+    # e2e through the C-ABI with pinned host buffers
+    hp, hq = pinned_like(p).numpy(), pinned_like(q).numpy()
+    hout = pinned_outputs(plan.alloc_outputs(args.nr_batch))
+    te = time_host(lambda: plan.solve(hp, hq, 1e-8, 20, out=hout), args.steps, 1, dev)
+    te = shard.max_over_ranks(te, dev)
+    conv_e = shard.sum_over_ranks(int(hout["converged"].sum()), dev)
+    res["nr"]["e2e"] = {
+        "value": conv_e * args.steps / te, "unit": "converged flows/s",
+        "h2d_bytes_per_step": int(hp.nbytes + hq.nbytes) * world,
+        "d2h_bytes_per_step": int(sum(v.nbytes for v in hout.values())) * world}
+    del pt, qt, out
+    plan_info = dict(info)
+
+    # ---------------- Z-Bus (secondary)
+    zmodel, sw, sd = build_zb(rank, world, args.zb_batch)
+    zplan = engine.zbus_plan_for(zmodel, local)
+    swt = torch.from_numpy(sw).to(dev)
+    sdt = torch.from_numpy(np.ascontiguousarray(sd.reshape(args.zb_batch, -1))).to(dev)
+    zout = zplan.alloc_outputs(args.zb_batch, like=swt)
+    zl = [0, 0.0]
+
+    def zb_step():
+        zplan.solve(swt, sdt, 1e-9, 100, out=zout, stream=stream)
+        ms, nl = zplan.last_timing()
+        zl[0] += nl
+        zl[1] += ms
+
+    with ClockSampler(local) as zclk:
+        for _ in range(args.warmup):
+            zb_step()
+        zl[:] = [0, 0.0]
+        tz = time_device(zb_step, args.steps, 0, stream, dev)
+    tz = shard.max_over_ranks(tz, dev)
+    zconv = shard.sum_over_ranks(int(zout["converged"].sum().item()), dev)
+    zits = zout["iterations"].cpu().numpy()
+    nloads = zmodel.wye_idx.size + zmodel.delta_p.size
+    zk = zl[1] / 1e3 / max(1, zl[0])
+    zper = args.zb_batch / max(1, zl[0] / args.steps)
+    zflops = float(roofline.zbus_flops_per_scenario(zits, zmodel.n, zmodel.load_cols.size,
+                                                    nloads).mean()) * zper
+    fp, fp_src = peaks.fp64_tflops()
+    zach = zflops / zk / 1e12
+    hsw, hsd = pinned_like(sw).numpy(), pinned_like(np.ascontiguousarray(sd.reshape(args.zb_batch, -1))).numpy()
+    hz = pinned_outputs(zplan.alloc_outputs(args.zb_batch))
+    tze = time_host(lambda: zplan.solve(hsw, hsd, 1e-9, 100, out=hz), args.steps, 1, dev)
+    tze = shard.max_over_ranks(tze, dev)
+    zconv_e = shard.sum_over_ranks(int(hz["converged"].sum()), dev)
+    res["zb"] = dict(
+        value=zconv * args.steps / tz, t=tz, launches=zl[0], clocks=zclk.summary(),
+        iterations=np.unique(zits).tolist(),
+        roofline={"bound": "tensor", "achieved": zach, "peak": fp, "unit": "TFLOP/s",
+                  "frac": zach / fp, "traffic": traffic_from_profiles("zbus_kernel", args.zb_batch),
+                  "kernel": "zbus_kernel<64>", "algorithmic_flops_per_launch": zflops,
+                  "avg_launch_ms": zk * 1e3, "peak_source": fp_src},
+        e2e={"value": zconv_e * args.steps / tze, "unit": "converged flows/s",
+             "h2d_bytes_per_step": int(hsw.nbytes + hsd.nbytes) * world,
+             "d2h_bytes_per_step": int(sum(v.nbytes for v in hz.values())) * world})
+    return res, plan_info
+
+
+# ---------------------------------------------------------------------------
+# CPU path (reference algorithm restated in oracle/) -- baseline / reference arm
+# ---------------------------------------------------------------------------
+
+_CPU = {}
+
+
+def _cpu_init(kind):
+    import paper_2605_14103_b200 as pf
+    from oracle import nr as onr
+    from oracle import zbus as ozb
+    if kind == "nr":
+        model, p, q = build_nr(0, 1, 1)
+        st = pf.flat_start(model.net, model.part)
+        case = onr.NrCase(model.y.csr, model.part.theta_block, model.part.q_block, st.theta, st.vmag)
+        case.fd()
+        _CPU["nr"] = (case, model)
+    else:
+        model = pf.build_zbus_model(__import__("paper_2605_14103_b200.fixtures", fromlist=["x"]).load_distribution(ZB_CASE))
+        _CPU["zb"] = (ozb.ZbCase(model.y_nn, model.v0, model.wye_idx, model.delta_p, model.delta_q,
+                                 model.voltage_floor), model)
+
+
+def _cpu_nr(args):
+    from oracle import nr as onr
+    p, q = args
+    return onr.newton(_CPU["nr"][0], p, q).converged
+
+
+def _cpu_zb(args):
+    from oracle import zbus as ozb
+    sw, sd = args
+    return ozb.zbus(_CPU["zb"][0], sw, sd).converged
+
+
+def cpu_throughput(kind: str, count: int, steps: int, warmup: int):
+    """Reference CPU algorithm over all host cores (fork pool, BLAS pinned to
+    one thread per worker, as the reference's run_batch does)."""
+    import multiprocessing as mp
+    from threadpoolctl import threadpool_limits
+    import paper_2605_14103_b200 as pf
+
+    cores = os.cpu_count() or 1
+    if kind == "nr":
+        model, _, _ = build_nr(0, 1, 1)
+        base = pf.transmission_base(model.net, model.part)
+        p, q = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=count, seed=NR_SEED))
+        work = list(zip(p, q))
+        fn = _cpu_nr
+    else:
+        zm, sw, sd = build_zb(0, 1, count)
+        work = list(zip(sw, sd))
+        fn = _cpu_zb
+    _cpu_init(kind)
+    ctx = mp.get_context("fork")
+    with threadpool_limits(limits=1):
+        with ctx.Pool(cores) as pool:
+            for _ in range(warmup):
+                pool.map(fn, work[:cores], chunksize=1)
+            t0 = time.perf_counter()
+            nconv = 0
+            for _ in range(steps):
+                nconv += sum(pool.map(fn, work, chunksize=max(1, len(work) // (cores * 4))))
+            t = time.perf_counter() - t0
+    return nconv / t, cores, t
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    rank, local, world = int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), \
+        int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = max(1, args.steps)
+        v, cores, t = cpu_throughput("nr", args.cpu_sample, steps, 1)
+        zv, zcores, zt = cpu_throughput("zb", args.cpu_sample, steps, 1)
+        line = {
+            "metric": METRIC, "value": v, "unit": "converged flows/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": t / steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded Philox load multipliers U[0.8,1.2] (reference generator)",
+            "impl": "reference",
+            "config": {"workload": f"GBnetwork ({NR_CASE}) Newton-Raphson, CPU sample of "
+                                   f"{args.cpu_sample} scenarios per step", "seed": NR_SEED},
+            "cpu_baseline": {"value": v, "unit": "converged flows/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.cpu_sample} {NR_CASE} scenarios x {steps} steps, "
+                                       f"oracle GMRES-FD Newton, fork pool of {cores}"},
+            "e2e": {"value": v, "unit": "converged flows/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "secondary": {"workload": f"EULV ({ZB_CASE}) Z-Bus", "value": zv,
+                          "unit": "converged flows/s", "cores": zcores,
+                          "sample": f"{args.cpu_sample} scenarios x {steps} steps"},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res, info = run_ours(args, rank, local, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, t = cpu_throughput("nr", args.cpu_sample, 1, 1)
+        zv, _, _ = cpu_throughput("zb", args.cpu_sample, 1, 1)
+        cpu = ({"value": v, "unit": "converged flows/s", "cores": cores, "kind": "port",
+                "sample": f"{args.cpu_sample} {NR_CASE} scenarios (seed {NR_SEED}), oracle "
+                          f"GMRES-FD Newton (reference algorithm), fork pool of {cores}"},
+               {"value": zv, "unit": "converged flows/s", "cores": cores, "kind": "port",
+                "sample": f"{args.cpu_sample} {ZB_CASE} scenarios (seed {ZB_SEED}), oracle LU Z-Bus"})
+    if rank == 0:
+        nr, zb = res["nr"], res["zb"]
+        line = {
+            "metric": METRIC, "value": nr["value"], "unit": "converged flows/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": nr["t"] / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded Philox load multipliers U[0.8,1.2] on the reference "
+                    "fixtures (reference generator, batch.py:45-60)",
+            "config": {"workload": f"GBnetwork ({NR_CASE}, 2224 buses) Newton-Raphson, "
+                                   f"{args.nr_batch} scenarios/GPU/step (BASELINE configs[2])",
+                       "batch_per_gpu": args.nr_batch, "global_batch": args.nr_batch * world,
+                       "seed": NR_SEED, "parallelism": f"scenario shards x{world}, no collective",
+                       "l2": "inputs (2.1 GB/GPU) larger than L2; no flush",
+                       "nnz_lu": info["nnz_lu"], "newton_iterations": nr["iterations"]},
+            "roofline": nr["roofline"],
+            "cpu_baseline": cpu[0] if cpu else None,
+            "e2e": nr["e2e"],
+            "gpu_launches": nr["launches"] + 0,
+            "clocks": nr["clocks"],
+            "secondary": {
+                "workload": f"EULV ({ZB_CASE}, 2724 phases) Z-Bus, {args.zb_batch} scenarios/GPU/step "
+                            "(BASELINE configs[3])",
+                "value": zb["value"], "unit": "converged flows/s",
+                "ms_per_step": zb["t"] / args.steps * 1e3, "roofline": zb["roofline"],
+                "e2e": zb["e2e"], "gpu_launches": zb["launches"], "clocks": zb["clocks"],
+                "iterations": zb["iterations"], "cpu_baseline": cpu[1] if cpu else None},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
