@@ -170,7 +170,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     const std::vector<int32_t> lperm = level_sorted_perm(first);
     build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block,
                       lperm.data());
-    build_nr_schedule(p->sym, y_rowptr, y_re, y_im, (int)env_int("ACPF_NR_CAP", 320), p->sch);
+    build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, (int)env_int("ACPF_NR_CAP", 320), p->sch);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;
@@ -187,8 +187,6 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   std::vector<int32_t> tpos(n_bus, -1), qpos(n_bus, -1);
   for (int k = 0; k < n_theta; ++k) tpos[theta_block[k]] = k;
   for (int k = 0; k < n_q; ++k) qpos[q_block[k]] = n_theta + k;
-  std::vector<double2> sy(s.nnz_lu);
-  for (int64_t t = 0; t < s.nnz_lu; ++t) sy[t] = make_double2(sc.slot_yr[t], sc.slot_yi[t]);
 
   NrDeviceModel& d = p->dm;
   d.n_bus = n_bus;
@@ -223,7 +221,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<int32_t**>(&d.tpos), tpos.data(), (size_t)n_bus);
   up(const_cast<int32_t**>(&d.qpos), qpos.data(), (size_t)n_bus);
   up(const_cast<int32_t**>(&d.ipos), s.ipos.data(), (size_t)nj);
-  up(const_cast<double2**>(&d.slot_y), sy.data(), sy.size());
+  up(const_cast<int32_t**>(&d.asm_ptr), sc.asm_ptr.data(), sc.asm_ptr.size());
+  up(const_cast<double2**>(&d.asm_y), reinterpret_cast<const double2*>(sc.asm_y.data()),
+     sc.asm_y.size() / 2);
+  up(const_cast<int32_t**>(&d.asm_j), sc.asm_j.data(), sc.asm_j.size());
+  up(const_cast<int4**>(&d.asm_slot), reinterpret_cast<const int4*>(sc.asm_slot.data()),
+     sc.asm_slot.size() / 4);
   up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
   up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
   up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());

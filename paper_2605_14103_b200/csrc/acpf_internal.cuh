@@ -28,7 +28,10 @@ struct NrDeviceModel {
   const int32_t* qpos;  // [n_bus] packed V index (>= n_theta) or -1
   const int32_t* ipos;  // [n_j] packed -> elimination position
   // streaming-Crout schedule (nr_symbolic.h NrSchedule)
-  const double2* slot_y;      // [nnz_lu] Ybus value feeding the slot
+  const int32_t* asm_ptr;     // [n_bus+1] Jacobian assembly list per bus
+  const double2* asm_y;       // [entries]
+  const int32_t* asm_j;       // [entries]
+  const int4* asm_slot;       // [entries] H, N, M, L slots (-1 absent)
   const uint32_t* slot_info;  // [nnz_lu]
   const uint32_t* brow;       // [n_j]
   const uint32_t* stream;     // [(n_seg+1)*32]

@@ -125,13 +125,16 @@ struct Streamer {
   int slot, off, len;
   uint32_t phase;
   int epoch;
+#ifdef ACPF_PROFILE_PHASES
+  long long t_wait = 0, t_issue = 0, n_wait = 0, n_issue = 0;
+#endif
 
   __device__ __forceinline__ void preload(int64_t k, uint32_t& win, uint32_t& mt) {
     win = stream[k * 32 + lane];
     mt = meta[k];
   }
 
-  __device__ void begin_step() {
+  __device__ __forceinline__ void begin_step() {
     k_iss = 0;
     k_cur = -1;
     off = len = 0;
@@ -140,7 +143,7 @@ struct Streamer {
     preload(n_seg > 0 ? 1 : 0, winB, metaB);
   }
 
-  __device__ void issue_one() {
+  __device__ __forceinline__ void issue_one() {
     const int s = (int)(iss_total % kNSeg);
     const int n = (int)(metaA & 63u);
     const uint32_t seg_base = ring + (uint32_t)s * 32 * kElemBytes;
@@ -168,13 +171,23 @@ struct Streamer {
     preload(nk, winB, metaB);
   }
 
-  __device__ void try_issue() {
+  __device__ __forceinline__ void try_issue() {
+#ifdef ACPF_PROFILE_PHASES
+    long long i0_ = clock64();
+#endif
     while (k_iss < n_seg && (k_iss - k_cur) <= kNSeg - (k_cur >= 0 ? 1 : 0) &&
-           (int)(metaA >> 6) <= epoch)
+           (int)(metaA >> 6) <= epoch) {
       issue_one();
+#ifdef ACPF_PROFILE_PHASES
+      ++n_issue;
+#endif
+    }
+#ifdef ACPF_PROFILE_PHASES
+    t_issue += clock64() - i0_;
+#endif
   }
 
-  __device__ void new_epoch(int e) {
+  __device__ __forceinline__ void new_epoch(int e) {
     epoch = e;
     // rows finished so far were written by this warp's lanes with st.global;
     // make them visible to the other lanes' cp.async reads
@@ -183,13 +196,20 @@ struct Streamer {
     try_issue();
   }
 
-  __device__ void advance() {
+  __device__ __forceinline__ void advance() {
     ++k_cur;
     if (k_cur > 0) ++cur_total;
     try_issue();
     if (k_iss <= k_cur) __trap();  // schedule bug: segment never issuable
     slot = (int)(cur_total % kNSeg);
+#ifdef ACPF_PROFILE_PHASES
+    long long w0_ = clock64();
+#endif
     mbar_wait(bar + slot * 8, (phase >> slot) & 1u);
+#ifdef ACPF_PROFILE_PHASES
+    t_wait += clock64() - w0_;
+    ++n_wait;
+#endif
     phase ^= 1u << slot;
     len = (int)lds_u32(rlen + slot * 4);
     off = 0;
@@ -207,10 +227,10 @@ struct Streamer {
     return v;
   }
 
-  __device__ void end_step() { ++cur_total; }
+  __device__ __forceinline__ void end_step() { ++cur_total; }
 };
 
-__global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io,
+__global__ void __launch_bounds__(32, 1) nr_stream_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io,
                                                        double tol, int max_newton) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
@@ -269,7 +289,16 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
   int status = 0, iters = 0;
   double fout = 0.0;
 
+#ifdef ACPF_PROFILE_PHASES
+  long long tA = 0, tB = 0, tC = 0, tD = 0, tq;
+#define PHASE_MARK(acc) do { long long now_ = clock64(); acc += now_ - tq; tq = now_; } while (0)
+#else
+#define PHASE_MARK(acc) do {} while (0)
+#endif
   for (int k = 0; k <= max_newton; ++k) {
+#ifdef ACPF_PROFILE_PHASES
+    tq = clock64();
+#endif
     // ---- A: phasors, min V
     double vmin = __longlong_as_double(0x7ff0000000000000LL);
     for (int i = r; i < m.n_bus; i += 4) {
@@ -283,6 +312,7 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
       vmin = fmin(vmin, v);
     }
     __syncwarp();
+    PHASE_MARK(tA);
     // ---- B: injections and mismatch
     double fmx = 0.0;
     int bad = 0;  // bit0 NaN, bit1 Inf
@@ -296,8 +326,6 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
         acc.x += y.x * ur - y.y * ui;
         acc.y += y.x * ui + y.y * ur;
       }
-      EL(m.off_i + 2 * i) = acc.x;
-      EL(m.off_i + 2 * i + 1) = acc.y;
       const double2 u = make_double2(EL(m.off_u + 2 * i), EL(m.off_u + 2 * i + 1));
       const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
       const int tp = m.tpos[i], qp = m.qpos[i];
@@ -312,6 +340,37 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
         bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
         fmx = fmx < fabs(f) ? fabs(f) : fmx;
         EL(m.off_yx + m.ipos[qp]) = -f;
+      }
+      // Jacobian blocks of row bus i straight into their LU slots
+      // (dense_jacobian formulas, transmission.py:383-407):
+      //   dS_i/dth_j = -j u_i conj(y u_j)        (j != i)
+      //   dS_i/dth_i =  j u_i conj(I_i - y u_i)
+      //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
+      //   H = Re dS/dth, N = Re dS/dV, M = Im dS/dth, L = Im dS/dV
+      const double2 ei = make_double2(EL(m.off_e + 2 * i), EL(m.off_e + 2 * i + 1));
+      const int a1 = m.asm_ptr[i + 1];
+      for (int a = m.asm_ptr[i]; a < a1; ++a) {
+        const double2 y = m.asm_y[a];
+        const int jb = m.asm_j[a];
+        const int4 sl = m.asm_slot[a];
+        const double2 uj = make_double2(EL(m.off_u + 2 * jb), EL(m.off_u + 2 * jb + 1));
+        const double2 ej = make_double2(EL(m.off_e + 2 * jb), EL(m.off_e + 2 * jb + 1));
+        double2 dth, dv;
+        const double2 wv = mul_conj(u, cmul(y, ej));
+        if (jb != i) {
+          const double2 wt = mul_conj(u, cmul(y, uj));
+          dth = make_double2(wt.y, -wt.x);
+          dv = wv;
+        } else {
+          const double2 yu = cmul(y, u);
+          const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
+          dth = make_double2(-wt.y, wt.x);
+          dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
+        }
+        if (sl.x >= 0) EL(m.off_lu + sl.x) = dth.x;
+        if (sl.y >= 0) EL(m.off_lu + sl.y) = dv.x;
+        if (sl.z >= 0) EL(m.off_lu + sl.z) = dth.y;
+        if (sl.w >= 0) EL(m.off_lu + sl.w) = dv.y;
       }
     }
     // quad reductions (order independent: max / min / or)
@@ -344,108 +403,97 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
         fout = fmx;
       }
     }
+    PHASE_MARK(tB);
     if (__all_sync(kFull, done)) break;
 
-    // ---- C: assembly + Crout refactorisation + forward substitution
+    // ---- C: Crout refactorisation + forward substitution
     st.begin_step();
     st.new_epoch(0);
     bool zero_pivot = false;
     int64_t t = 0;  // LU slot
-    // slot descriptor windows (lane j holds slot w0 + j), double buffered
+    // slot control words (lane j holds slot w0 + j), double buffered
     int64_t w0 = 0;
-    double wyr = 0, wyi = 0, nyr = 0, nyi = 0;
-    uint32_t winfo = 0, ninfo = 0;
-    if (lane < m.nnz_lu) {
-      wyr = m.slot_y[lane].x;
-      wyi = m.slot_y[lane].y;
-      winfo = m.slot_info[lane];
-    }
-    if (32 + lane < m.nnz_lu) {
-      nyr = m.slot_y[32 + lane].x;
-      nyi = m.slot_y[32 + lane].y;
-      ninfo = m.slot_info[32 + lane];
-    }
+    uint32_t winfo = lane < m.nnz_lu ? m.slot_info[lane] : 0u;
+    uint32_t ninfo = 32 + lane < m.nnz_lu ? m.slot_info[32 + lane] : 0u;
     int epoch = 0;
     for (int p = 0; p < m.n_j; ++p) {
-      double ur = 0, ui = 0, Ir = 0, Ii = 0, yacc = 0;
+      double yacc = 0.0;
       int pos = 0;  // position within the row
       for (;;) {
         if (t - w0 == 32) {
           w0 += 32;
-          wyr = nyr;
-          wyi = nyi;
           winfo = ninfo;
           const int64_t nt = w0 + 32 + lane;
-          if (nt < m.nnz_lu) {
-            nyr = m.slot_y[nt].x;
-            nyi = m.slot_y[nt].y;
-            ninfo = m.slot_info[nt];
-          }
+          if (nt < m.nnz_lu) ninfo = m.slot_info[nt];
         }
-        const int j = (int)(t - w0);
-        const uint32_t info = __shfl_sync(kFull, winfo, j);
-        if (info & kSlotRowStart) {
-          if (info & kSlotNewEpoch) st.new_epoch(++epoch);
-          ur = st.get();
-          ui = st.get();
-          Ir = st.get();
-          Ii = st.get();
-          yacc = st.get();
-        }
-        const int type = info & 15u;
-        double a = 0.0;
-        if (type < 8) {
-          const double yr = __shfl_sync(kFull, wyr, j);
-          const double yi = __shfl_sync(kFull, wyi, j);
-          const double xr = st.get(), xi = st.get();  // u_j (theta col) or E_j (V col)
-          const double2 y = make_double2(yr, yi);
-          const double2 ui2 = make_double2(ur, ui);
-          const bool diag = type & 4, qrow = type & 2;
-          if (type & 1) {  // d/dV_j: u_i conj(y E_j) [+ conj(I_i) E_i]
-            const double2 wv = mul_conj(ui2, cmul(y, make_double2(xr, xi)));
-            if (!diag)
-              a = qrow ? wv.y : wv.x;
-            else
-              a = qrow ? wv.y + (Ir * xi - Ii * xr) : wv.x + (Ir * xr + Ii * xi);
-          } else if (!diag) {  // -j u_i conj(y u_j)
-            const double2 wv = mul_conj(ui2, cmul(y, make_double2(xr, xi)));
-            a = qrow ? -wv.x : wv.y;
-          } else {  // j u_i conj(I_i - y u_i)
-            const double2 yu = cmul(y, ui2);
-            const double2 wv = mul_conj(ui2, make_double2(Ir - yu.x, Ii - yu.y));
-            a = qrow ? wv.x : -wv.y;
-          }
-        }
-        int cnt = (int)(info >> 16);
-        if (cnt) {
-          double part = 0.0;
-          while (cnt > 0) {
+        const uint32_t info = __shfl_sync(kFull, winfo, (int)(t - w0));
+        if (info & kSlotNewEpoch) st.new_epoch(++epoch);
+        const int cnt = (int)(info >> 16);
+        const bool lslot = info & kSlotL, fill = info & kSlotFill;
+        const int head = ((info & kSlotRowStart) ? 1 : 0) + (fill ? 0 : 1);
+        const int need = head + cnt + (lslot ? 2 : 0);
+        double a = 0.0, inv = 0.0, yc = 0.0;
+        if (need <= 32) {
+          // the whole unit sits in one ring segment (schedule guarantee)
+          if (need) {
             if (st.off == st.len) st.advance();
-            const int nb = min(cnt, st.len - st.off);
-            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off) * 2;
-            const uint32_t ra = st.elem(st.off);
+          }
+          const uint32_t e0 = st.elem(st.off);
+          int o = 0;
+          if (info & kSlotRowStart) yacc = lds_f64(e0 + (o++) * kElemBytes);
+          if (!fill) a = lds_f64(e0 + (o++) * kElemBytes);
+          if (cnt) {
+            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off + o) * 2;
+            const uint32_t ra = e0 + o * kElemBytes;
+            double part = 0.0;
             if (no_spill) {
 #pragma unroll 2
-              for (int q = r; q < nb; q += 4) {
-                const uint32_t lp = lds_u16(la + 2 * q);
-                part = fma(-lds_f64(lbuf_sc + lp * kElemBytes), lds_f64(ra + q * kElemBytes), part);
-              }
+              for (int q = r; q < cnt; q += 4)
+                part = fma(-lds_f64(lbuf_sc + lds_u16(la + 2 * q) * kElemBytes),
+                           lds_f64(ra + q * kElemBytes), part);
             } else {
-              for (int q = r; q < nb; q += 4) {
+              for (int q = r; q < cnt; q += 4) {
                 const int lp = (int)lds_u16(la + 2 * q);
                 const double l = lp < m.cap ? lds_f64(lbuf_sc + lp * kElemBytes)
                                             : EL(m.off_spill + (lp - m.cap));
                 part = fma(-l, lds_f64(ra + q * kElemBytes), part);
               }
             }
+            a = a + quad_sum(part);
+            o += cnt;
+          }
+          if (lslot) {
+            inv = lds_f64(e0 + o * kElemBytes);
+            yc = lds_f64(e0 + (o + 1) * kElemBytes);
+          }
+          st.off += need;
+        } else {
+          // long unit: generic path across segment boundaries
+          if (info & kSlotRowStart) yacc = st.get();
+          if (!fill) a = st.get();
+          double part = 0.0;
+          int rem = cnt;
+          while (rem > 0) {
+            if (st.off == st.len) st.advance();
+            const int nb = min(rem, st.len - st.off);
+            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off) * 2;
+            const uint32_t ra = st.elem(st.off);
+            for (int q = r; q < nb; q += 4) {
+              const int lp = (int)lds_u16(la + 2 * q);
+              const double l = lp < m.cap ? lds_f64(lbuf_sc + lp * kElemBytes)
+                                          : EL(m.off_spill + (lp - m.cap));
+              part = fma(-l, lds_f64(ra + q * kElemBytes), part);
+            }
             st.off += nb;
-            cnt -= nb;
+            rem -= nb;
           }
           a = a + quad_sum(part);
+          if (lslot) {
+            inv = st.get();
+            yc = st.get();
+          }
         }
-        if (info & kSlotL) {
-          const double inv = st.get();
-          const double yc = st.get();
+        if (lslot) {
           a *= inv;
           yacc = fma(-a, yc, yacc);
           // every quad lane holds the same value: each writes it, so each
@@ -467,6 +515,7 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
       }
       if (r == 0) EL(m.off_yx + p) = yacc;
     }
+    PHASE_MARK(tC);
     // ---- D: back substitution (rows by back level)
     st.new_epoch(m.n_levels);
     epoch = m.n_levels;
@@ -482,30 +531,42 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
       if (b >> 31) st.new_epoch(++epoch);
       const int p = (int)(b & 0xfffffu);
       int rem = (int)((b >> 20) & 0x7ffu);
-      const double y0 = st.get();
-      const double inv = st.get();
-      double part = 0.0;
-      while (rem > 0) {
+      double y0, inv, part = 0.0;
+      const int need = 2 + 2 * rem;
+      if (need <= 32) {
         if (st.off == st.len) st.advance();
-        const int nb = min(rem, (st.len - st.off) >> 1);
-        if (nb == 0) {  // a (u, x) pair straddles two segments
-          const double u = st.get();
-          const double x = st.get();
-          if (r == 0) part = fma(-u, x, part);
-          --rem;
-          continue;
+        const uint32_t e0 = st.elem(st.off);
+        y0 = lds_f64(e0);
+        inv = lds_f64(e0 + kElemBytes);
+        for (int q = r; q < rem; q += 4)
+          part = fma(-lds_f64(e0 + (2 + 2 * q) * kElemBytes), lds_f64(e0 + (3 + 2 * q) * kElemBytes), part);
+        st.off += need;
+      } else {
+        y0 = st.get();
+        inv = st.get();
+        while (rem > 0) {
+          if (st.off == st.len) st.advance();
+          const int nb = min(rem, (st.len - st.off) >> 1);
+          if (nb == 0) {  // a (u, x) pair straddles two segments
+            const double u = st.get();
+            const double x = st.get();
+            if (r == 0) part = fma(-u, x, part);
+            --rem;
+            continue;
+          }
+          const uint32_t ra = st.elem(st.off);
+          for (int q = r; q < nb; q += 4)
+            part = fma(-lds_f64(ra + 2 * q * kElemBytes), lds_f64(ra + (2 * q + 1) * kElemBytes), part);
+          st.off += 2 * nb;
+          rem -= nb;
         }
-        const uint32_t ra = st.elem(st.off);
-        for (int q = r; q < nb; q += 4)
-          part = fma(-lds_f64(ra + 2 * q * kElemBytes), lds_f64(ra + (2 * q + 1) * kElemBytes), part);
-        st.off += 2 * nb;
-        rem -= nb;
       }
       const double x = (y0 + quad_sum(part)) * inv;
       if (r == 0) EL(m.off_yx + p) = x;
     }
     st.end_step();
     __syncwarp();
+    PHASE_MARK(tD);
     // per scenario: every lane of a quad saw the same pivots
     zero_pivot = zero_pivot || __shfl_xor_sync(kFull, (int)zero_pivot, 8) ||
                  __shfl_xor_sync(kFull, (int)zero_pivot, 16);
@@ -525,6 +586,11 @@ __global__ void __launch_bounds__(32) nr_stream_kernel(NrDeviceModel m, NrWorksp
     __syncwarp();
   }
 
+#ifdef ACPF_PROFILE_PHASES
+  if (g == 0 && lane == 0)
+    printf("phase cycles A %lld B %lld C %lld D %lld | wait %lld (%lld) issue %lld (%lld)\n", tA, tB, tC,
+           tD, st.t_wait, st.n_wait, st.t_issue, st.n_issue);
+#endif
   if (!valid) return;
   for (int i = r; i < m.n_bus; i += 4) {
     io.theta_out[s * m.n_bus + i] = EL(m.off_th + i);

@@ -265,9 +265,8 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
   return perm;
 }
 
-void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const double* y_re,
-                       const double* y_im, int cap_limit, NrSchedule& o) {
-  (void)y_rowptr;
+void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
+                       const double* y_re, const double* y_im, int cap_limit, NrSchedule& o) {
   const int nj = s.n_j, nb = s.n_bus;
   // ---- arena layout
   int64_t e = 0;
@@ -288,8 +287,56 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const doubl
   if (o.n_elem >= (1 << 22)) throw std::length_error("arena exceeds 22-bit gather index");
   if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 entries");
 
+  // ---- per-bus assembly lists (phase B of the kernel): for every Ybus entry
+  // (i, j) plus the diagonal bus block, the LU slots of the H, N, M, L
+  // derivatives it feeds (-1 where the unknown/equation does not exist)
+  std::vector<int64_t> where(nj, -1);
+  std::vector<int> tpos(nb, -1), qpos(nb, -1);
+  for (int p = 0; p < nj; ++p) {
+    const int var = s.perm[p];
+    if (var < s.n_theta) tpos[s.row_bus[p]] = p; else qpos[s.row_bus[p]] = p;
+  }
+  o.asm_ptr.assign(nb + 1, 0);
+  o.asm_y.clear();
+  o.asm_j.clear();
+  o.asm_slot.clear();
+  for (int i = 0; i < nb; ++i) {
+    bool have_diag = false;
+    for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) have_diag |= (y_col[k] == i);
+    auto emit = [&](int j, double yr, double yi) {
+      int32_t sl[4] = {-1, -1, -1, -1};  // H (P,theta) N (P,V) M (Q,theta) L (Q,V)
+      const int rows[2] = {tpos[i], qpos[i]};
+      const int cols[2] = {tpos[j], qpos[j]};
+      for (int a = 0; a < 2; ++a) {
+        if (rows[a] < 0) continue;
+        const int p = rows[a];
+        for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
+        for (int b = 0; b < 2; ++b)
+          if (cols[b] >= 0) {
+            const int64_t t = where[cols[b]];
+            if (t < 0) throw std::logic_error("assembly slot missing");
+            sl[a * 2 + b] = (int32_t)t;
+          }
+        for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = -1;
+      }
+      if (sl[0] < 0 && sl[1] < 0 && sl[2] < 0 && sl[3] < 0) return;
+      o.asm_y.push_back(yr);
+      o.asm_y.push_back(yi);
+      o.asm_j.push_back(j);
+      for (int a = 0; a < 4; ++a) o.asm_slot.push_back(sl[a]);
+    };
+    if (!have_diag) emit(i, 0.0, 0.0);
+    for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) emit(y_col[k], y_re[k], y_im[k]);
+    o.asm_ptr[i + 1] = (int32_t)o.asm_j.size();
+  }
+
   // ---- levels
-  const std::vector<int> lev = factor_levels(s);
+  std::vector<int> lev(nj, 0);
+  for (int p = 0; p < nj; ++p) {
+    int l = 0;
+    for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) l = std::max(l, lev[s.col[t]] + 1);
+    lev[p] = l;
+  }
   std::vector<int> blev(nj, 0);
   for (int p = nj - 1; p >= 0; --p) {
     int l = 0;
@@ -304,55 +351,62 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const doubl
     if (p && lev[p] < lev[p - 1]) throw std::logic_error("rows not level-sorted");
   }
 
-  // ---- stream construction
-  std::vector<uint32_t> flat;     // gidx | lpos << 22
-  std::vector<int> flat_epoch;
-  auto push = [&](int64_t gidx, int lpos, int epoch) {
-    flat.push_back((uint32_t)gidx | ((uint32_t)lpos << 22));
-    flat_epoch.push_back(epoch);
+  // ---- stream: a list of "units" (one per LU slot, one per back row); a
+  // unit's gathers never straddle a segment when it has <= kSeg of them
+  o.stream.clear();
+  o.segmeta.clear();
+  std::vector<uint32_t> seg;
+  int seg_epoch = -1;
+  auto close = [&]() {
+    if (seg.empty()) return;
+    o.segmeta.push_back((uint32_t)seg.size() | ((uint32_t)seg_epoch << 6));
+    for (uint32_t w : seg) o.stream.push_back(w);
+    for (size_t k = seg.size(); k < (size_t)kSeg; ++k) o.stream.push_back(0u);
+    seg.clear();
   };
-  o.slot_yr.assign(s.nnz_lu, 0.0);
-  o.slot_yi.assign(s.nnz_lu, 0.0);
+  std::vector<uint32_t> unit;
+  auto flush_unit = [&](int epoch) {
+    if (epoch != seg_epoch) {
+      close();
+      seg_epoch = epoch;
+    }
+    if (unit.size() <= (size_t)kSeg && seg.size() + unit.size() > (size_t)kSeg) close();
+    for (uint32_t w : unit) {
+      if (seg.size() == (size_t)kSeg) close();
+      seg.push_back(w);
+    }
+    unit.clear();
+  };
+  auto gw = [&](int64_t gidx, int lpos) { unit.push_back((uint32_t)gidx | ((uint32_t)lpos << 22)); };
   o.slot_info.assign(s.nnz_lu, 0);
+  o.n_stream = 0;
   for (int p = 0; p < nj; ++p) {
-    const int ep = lev[p];
-    const int bi = s.row_bus[p];
-    push(o.off_u + 2 * bi, 0, ep);
-    push(o.off_u + 2 * bi + 1, 0, ep);
-    push(o.off_i + 2 * bi, 0, ep);
-    push(o.off_i + 2 * bi + 1, 0, ep);
-    push(o.off_yx + p, 0, ep);
     const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
     for (int64_t t = r0; t < r1; ++t) {
-      uint32_t info = s.slot_type[t];
+      uint32_t info = 0;
       if (t == r0) info |= kSlotRowStart;
       if (t == r0 && p > 0 && lev[p] != lev[p - 1]) info |= kSlotNewEpoch;
       if (t == s.diag[p]) info |= kSlotDiag;
       if (t == r1 - 1) info |= kSlotRowEnd;
       if (t < s.diag[p]) info |= kSlotL;
+      const bool fill = s.slot_type[t] == 8;
+      if (fill) info |= kSlotFill;
       const int64_t cnt = s.pair_ptr[t + 1] - s.pair_ptr[t];
       if (cnt >= 65536) throw std::length_error("too many updates for one slot");
       info |= (uint32_t)cnt << 16;
       o.slot_info[t] = info;
-      if (s.slot_type[t] < 8) {
-        const int j = s.slot_jbus[t];
-        if (s.slot_ynz[t] >= 0) {
-          o.slot_yr[t] = y_re[s.slot_ynz[t]];
-          o.slot_yi[t] = y_im[s.slot_ynz[t]];
-        }
-        const int64_t base = (s.slot_type[t] & 1) ? o.off_e : o.off_u;
-        push(base + 2 * j, 0, ep);
-        push(base + 2 * j + 1, 0, ep);
-      }
+      if (t == r0) gw(o.off_yx + p, 0);          // b_p (rhs, written by the mismatch phase)
+      if (!fill) gw(o.off_lu + t, 0);            // assembled Jacobian value
       for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
-        push(o.off_lu + s.pair_u[q], (int)(s.pair_l[q] - r0), ep);
+        gw(o.off_lu + s.pair_u[q], (int)(s.pair_l[q] - r0));
       if (t < s.diag[p]) {
-        push(o.off_invd + s.col[t], 0, ep);
-        push(o.off_yx + s.col[t], 0, ep);
+        gw(o.off_invd + s.col[t], 0);
+        gw(o.off_yx + s.col[t], 0);
       }
+      o.n_stream += (int64_t)unit.size();
+      flush_unit(lev[p]);
     }
   }
-  // back rows: by back level, descending p within a level
   std::vector<int32_t> border(nj);
   for (int p = 0; p < nj; ++p) border[p] = p;
   std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
@@ -366,27 +420,16 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const doubl
     if (p >= (1 << 20) || cnt >= 2048) throw std::length_error("back row too large");
     o.brow[r] = (uint32_t)p | ((uint32_t)cnt << 20) |
                 ((r > 0 && blev[p] != blev[border[r - 1]]) ? (1u << 31) : 0u);
-    push(o.off_yx + p, 0, ep);
-    push(o.off_invd + p, 0, ep);
+    gw(o.off_yx + p, 0);
+    gw(o.off_invd + p, 0);
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
-      push(o.off_lu + t, 0, ep);
-      push(o.off_yx + s.col[t], 0, ep);
+      gw(o.off_lu + t, 0);
+      gw(o.off_yx + s.col[t], 0);
     }
+    o.n_stream += (int64_t)unit.size();
+    flush_unit(ep);
   }
-  o.n_stream = (int64_t)flat.size();
-  // ---- segment: at most kSeg words, never across an epoch change
-  o.stream.clear();
-  o.segmeta.clear();
-  size_t i = 0;
-  while (i < flat.size()) {
-    const int ep = flat_epoch[i];
-    size_t j = i;
-    while (j < flat.size() && j - i < (size_t)kSeg && flat_epoch[j] == ep) ++j;
-    for (size_t k = i; k < j; ++k) o.stream.push_back(flat[k]);
-    for (size_t k = j - i; k < (size_t)kSeg; ++k) o.stream.push_back(0u);
-    o.segmeta.push_back((uint32_t)(j - i) | ((uint32_t)ep << 6));
-    i = j;
-  }
+  close();
   o.n_seg = (int64_t)o.segmeta.size();
   // sentinel segment (never issued): epoch beyond every consumer epoch
   for (int k = 0; k < kSeg; ++k) o.stream.push_back(0u);

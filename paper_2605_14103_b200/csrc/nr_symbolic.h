@@ -35,9 +35,13 @@ struct NrSchedule {
   int max_l = 0;     // longest L part of any row
   int n_levels = 0;  // factor levels (etree height)
   int n_blevels = 0; // back-substitution levels
+  // per-bus Jacobian assembly lists: entries asm_ptr[i]..asm_ptr[i+1]
+  std::vector<int32_t> asm_ptr;
+  std::vector<double> asm_y;      // [entries][2] Ybus value (0 for a missing diagonal)
+  std::vector<int32_t> asm_j;     // [entries] column bus
+  std::vector<int32_t> asm_slot;  // [entries][4] LU slot of H, N, M, L (or -1)
   // factor slots in slot order
-  std::vector<double> slot_yr, slot_yi;
-  std::vector<uint32_t> slot_info;  // type(4) | flags(4) | cnt << 16
+  std::vector<uint32_t> slot_info;  // flags | cnt << 16
   // back rows in back order: p | cnt << 20 | new_epoch << 31
   std::vector<uint32_t> brow;
   // segmented stream: 32 words per segment, word = gidx | lpos << 22
@@ -53,10 +57,11 @@ constexpr uint32_t kSlotDiag = 1u << 5;
 constexpr uint32_t kSlotRowEnd = 1u << 6;
 constexpr uint32_t kSlotNewEpoch = 1u << 7;
 constexpr uint32_t kSlotL = 1u << 8;
+constexpr uint32_t kSlotFill = 1u << 9;
 constexpr int kSeg = 32;
 
-void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const double* y_re,
-                       const double* y_im, int cap_limit, NrSchedule& out);
+void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
+                       const double* y_re, const double* y_im, int cap_limit, NrSchedule& out);
 
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
