@@ -89,6 +89,7 @@ struct acpf_nr_plan {
   int device = 0;
   NrSymbolic sym;
   NrSchedule sch;
+  NrHostSchedule hs{};
   NrDeviceModel dm{};
   DevArena model;
   DevArena work;
@@ -98,6 +99,7 @@ struct acpf_nr_plan {
   DevArena stage;
   size_t stage_bytes = 0;
   void* stage_base = nullptr;
+  int* host_active = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
@@ -170,7 +172,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     const std::vector<int32_t> lperm = level_sorted_perm(first);
     build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block,
                       lperm.data());
-    build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, (int)env_int("ACPF_NR_CAP", 320), p->sch);
+    build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;
@@ -194,7 +196,6 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.n_q = n_q;
   d.n_j = nj;
   d.nnz_lu = s.nnz_lu;
-  d.n_seg = sc.n_seg;
   d.n_elem = sc.n_elem;
   d.off_lu = sc.off_lu;
   d.off_invd = sc.off_invd;
@@ -205,10 +206,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.off_spec = sc.off_spec;
   d.off_th = sc.off_th;
   d.off_vm = sc.off_vm;
-  d.off_spill = sc.off_spill;
-  d.cap = sc.cap;
-  d.max_l = sc.max_l;
-  d.n_levels = sc.n_levels;
+  p->hs.level_ptr = sc.level_ptr.data();
+  p->hs.level_maxl = sc.level_maxl.data();
+  p->hs.blevel_ptr = sc.blevel_ptr.data();
+  p->hs.n_levels = sc.n_levels;
+  p->hs.n_blevels = sc.n_blevels;
+  p->hs.max_l = sc.max_l;
   cudaError_t e = cudaSuccess;
   auto up = [&](auto** dst, const auto* src, size_t cnt) {
     if (e == cudaSuccess) e = p->model.upload(dst, src, cnt);
@@ -228,9 +231,11 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<int4**>(&d.asm_slot), reinterpret_cast<const int4*>(sc.asm_slot.data()),
      sc.asm_slot.size() / 4);
   up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
+  up(const_cast<int32_t**>(&d.row_slot), sc.row_slot.data(), sc.row_slot.size());
+  up(const_cast<int32_t**>(&d.row_sptr), sc.row_sptr.data(), sc.row_sptr.size());
   up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
+  up(const_cast<int32_t**>(&d.brow_sptr), sc.brow_sptr.data(), sc.brow_sptr.size());
   up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());
-  up(const_cast<uint32_t**>(&d.segmeta), sc.segmeta.data(), sc.segmeta.size());
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
   if (e != cudaSuccess) {
@@ -238,7 +243,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     delete p;
     return e == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;
   }
-  p->bytes_per_group = sc.n_elem * kGroup * 8;
+  p->bytes_per_group = sc.n_elem * kGroup * 8 + (int64_t)nr_group_state_bytes();
   *out = p;
   return ACPF_OK;
 }
@@ -285,16 +290,42 @@ static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
   if (p->ws_groups >= groups) return ACPF_OK;
   p->work.release();
   p->ws_groups = 0;
+  const size_t S = (size_t)groups * kGroup;
+  NrWorkspace& w = p->ws;
   void* ptr = nullptr;
-  if (p->work.alloc(&ptr, (size_t)groups * p->bytes_per_group) != cudaSuccess) {
+  bool ok = true;
+  auto get = [&](size_t bytes) -> void* {
+    if (!ok || p->work.alloc(&ptr, bytes) != cudaSuccess) {
+      ok = false;
+      return nullptr;
+    }
+    return ptr;
+  };
+  w.arena = (double*)get((size_t)groups * p->sch.n_elem * kGroup * 8);
+  w.fmax_bits = (unsigned long long*)get(S * 8);
+  w.flags = (int*)get(S * 4);
+  w.status = (int*)get(S * 4);
+  w.iters = (int*)get(S * 4);
+  w.fout = (double*)get(S * 8);
+  w.active = (uint8_t*)get(S);
+  w.gactive = (int*)get((size_t)groups * 4);
+  w.n_active = (int*)get(4);
+  if (!ok) {
     p->work.release();
     cudaGetLastError();
     set_error("acpf_nr_solve: device workspace allocation failed (" + std::to_string(groups) +
               " groups); lower ACPF_NR_CHUNK");
     return ACPF_ENOMEM;
   }
-  p->ws.arena = (double*)ptr;
-  p->ws.groups = groups;
+  if (!p->host_active) {
+    if (cudaMallocHost(&p->host_active, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("pinned host allocation failed");
+      return ACPF_ENOMEM;
+    }
+  }
+  w.host_active = p->host_active;
+  w.groups = groups;
   p->ws_groups = groups;
   return ACPF_OK;
 }
@@ -335,7 +366,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     const int64_t have_groups = p->ws_groups;
     const int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
     int64_t groups = std::max<int64_t>(1, budget / std::max<int64_t>(1, p->bytes_per_group));
-    groups = std::min<int64_t>(groups, 16384);
+    groups = std::min<int64_t>(groups, 4096);
     chunk = groups * kGroup;
   }
   chunk = std::min<int64_t>(chunk, batch);
@@ -397,9 +428,12 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
       io.converged = cv;
     }
     ACPF_CUDA(cudaEventRecord(p->ev0, st));
-    ACPF_CUDA(launch_nr_newton(d, p->ws, io, tol_mismatch, max_newton, st));
+    int nl = 0;
+    NrWorkspace wsb = p->ws;  // capacity may exceed this chunk: index by the chunk's groups
+    wsb.groups = (nb + kGroup - 1) / kGroup;
+    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol_mismatch, max_newton, st, &nl));
     ACPF_CUDA(cudaEventRecord(p->ev1, st));
-    ++launches;
+    launches += nl;
     if (!dev_ptrs) {
       ACPF_CUDA(cudaMemcpyAsync(theta_out + s0 * d.n_bus, io.theta_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
       ACPF_CUDA(cudaMemcpyAsync(vmag_out + s0 * d.n_bus, io.vmag_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
@@ -437,6 +471,7 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
     DeviceGuard dg(p->device);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->host_active) cudaFreeHost(p->host_active);
     p->work.release();
     p->stage.release();
     p->model.release();

@@ -12,7 +12,7 @@ namespace acpf {
 
 void set_error(const std::string& msg);
 
-constexpr int kGroup = 8;  // NR: scenarios per warp (a quad of lanes each)
+constexpr int kGroup = 32;  // NR: scenarios per warp (one lane each)
 
 // ---------------------------------------------------------------------------
 // Newton plan (device side view passed to the kernel by value)
@@ -27,27 +27,42 @@ struct NrDeviceModel {
   const int32_t* tpos;  // [n_bus] packed theta index or -1
   const int32_t* qpos;  // [n_bus] packed V index (>= n_theta) or -1
   const int32_t* ipos;  // [n_j] packed -> elimination position
-  // streaming-Crout schedule (nr_symbolic.h NrSchedule)
+  // level-synchronous Crout schedule (nr_symbolic.h NrSchedule)
   const int32_t* asm_ptr;     // [n_bus+1] Jacobian assembly list per bus
   const double2* asm_y;       // [entries]
   const int32_t* asm_j;       // [entries]
   const int4* asm_slot;       // [entries] H, N, M, L slots (-1 absent)
   const uint32_t* slot_info;  // [nnz_lu]
+  const int32_t* row_slot;    // [n_j+1]
+  const int32_t* row_sptr;    // [n_j+1]
   const uint32_t* brow;       // [n_j]
-  const uint32_t* stream;     // [(n_seg+1)*32]
-  const uint32_t* segmeta;    // [n_seg+1]
-  int64_t n_seg;
+  const int32_t* brow_sptr;   // [n_j+1]
+  const uint32_t* stream;     // [n_stream]
   int64_t nnz_lu;
   int64_t n_elem;
-  int64_t off_lu, off_invd, off_yx, off_u, off_e, off_i, off_spec, off_th, off_vm, off_spill;
-  int cap;
-  int max_l;
-  int n_levels;
+  int64_t off_lu, off_invd, off_yx, off_u, off_e, off_i, off_spec, off_th, off_vm;
+};
+
+struct NrHostSchedule {
+  const int32_t* level_ptr;   // [n_levels+1]
+  const int32_t* level_maxl;  // [n_levels]
+  const int32_t* blevel_ptr;  // [n_blevels+1]
+  int n_levels, n_blevels, max_l;
 };
 
 struct NrWorkspace {
   double* arena;  // [groups][n_elem][kGroup]
   int64_t groups;
+  // per scenario [groups*kGroup]
+  unsigned long long* fmax_bits;
+  int* flags;
+  int* status;
+  int* iters;
+  double* fout;
+  uint8_t* active;
+  int* gactive;     // [groups]
+  int* n_active;    // device counter
+  int* host_active; // pinned host mirror
 };
 
 struct NrBatchIO {
@@ -63,8 +78,10 @@ struct NrBatchIO {
 };
 
 size_t nr_smem_bytes(int cap);
-cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrWorkspace& w, const NrBatchIO& io,
-                             double tol, int max_newton, cudaStream_t stream);
+size_t nr_group_state_bytes();
+cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
+                             const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
+                             int* launches);
 
 // ---------------------------------------------------------------------------
 // Z-Bus plan

@@ -1,36 +1,37 @@
-// Batched polar Newton-Raphson on sm_100a, streaming-Crout formulation.
+// Batched polar Newton-Raphson on sm_100a: level-synchronous sparse LU.
 //
-// Layout: one warp = one group of kGroup = 8 scenarios; each scenario owns a
-// quad of lanes (lane = r*8 + sc, sub-lane r = 0..3, scenario sc = 0..7).
-// Every per-scenario quantity lives in a per-group arena of "elements":
-// element e of scenario sc at arena[e*8 + sc], so one element of a group is
-// 64 contiguous bytes and a warp instruction touching 4 elements is four
-// fully used 64-byte segments. The schedule (LU pattern, Crout updates,
-// Ybus values) is shared by all groups and read as warp-uniform data.
+// Data layout: scenarios are processed in groups of kGroup = 32 (one lane
+// each); every per-scenario quantity lives in a per-group arena of
+// "elements", element e of lane l at arena[e*32 + l], so every warp access to
+// one element is a single coalesced 256-byte transaction. The schedule
+// (Ybus, LU pattern, Crout updates) is shared by all groups.
 //
-// One launch runs the whole Newton loop of the reference `_newton_loop`
-// (transmission.py:333-380) for its group with no host round trip:
-//   A  phasors      u = V e^{j theta}                     (transmission.py:196)
-//   B  mismatch     I = Y u, S = u conj(I), F, ||F||inf    (transmission.py:194-215)
-//      exit checks in the reference order: non-finite -> converged ->
-//      min V <= 0 -> k == max_newton                     (transmission.py:347-359)
-//   C  Jacobian assembly fused into a row-by-row (Crout, dot-product form)
-//      static-pivot sparse LU refactorisation with the forward substitution
-//      fused in (replaces the GMRES/FD step solve, transmission.py:361-369);
-//   D  back substitution, x += dx                         (transmission.py:378)
-// A, B and D split buses/updates over the four sub-lanes of a scenario.
+// One Newton step of the reference `_newton_loop` (transmission.py:333-380)
+// for the whole batch is a short sequence of launches on one stream:
+//   nr_phasor    u = V e^{j theta}, E = e^{j theta}; V <= 0 flag  (transmission.py:196, :355)
+//   nr_mismatch  I = Y u, S = u conj(I), F -> rhs, ||F||inf, non-finite flags
+//                (transmission.py:194-215), and the Jacobian blocks H, N, M, L
+//                of every Ybus entry straight into their LU slots
+//                (dense_jacobian formulas, transmission.py:383-407)
+//   nr_check     the reference exit checks in order: non-finite -> converged
+//                -> min V <= 0 -> k == max_newton (transmission.py:347-359)
+//   nr_factor    one launch per elimination level: every (row of the level,
+//                group) pair is an independent warp task that computes the
+//                row by Crout (dot-product) updates + fused forward
+//                substitution; rows of one level never read each other
+//   nr_back      one launch per back-substitution level
+//   nr_update    x += dx (transmission.py:378)
+// This replaces the reference's FD-preconditioned GMRES step
+// (transmission.py:361-369) by an exact static-pivot sparse LU solve.
 //
-// C and D are driven by one precomputed *gather stream*: every operand not
-// produced inside the current row (earlier U rows, pivots, y/x entries,
-// phasors) is an element index in the stream. The warp prefetches the stream
-// ahead of use with cp.async (LDGSTS, 8 B per lane, 4 elements per warp
-// instruction) into a shared-memory ring; completion is tracked by one
-// mbarrier per 32-element segment. Rows are level-sorted (same fill), so
-// prefetch runs across row boundaries and only drains where a level starts.
-// The Crout updates of one LU slot are split over the quad (4 partial dot
-// products, combined by a fixed butterfly), and the current row's L part
-// never leaves shared memory (later rows only read U), so global traffic is
-// the gathers of earlier U rows plus one write per U slot.
+// Inside a factor/back task every operand that is not produced by the task
+// itself (earlier U rows, pivots, y/x, assembled J values) is a precomputed
+// element index in a gather stream; the warp runs a cp.async (LDGSTS)
+// multistage pipeline over its stream (8 elements per stage, 7 stages in
+// flight) into a shared-memory ring. No stream element of a task can be
+// produced by another task of the same level, so the pipeline needs no
+// hazard checks. The task's own L values stay in shared memory (later rows
+// only read U), so global traffic is the U gathers plus one write per U slot.
 
 #include "acpf_internal.cuh"
 
@@ -38,9 +39,11 @@ namespace acpf {
 
 namespace {
 
-constexpr int kNSeg = 4;                      // ring segments (kNSeg*32 elements in flight)
-constexpr int kElemBytes = kGroup * 8;        // 64
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCh = 8;     // elements per pipeline stage
+constexpr int kNBuf = 8;   // stages in the ring (kNBuf-1 in flight)
+constexpr int kElemBytes = kGroup * 8;
+constexpr int kBusChunk = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -49,12 +52,6 @@ __device__ __forceinline__ uint32_t su32(const void* p) {
 __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
 
@@ -68,28 +65,19 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
 }
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "W_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
 
-__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(bar) : "memory");
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -101,525 +89,457 @@ __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
   return make_double2(u.x * a.x + u.y * a.y, u.y * a.x - u.x * a.y);
 }
 
-// sum over the quad (sub-lanes r = 0..3 of one scenario), fixed order
-__device__ __forceinline__ double quad_sum(double x) {
-  x = x + __shfl_xor_sync(kFull, x, 8);
-  x = x + __shfl_xor_sync(kFull, x, 16);
-  return x;
-}
+// Per-warp gather pipeline over the stream range [s0, s0 + n).
+struct Pipe {
+  const uint32_t* stream;
+  const double* arena;  // this lane's arena base (element e at arena[e*32])
+  uint32_t ring;        // smem [kNBuf*kCh][32] doubles
+  uint32_t wring;       // smem [kNBuf*kCh] u32 stream words
+  int lane;
+  int s0, n;            // first stream index, element count
+  int issued;           // stages issued
+  int q;                // next element to consume (relative)
+  uint32_t wcur, wnext; // stream-word windows: lane j holds word of element (wbase + j)
+  int wbase;
 
-// Warp-level gather streamer; every lane executes every call.
-struct Streamer {
-  const uint32_t* stream;  // [n_seg + 1][32]  gidx | lpos << 22
-  const uint32_t* meta;    // [n_seg + 1]      len | epoch << 6
-  const double* arena;     // group arena (element e, scenario sc at arena[e*8 + sc])
-  uint32_t ring;           // smem [kNSeg*32 elements][8] doubles
-  uint32_t rlpos;          // smem [kNSeg*32] u16
-  uint32_t rlen;           // smem [kNSeg] u32
-  uint32_t bar;            // smem [kNSeg] mbarriers (count 32)
-  int lane, r, sc;
-  int64_t n_seg;
-  int64_t k_iss, iss_total;
-  uint32_t winA, winB, metaA, metaB;
-  int64_t k_cur, cur_total;
-  int slot, off, len;
-  uint32_t phase;
-  int epoch;
-#ifdef ACPF_PROFILE_PHASES
-  long long t_wait = 0, t_issue = 0, n_wait = 0, n_issue = 0;
-#endif
-
-  __device__ __forceinline__ void preload(int64_t k, uint32_t& win, uint32_t& mt) {
-    win = stream[k * 32 + lane];
-    mt = meta[k];
+  __device__ __forceinline__ uint32_t load_window(int base) const {
+    const int k = base + lane;
+    return k < n ? stream[s0 + k] : 0u;
   }
 
-  __device__ __forceinline__ void begin_step() {
-    k_iss = 0;
-    k_cur = -1;
-    off = len = 0;
-    epoch = 0;
-    preload(0, winA, metaA);
-    preload(n_seg > 0 ? 1 : 0, winB, metaB);
-  }
-
-  __device__ __forceinline__ void issue_one() {
-    const int s = (int)(iss_total % kNSeg);
-    const int n = (int)(metaA & 63u);
-    const uint32_t seg_base = ring + (uint32_t)s * 32 * kElemBytes;
-    __syncwarp();
-    if (lane < n)
-      asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(rlpos + (s * 32 + lane) * 2),
-                   "h"((unsigned short)(winA >> 22))
-                   : "memory");
-    if (lane == 0)
-      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(rlen + s * 4), "r"(n) : "memory");
+  __device__ __forceinline__ void issue_stage() {
+    const int c = issued++;
+    const int e0 = c * kCh;
+    if (e0 < n) {
+      if (e0 >= wbase + 32) {  // advance the double-buffered word window
+        wbase += 32;
+        wcur = wnext;
+        wnext = load_window(wbase + 32);
+      }
+      const int slot = (c % kNBuf) * kCh;
+      const int lim = min(kCh, n - e0);
+      const int jw = e0 - wbase;
+      const uint32_t mine = __shfl_sync(kFull, wcur, (jw + lane) & 31);
+      if (lane < lim) sts_u32(wring + (slot + lane) * 4, mine);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int e = 4 * j + r;
-      const uint32_t w = __shfl_sync(kFull, winA, e);
-      if (e < n)
-        cp_async8(seg_base + (uint32_t)e * kElemBytes + sc * 8, arena + (size_t)(w & 0x3fffffu) * kGroup + sc);
+      for (int j = 0; j < kCh; ++j) {
+        const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
+        if (j < lim)
+          cp_async8(ring + ((slot + j) * 32 + lane) * 8, arena + (size_t)(w & 0x3fffffu) * kGroup);
+      }
     }
-    cp_async_arrive(bar + s * 8);
-    __syncwarp();
-    ++k_iss;
-    ++iss_total;
-    winA = winB;
-    metaA = metaB;
-    const int64_t nk = k_iss + 1 <= n_seg ? k_iss + 1 : n_seg;
-    preload(nk, winB, metaB);
+    cp_commit();
   }
 
-  __device__ __forceinline__ void try_issue() {
-#ifdef ACPF_PROFILE_PHASES
-    long long i0_ = clock64();
-#endif
-    while (k_iss < n_seg && (k_iss - k_cur) <= kNSeg - (k_cur >= 0 ? 1 : 0) &&
-           (int)(metaA >> 6) <= epoch) {
-      issue_one();
-#ifdef ACPF_PROFILE_PHASES
-      ++n_issue;
-#endif
+  __device__ __forceinline__ void begin(const uint32_t* st, int start, int end) {
+    stream = st;
+    s0 = start;
+    n = end - start;
+    issued = 0;
+    q = 0;
+    wbase = 0;
+    wcur = load_window(0);
+    wnext = load_window(32);
+#pragma unroll 1
+    for (int k = 0; k < kNBuf - 1; ++k) issue_stage();
+  }
+
+  // make element q resident (call before reading it)
+  __device__ __forceinline__ void ready() {
+    if ((q & (kCh - 1)) == 0) {
+      cp_wait<kNBuf - 2>();
+      __syncwarp();
+      issue_stage();
     }
-#ifdef ACPF_PROFILE_PHASES
-    t_issue += clock64() - i0_;
-#endif
   }
 
-  __device__ __forceinline__ void new_epoch(int e) {
-    epoch = e;
-    // rows finished so far were written by this warp's lanes with st.global;
-    // make them visible to the other lanes' cp.async reads
-    __syncwarp();
-    __threadfence_block();
-    try_issue();
+  __device__ __forceinline__ uint32_t addr() const {
+    return ring + ((q % (kNBuf * kCh)) * 32 + lane) * 8;
   }
 
-  __device__ __forceinline__ void advance() {
-    ++k_cur;
-    if (k_cur > 0) ++cur_total;
-    try_issue();
-    if (k_iss <= k_cur) __trap();  // schedule bug: segment never issuable
-    slot = (int)(cur_total % kNSeg);
-#ifdef ACPF_PROFILE_PHASES
-    long long w0_ = clock64();
-#endif
-    mbar_wait(bar + slot * 8, (phase >> slot) & 1u);
-#ifdef ACPF_PROFILE_PHASES
-    t_wait += clock64() - w0_;
-    ++n_wait;
-#endif
-    phase ^= 1u << slot;
-    len = (int)lds_u32(rlen + slot * 4);
-    off = 0;
-  }
-
-  __device__ __forceinline__ uint32_t elem(int o) const {
-    return ring + (uint32_t)(slot * 32 + o) * kElemBytes + sc * 8;
-  }
-
-  // scalar element (all four sub-lanes read their scenario's value)
   __device__ __forceinline__ double get() {
-    if (off == len) advance();
-    const double v = lds_f64(elem(off));
-    ++off;
+    ready();
+    const double v = lds_f64(addr());
+    ++q;
     return v;
   }
 
-  __device__ __forceinline__ void end_step() { ++cur_total; }
+  __device__ __forceinline__ double get(uint32_t& word) {
+    ready();
+    word = lds_u32(wring + (q % (kNBuf * kCh)) * 4);
+    const double v = lds_f64(addr());
+    ++q;
+    return v;
+  }
+
+  __device__ __forceinline__ void finish() {
+    cp_wait<0>();
+    __syncwarp();
+  }
 };
 
-__global__ void __launch_bounds__(32, 1) nr_stream_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io,
-                                                       double tol, int max_newton) {
+#define EL(A, e) (A)[(size_t)(e) * kGroup]
+
+__global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= w.groups) return;
+  const int64_t s = g * kGroup + lane;
+  const bool valid = s < io.batch;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  for (int i = 0; i < m.n_bus; ++i) {
+    EL(A, m.off_th + i) = m.theta_init[i];
+    EL(A, m.off_vm + i) = m.vmag_init[i];
+  }
+  for (int k = 0; k < m.n_j; ++k) {
+    double v = 0.0;
+    if (valid) v = k < m.n_theta ? io.p_spec[s * m.n_theta + k] : io.q_spec[s * m.n_q + (k - m.n_theta)];
+    EL(A, m.off_spec + k) = v;
+  }
+  w.active[s] = valid;
+  w.status[s] = 0;
+  w.iters[s] = 0;
+  w.fout[s] = 0.0;
+  w.fmax_bits[s] = 0ull;
+  w.flags[s] = 0;
+  if (lane == 0) w.gactive[g] = 1;
+}
+
+__global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int64_t g = item / nch;
+  if (g >= w.groups || !w.gactive[g]) return;
+  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  bool neg = false;
+  for (int i = i0; i < i1; ++i) {
+    const double t = EL(A, m.off_th + i), v = EL(A, m.off_vm + i);
+    double sn, cs;
+    sincos(t, &sn, &cs);
+    EL(A, m.off_e + 2 * i) = cs;
+    EL(A, m.off_e + 2 * i + 1) = sn;
+    EL(A, m.off_u + 2 * i) = v * cs;
+    EL(A, m.off_u + 2 * i + 1) = v * sn;
+    neg |= v <= 0.0;
+  }
+  if (neg) atomicOr(&w.flags[g * kGroup + lane], 4);
+}
+
+__global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int64_t g = item / nch;
+  if (g >= w.groups || !w.gactive[g]) return;
+  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  double fmx = 0.0;
+  int bad = 0;  // bit0 NaN, bit1 Inf
+  for (int i = i0; i < i1; ++i) {
+    double2 acc = make_double2(0.0, 0.0);
+    const int e1 = m.y_rowptr[i + 1];
+    for (int e = m.y_rowptr[i]; e < e1; ++e) {
+      const double2 y = m.y_val[e];
+      const int c = m.y_col[e];
+      const double ur = EL(A, m.off_u + 2 * c), ui = EL(A, m.off_u + 2 * c + 1);
+      acc.x += y.x * ur - y.y * ui;
+      acc.y += y.x * ui + y.y * ur;
+    }
+    const double2 u = make_double2(EL(A, m.off_u + 2 * i), EL(A, m.off_u + 2 * i + 1));
+    const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
+    const int tp = m.tpos[i], qp = m.qpos[i];
+    if (tp >= 0) {
+      const double f = sv.x - EL(A, m.off_spec + tp);
+      bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
+      fmx = fmx < fabs(f) ? fabs(f) : fmx;
+      EL(A, m.off_yx + m.ipos[tp]) = -f;
+    }
+    if (qp >= 0) {
+      const double f = sv.y - EL(A, m.off_spec + qp);
+      bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
+      fmx = fmx < fabs(f) ? fabs(f) : fmx;
+      EL(A, m.off_yx + m.ipos[qp]) = -f;
+    }
+    // Jacobian blocks of row bus i into their LU slots:
+    //   dS_i/dth_j = -j u_i conj(y u_j)  (j != i);  dS_i/dth_i = j u_i conj(I_i - y u_i)
+    //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
+    //   H = Re dS/dth, N = Re dS/dV, M = Im dS/dth, L = Im dS/dV
+    const double2 ei = make_double2(EL(A, m.off_e + 2 * i), EL(A, m.off_e + 2 * i + 1));
+    const int a1 = m.asm_ptr[i + 1];
+    for (int a = m.asm_ptr[i]; a < a1; ++a) {
+      const double2 y = m.asm_y[a];
+      const int jb = m.asm_j[a];
+      const int4 sl = m.asm_slot[a];
+      const double2 ej = make_double2(EL(A, m.off_e + 2 * jb), EL(A, m.off_e + 2 * jb + 1));
+      const double2 wv = mul_conj(u, cmul(y, ej));
+      double2 dth, dv;
+      if (jb != i) {
+        const double2 uj = make_double2(EL(A, m.off_u + 2 * jb), EL(A, m.off_u + 2 * jb + 1));
+        const double2 wt = mul_conj(u, cmul(y, uj));
+        dth = make_double2(wt.y, -wt.x);
+        dv = wv;
+      } else {
+        const double2 yu = cmul(y, u);
+        const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
+        dth = make_double2(-wt.y, wt.x);
+        dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
+      }
+      if (sl.x >= 0) EL(A, m.off_lu + sl.x) = dth.x;
+      if (sl.y >= 0) EL(A, m.off_lu + sl.y) = dv.x;
+      if (sl.z >= 0) EL(A, m.off_lu + sl.z) = dth.y;
+      if (sl.w >= 0) EL(A, m.off_lu + sl.w) = dv.y;
+    }
+  }
+  const int64_t s = g * kGroup + lane;
+  // fmax of non-negative doubles is the max of their bit patterns
+  if (fmx > 0.0) atomicMax(&w.fmax_bits[s], (unsigned long long)__double_as_longlong(fmx));
+  if (bad) atomicOr(&w.flags[s], bad);
+}
+
+__global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_newton, double tol) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= w.groups) return;
+  const int64_t s = g * kGroup + lane;
+  bool act = s < batch && w.active[s];
+  if (act) {
+    const double fmx = __longlong_as_double((long long)w.fmax_bits[s]);
+    const int fl = w.flags[s];
+    int st = -1;
+    double fo = fmx;
+    if (fl & 3) {
+      st = ACPF_NR_NONFINITE;
+      fo = (fl & 1) ? __longlong_as_double(0x7ff8000000000000LL)
+                    : __longlong_as_double(0x7ff0000000000000LL);
+    } else if (fmx <= tol) {
+      st = ACPF_NR_CONVERGED;
+    } else if (fl & 4) {
+      st = ACPF_NR_VMAG_LE0;
+    } else if (k == max_newton) {
+      st = ACPF_NR_MAX_ITER;
+    }
+    w.fout[s] = fo;
+    if (st >= 0) {
+      w.status[s] = st;
+      w.iters[s] = st == ACPF_NR_MAX_ITER ? max_newton : k;
+      w.active[s] = 0;
+      act = false;
+    }
+  }
+  if (s < batch) {
+    w.fmax_bits[s] = 0ull;
+    w.flags[s] = 0;
+  }
+  const unsigned any = __ballot_sync(kFull, act);
+  if (lane == 0) {
+    w.gactive[g] = any != 0;
+    if (any) atomicAdd(w.n_active, __popc(any));
+  }
+}
+
+// One elimination level: task = (row of the level, group).
+__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int r0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x;
-  const int r = lane >> 3, sc = lane & 7;
-  const int64_t g = blockIdx.x;
-  if (g >= w.groups) return;
-  const int64_t s = g * kGroup + sc;
-  const bool valid = s < io.batch;
-  double* __restrict__ A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
-#define EL(e) A[(size_t)(e) * kGroup]
-
-  const uint32_t sbase = su32(smem);
-  const uint32_t ring = sbase;                                   // kNSeg*32 elements
-  const uint32_t lbuf = ring + kNSeg * 32 * kElemBytes;          // cap elements
-  const uint32_t bar = lbuf + (uint32_t)m.cap * kElemBytes;      // kNSeg mbarriers
-  const uint32_t rlpos = bar + kNSeg * 8;                        // kNSeg*32 u16
-  const uint32_t rlen = rlpos + kNSeg * 32 * 2;                  // kNSeg u32
-  const uint32_t lbuf_sc = lbuf + sc * 8;
-  if (lane == 0) {
-    for (int k = 0; k < kNSeg; ++k) mbar_init(bar + k * 8, 32);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  const int64_t task = blockIdx.x;
+  const int64_t g = task % w.groups;
+  const int p = r0 + (int)(task / w.groups);
+  if (!w.gactive[g]) return;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  const uint32_t ring = su32(smem);
+  const uint32_t wring = ring + kNBuf * kCh * kElemBytes;
+  const uint32_t lbuf = wring + kNBuf * kCh * 4 + lane * 8;
+  Pipe pp;
+  pp.arena = A;
+  pp.ring = ring;
+  pp.wring = wring;
+  pp.lane = lane;
+  pp.begin(m.stream, m.row_sptr[p], m.row_sptr[p + 1]);
+  const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
+  double yacc = pp.get();  // b_p
+  bool zero = false;
+  uint32_t winfo = 0;
+  for (int t = t0; t < t1; ++t) {
+    const int j = (t - t0) & 31;
+    if (j == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
+    const uint32_t info = __shfl_sync(kFull, winfo, j);
+    const int cnt = (int)(info >> 16);
+    double a = (info & kSlotFill) ? 0.0 : pp.get();
+    double a2 = 0.0;
+    int q = 0;
+    for (; q + 1 < cnt; q += 2) {
+      uint32_t w0, w1;
+      const double u0 = pp.get(w0);
+      const double u1 = pp.get(w1);
+      a = fma(-lds_f64(lbuf + (w0 >> 22) * kElemBytes), u0, a);
+      a2 = fma(-lds_f64(lbuf + (w1 >> 22) * kElemBytes), u1, a2);
+    }
+    if (q < cnt) {
+      uint32_t w0;
+      const double u0 = pp.get(w0);
+      a = fma(-lds_f64(lbuf + (w0 >> 22) * kElemBytes), u0, a);
+    }
+    a = a + a2;
+    if (info & kSlotL) {
+      const double inv = pp.get();
+      const double yc = pp.get();
+      a *= inv;
+      yacc = fma(-a, yc, yacc);
+      sts_f64(lbuf + (t - t0) * kElemBytes, a);
+    } else {
+      if (info & kSlotDiag) {
+        zero |= a == 0.0;
+        EL(A, m.off_invd + p) = 1.0 / a;
+      }
+      EL(A, m.off_lu + t) = a;
+    }
   }
-  __syncwarp();
-
-  Streamer st;
-  st.stream = m.stream;
-  st.meta = m.segmeta;
-  st.arena = w.arena + (size_t)g * m.n_elem * kGroup;
-  st.ring = ring;
-  st.rlpos = rlpos;
-  st.rlen = rlen;
-  st.bar = bar;
-  st.lane = lane;
-  st.r = r;
-  st.sc = sc;
-  st.n_seg = m.n_seg;
-  st.iss_total = 0;
-  st.cur_total = 0;
-  st.phase = 0;
-  const bool no_spill = m.cap >= m.max_l;
-
-  // flat start + this scenario's specified injections (buses/entries split over the quad)
-  for (int i = r; i < m.n_bus; i += 4) {
-    EL(m.off_th + i) = m.theta_init[i];
-    EL(m.off_vm + i) = m.vmag_init[i];
-  }
-  for (int k = r; k < m.n_j; k += 4) {
-    double v = 0.0;
-    if (valid)
-      v = k < m.n_theta ? io.p_spec[s * m.n_theta + k] : io.q_spec[s * m.n_q + (k - m.n_theta)];
-    EL(m.off_spec + k) = v;
-  }
-  __syncwarp();
-
-  bool done = !valid;
-  int status = 0, iters = 0;
-  double fout = 0.0;
-
-#ifdef ACPF_PROFILE_PHASES
-  long long tA = 0, tB = 0, tC = 0, tD = 0, tq;
-#define PHASE_MARK(acc) do { long long now_ = clock64(); acc += now_ - tq; tq = now_; } while (0)
-#else
-#define PHASE_MARK(acc) do {} while (0)
-#endif
-  for (int k = 0; k <= max_newton; ++k) {
-#ifdef ACPF_PROFILE_PHASES
-    tq = clock64();
-#endif
-    // ---- A: phasors, min V
-    double vmin = __longlong_as_double(0x7ff0000000000000LL);
-    for (int i = r; i < m.n_bus; i += 4) {
-      const double t = EL(m.off_th + i), v = EL(m.off_vm + i);
-      double sn, cs;
-      sincos(t, &sn, &cs);
-      EL(m.off_e + 2 * i) = cs;
-      EL(m.off_e + 2 * i + 1) = sn;
-      EL(m.off_u + 2 * i) = v * cs;
-      EL(m.off_u + 2 * i + 1) = v * sn;
-      vmin = fmin(vmin, v);
-    }
-    __syncwarp();
-    PHASE_MARK(tA);
-    // ---- B: injections and mismatch
-    double fmx = 0.0;
-    int bad = 0;  // bit0 NaN, bit1 Inf
-    for (int i = r; i < m.n_bus; i += 4) {
-      double2 acc = make_double2(0.0, 0.0);
-      const int e1 = m.y_rowptr[i + 1];
-      for (int e = m.y_rowptr[i]; e < e1; ++e) {
-        const double2 y = m.y_val[e];
-        const int c = m.y_col[e];
-        const double ur = EL(m.off_u + 2 * c), ui = EL(m.off_u + 2 * c + 1);
-        acc.x += y.x * ur - y.y * ui;
-        acc.y += y.x * ui + y.y * ur;
-      }
-      const double2 u = make_double2(EL(m.off_u + 2 * i), EL(m.off_u + 2 * i + 1));
-      const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
-      const int tp = m.tpos[i], qp = m.qpos[i];
-      if (tp >= 0) {
-        const double f = sv.x - EL(m.off_spec + tp);
-        bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
-        fmx = fmx < fabs(f) ? fabs(f) : fmx;
-        EL(m.off_yx + m.ipos[tp]) = -f;
-      }
-      if (qp >= 0) {
-        const double f = sv.y - EL(m.off_spec + qp);
-        bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
-        fmx = fmx < fabs(f) ? fabs(f) : fmx;
-        EL(m.off_yx + m.ipos[qp]) = -f;
-      }
-      // Jacobian blocks of row bus i straight into their LU slots
-      // (dense_jacobian formulas, transmission.py:383-407):
-      //   dS_i/dth_j = -j u_i conj(y u_j)        (j != i)
-      //   dS_i/dth_i =  j u_i conj(I_i - y u_i)
-      //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
-      //   H = Re dS/dth, N = Re dS/dV, M = Im dS/dth, L = Im dS/dV
-      const double2 ei = make_double2(EL(m.off_e + 2 * i), EL(m.off_e + 2 * i + 1));
-      const int a1 = m.asm_ptr[i + 1];
-      for (int a = m.asm_ptr[i]; a < a1; ++a) {
-        const double2 y = m.asm_y[a];
-        const int jb = m.asm_j[a];
-        const int4 sl = m.asm_slot[a];
-        const double2 uj = make_double2(EL(m.off_u + 2 * jb), EL(m.off_u + 2 * jb + 1));
-        const double2 ej = make_double2(EL(m.off_e + 2 * jb), EL(m.off_e + 2 * jb + 1));
-        double2 dth, dv;
-        const double2 wv = mul_conj(u, cmul(y, ej));
-        if (jb != i) {
-          const double2 wt = mul_conj(u, cmul(y, uj));
-          dth = make_double2(wt.y, -wt.x);
-          dv = wv;
-        } else {
-          const double2 yu = cmul(y, u);
-          const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
-          dth = make_double2(-wt.y, wt.x);
-          dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
-        }
-        if (sl.x >= 0) EL(m.off_lu + sl.x) = dth.x;
-        if (sl.y >= 0) EL(m.off_lu + sl.y) = dv.x;
-        if (sl.z >= 0) EL(m.off_lu + sl.z) = dth.y;
-        if (sl.w >= 0) EL(m.off_lu + sl.w) = dv.y;
-      }
-    }
-    // quad reductions (order independent: max / min / or)
-    fmx = fmax(fmx, __shfl_xor_sync(kFull, fmx, 8));
-    fmx = fmax(fmx, __shfl_xor_sync(kFull, fmx, 16));
-    vmin = fmin(vmin, __shfl_xor_sync(kFull, vmin, 8));
-    vmin = fmin(vmin, __shfl_xor_sync(kFull, vmin, 16));
-    bad |= __shfl_xor_sync(kFull, bad, 8);
-    bad |= __shfl_xor_sync(kFull, bad, 16);
-    if (!done) {
-      if (bad) {
-        done = true;
-        status = ACPF_NR_NONFINITE;
-        iters = k;
-        fout = (bad & 1) ? __longlong_as_double(0x7ff8000000000000LL) : fmx;
-      } else if (fmx <= tol) {
-        done = true;
-        status = ACPF_NR_CONVERGED;
-        iters = k;
-        fout = fmx;
-      } else if (vmin <= 0.0) {
-        done = true;
-        status = ACPF_NR_VMAG_LE0;
-        iters = k;
-        fout = fmx;
-      } else if (k == max_newton) {
-        done = true;
-        status = ACPF_NR_MAX_ITER;
-        iters = max_newton;
-        fout = fmx;
-      }
-    }
-    PHASE_MARK(tB);
-    if (__all_sync(kFull, done)) break;
-
-    // ---- C: Crout refactorisation + forward substitution
-    st.begin_step();
-    st.new_epoch(0);
-    bool zero_pivot = false;
-    int64_t t = 0;  // LU slot
-    // slot control words (lane j holds slot w0 + j), double buffered
-    int64_t w0 = 0;
-    uint32_t winfo = lane < m.nnz_lu ? m.slot_info[lane] : 0u;
-    uint32_t ninfo = 32 + lane < m.nnz_lu ? m.slot_info[32 + lane] : 0u;
-    int epoch = 0;
-    for (int p = 0; p < m.n_j; ++p) {
-      double yacc = 0.0;
-      int pos = 0;  // position within the row
-      for (;;) {
-        if (t - w0 == 32) {
-          w0 += 32;
-          winfo = ninfo;
-          const int64_t nt = w0 + 32 + lane;
-          if (nt < m.nnz_lu) ninfo = m.slot_info[nt];
-        }
-        const uint32_t info = __shfl_sync(kFull, winfo, (int)(t - w0));
-        if (info & kSlotNewEpoch) st.new_epoch(++epoch);
-        const int cnt = (int)(info >> 16);
-        const bool lslot = info & kSlotL, fill = info & kSlotFill;
-        const int head = ((info & kSlotRowStart) ? 1 : 0) + (fill ? 0 : 1);
-        const int need = head + cnt + (lslot ? 2 : 0);
-        double a = 0.0, inv = 0.0, yc = 0.0;
-        if (need <= 32) {
-          // the whole unit sits in one ring segment (schedule guarantee)
-          if (need) {
-            if (st.off == st.len) st.advance();
-          }
-          const uint32_t e0 = st.elem(st.off);
-          int o = 0;
-          if (info & kSlotRowStart) yacc = lds_f64(e0 + (o++) * kElemBytes);
-          if (!fill) a = lds_f64(e0 + (o++) * kElemBytes);
-          if (cnt) {
-            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off + o) * 2;
-            const uint32_t ra = e0 + o * kElemBytes;
-            double part = 0.0;
-            if (no_spill) {
-#pragma unroll 2
-              for (int q = r; q < cnt; q += 4)
-                part = fma(-lds_f64(lbuf_sc + lds_u16(la + 2 * q) * kElemBytes),
-                           lds_f64(ra + q * kElemBytes), part);
-            } else {
-              for (int q = r; q < cnt; q += 4) {
-                const int lp = (int)lds_u16(la + 2 * q);
-                const double l = lp < m.cap ? lds_f64(lbuf_sc + lp * kElemBytes)
-                                            : EL(m.off_spill + (lp - m.cap));
-                part = fma(-l, lds_f64(ra + q * kElemBytes), part);
-              }
-            }
-            a = a + quad_sum(part);
-            o += cnt;
-          }
-          if (lslot) {
-            inv = lds_f64(e0 + o * kElemBytes);
-            yc = lds_f64(e0 + (o + 1) * kElemBytes);
-          }
-          st.off += need;
-        } else {
-          // long unit: generic path across segment boundaries
-          if (info & kSlotRowStart) yacc = st.get();
-          if (!fill) a = st.get();
-          double part = 0.0;
-          int rem = cnt;
-          while (rem > 0) {
-            if (st.off == st.len) st.advance();
-            const int nb = min(rem, st.len - st.off);
-            const uint32_t la = rlpos + (uint32_t)(st.slot * 32 + st.off) * 2;
-            const uint32_t ra = st.elem(st.off);
-            for (int q = r; q < nb; q += 4) {
-              const int lp = (int)lds_u16(la + 2 * q);
-              const double l = lp < m.cap ? lds_f64(lbuf_sc + lp * kElemBytes)
-                                          : EL(m.off_spill + (lp - m.cap));
-              part = fma(-l, lds_f64(ra + q * kElemBytes), part);
-            }
-            st.off += nb;
-            rem -= nb;
-          }
-          a = a + quad_sum(part);
-          if (lslot) {
-            inv = st.get();
-            yc = st.get();
-          }
-        }
-        if (lslot) {
-          a *= inv;
-          yacc = fma(-a, yc, yacc);
-          // every quad lane holds the same value: each writes it, so each
-          // lane's later reads depend only on its own store
-          if (pos < m.cap)
-            sts_f64(lbuf_sc + pos * kElemBytes, a);
-          else
-            EL(m.off_spill + (pos - m.cap)) = a;
-        } else {
-          if (info & kSlotDiag) {
-            zero_pivot |= (a == 0.0);
-            if (r == 0) EL(m.off_invd + p) = 1.0 / a;
-          }
-          if (r == 0) EL(m.off_lu + t) = a;
-        }
-        ++t;
-        ++pos;
-        if (info & kSlotRowEnd) break;
-      }
-      if (r == 0) EL(m.off_yx + p) = yacc;
-    }
-    PHASE_MARK(tC);
-    // ---- D: back substitution (rows by back level)
-    st.new_epoch(m.n_levels);
-    epoch = m.n_levels;
-    uint32_t bwin = 0, bnext = 0;
-    if (lane < m.n_j) bwin = m.brow[lane];
-    if (32 + lane < m.n_j) bnext = m.brow[32 + lane];
-    for (int rr = 0; rr < m.n_j; ++rr) {
-      if (rr && (rr & 31) == 0) {
-        bwin = bnext;
-        if (rr + 32 + lane < m.n_j) bnext = m.brow[rr + 32 + lane];
-      }
-      const uint32_t b = __shfl_sync(kFull, bwin, rr & 31);
-      if (b >> 31) st.new_epoch(++epoch);
-      const int p = (int)(b & 0xfffffu);
-      int rem = (int)((b >> 20) & 0x7ffu);
-      double y0, inv, part = 0.0;
-      const int need = 2 + 2 * rem;
-      if (need <= 32) {
-        if (st.off == st.len) st.advance();
-        const uint32_t e0 = st.elem(st.off);
-        y0 = lds_f64(e0);
-        inv = lds_f64(e0 + kElemBytes);
-        for (int q = r; q < rem; q += 4)
-          part = fma(-lds_f64(e0 + (2 + 2 * q) * kElemBytes), lds_f64(e0 + (3 + 2 * q) * kElemBytes), part);
-        st.off += need;
-      } else {
-        y0 = st.get();
-        inv = st.get();
-        while (rem > 0) {
-          if (st.off == st.len) st.advance();
-          const int nb = min(rem, (st.len - st.off) >> 1);
-          if (nb == 0) {  // a (u, x) pair straddles two segments
-            const double u = st.get();
-            const double x = st.get();
-            if (r == 0) part = fma(-u, x, part);
-            --rem;
-            continue;
-          }
-          const uint32_t ra = st.elem(st.off);
-          for (int q = r; q < nb; q += 4)
-            part = fma(-lds_f64(ra + 2 * q * kElemBytes), lds_f64(ra + (2 * q + 1) * kElemBytes), part);
-          st.off += 2 * nb;
-          rem -= nb;
-        }
-      }
-      const double x = (y0 + quad_sum(part)) * inv;
-      if (r == 0) EL(m.off_yx + p) = x;
-    }
-    st.end_step();
-    __syncwarp();
-    PHASE_MARK(tD);
-    // per scenario: every lane of a quad saw the same pivots
-    zero_pivot = zero_pivot || __shfl_xor_sync(kFull, (int)zero_pivot, 8) ||
-                 __shfl_xor_sync(kFull, (int)zero_pivot, 16);
-    if (!done && zero_pivot) {
-      done = true;
-      status = ACPF_NR_ZERO_PIVOT;
-      iters = k;
-      fout = fmx;
-    }
-    if (!done) {
-      for (int i = r; i < m.n_bus; i += 4) {
-        const int tp = m.tpos[i], qp = m.qpos[i];
-        if (tp >= 0) EL(m.off_th + i) = EL(m.off_th + i) + EL(m.off_yx + m.ipos[tp]);
-        if (qp >= 0) EL(m.off_vm + i) = EL(m.off_vm + i) + EL(m.off_yx + m.ipos[qp]);
-      }
-    }
-    __syncwarp();
-  }
-
-#ifdef ACPF_PROFILE_PHASES
-  if (g == 0 && lane == 0)
-    printf("phase cycles A %lld B %lld C %lld D %lld | wait %lld (%lld) issue %lld (%lld)\n", tA, tB, tC,
-           tD, st.t_wait, st.n_wait, st.t_issue, st.n_issue);
-#endif
-  if (!valid) return;
-  for (int i = r; i < m.n_bus; i += 4) {
-    io.theta_out[s * m.n_bus + i] = EL(m.off_th + i);
-    io.vmag_out[s * m.n_bus + i] = EL(m.off_vm + i);
-  }
-  if (r == 0) {
-    if (io.converged) io.converged[s] = status == ACPF_NR_CONVERGED;
-    if (io.iterations) io.iterations[s] = iters;
-    if (io.fnorm) io.fnorm[s] = fout;
-    if (io.status) io.status[s] = status;
-  }
-#undef EL
+  EL(A, m.off_yx + p) = yacc;
+  pp.finish();
+  if (zero) atomicOr(&w.flags[g * kGroup + lane], 8);
 }
+
+// One back-substitution level: task = (row of the level, group).
+__global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int b0) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const int64_t task = blockIdx.x;
+  const int64_t g = task % w.groups;
+  const int r = b0 + (int)(task / w.groups);
+  if (!w.gactive[g]) return;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  const uint32_t ring = su32(smem);
+  Pipe pp;
+  pp.arena = A;
+  pp.ring = ring;
+  pp.wring = ring + kNBuf * kCh * kElemBytes;
+  pp.lane = lane;
+  pp.begin(m.stream, m.brow_sptr[r], m.brow_sptr[r + 1]);
+  const uint32_t b = m.brow[r];
+  const int p = (int)(b & 0xfffffu);
+  const int cnt = (int)(b >> 20);
+  double acc = pp.get();
+  const double inv = pp.get();
+  double acc2 = 0.0;
+  int q = 0;
+  for (; q + 1 < cnt; q += 2) {
+    const double u0 = pp.get(), x0 = pp.get();
+    const double u1 = pp.get(), x1 = pp.get();
+    acc = fma(-u0, x0, acc);
+    acc2 = fma(-u1, x1, acc2);
+  }
+  if (q < cnt) {
+    const double u0 = pp.get(), x0 = pp.get();
+    acc = fma(-u0, x0, acc);
+  }
+  EL(A, m.off_yx + p) = (acc + acc2) * inv;
+  pp.finish();
+}
+
+__global__ void nr_update_kernel(NrDeviceModel m, NrWorkspace w, int k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int64_t g = item / nch;
+  if (g >= w.groups || !w.gactive[g]) return;
+  const int64_t s = g * kGroup + lane;
+  if (!w.active[s]) return;
+  if (w.flags[s] & 8) {  // zero pivot in this step's factorisation: stop here
+    if (item % nch == 0) {
+      w.status[s] = ACPF_NR_ZERO_PIVOT;
+      w.iters[s] = k;
+    }
+    return;
+  }
+  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  for (int i = i0; i < i1; ++i) {
+    const int tp = m.tpos[i], qp = m.qpos[i];
+    if (tp >= 0) EL(A, m.off_th + i) = EL(A, m.off_th + i) + EL(A, m.off_yx + m.ipos[tp]);
+    if (qp >= 0) EL(A, m.off_vm + i) = EL(A, m.off_vm + i) + EL(A, m.off_yx + m.ipos[qp]);
+  }
+}
+
+// scenarios whose factorisation hit an exact zero pivot stop (state not updated)
+__global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= batch || !w.active[s]) return;
+  if (w.flags[s] & 8) w.active[s] = 0;
+}
+
+__global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int64_t g = item / nch;
+  if (g >= w.groups) return;
+  const int64_t s = g * kGroup + lane;
+  if (s >= io.batch) return;
+  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
+  const double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  for (int i = i0; i < i1; ++i) {
+    io.theta_out[s * m.n_bus + i] = EL(A, m.off_th + i);
+    io.vmag_out[s * m.n_bus + i] = EL(A, m.off_vm + i);
+  }
+  if (item % nch == 0) {
+    const int st = w.status[s];
+    if (io.converged) io.converged[s] = st == ACPF_NR_CONVERGED;
+    if (io.iterations) io.iterations[s] = w.iters[s];
+    if (io.fnorm) io.fnorm[s] = w.fout[s];
+    if (io.status) io.status[s] = st;
+  }
+}
+
+size_t pipe_smem() { return (size_t)kNBuf * kCh * (kElemBytes + 4); }
 
 }  // namespace
 
-size_t nr_smem_bytes(int cap) {
-  return (size_t)kNSeg * 32 * kElemBytes + (size_t)cap * kElemBytes + kNSeg * 8 + kNSeg * 32 * 2 +
-         kNSeg * 4 + 16;
-}
+size_t nr_smem_bytes(int cap) { return pipe_smem() + (size_t)cap * kElemBytes; }
 
-cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrWorkspace& w, const NrBatchIO& io,
-                             double tol, int max_newton, cudaStream_t stream) {
-  const size_t smem = nr_smem_bytes(m.cap);
-  cudaError_t e = cudaFuncSetAttribute(nr_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
+
+cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
+                             const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
+                             int* launches) {
+  cudaError_t e = cudaFuncSetAttribute(nr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nr_smem_bytes(hs.max_l));
   if (e != cudaSuccess) return e;
   const int64_t groups = (io.batch + kGroup - 1) / kGroup;
-  nr_stream_kernel<<<(unsigned)groups, 32, smem, stream>>>(m, w, io, tol, max_newton);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int wpb = 4;
+  auto blocks = [&](int64_t items) { return (unsigned)((items + wpb - 1) / wpb); };
+  int nl = 0;
+  nr_init_kernel<<<blocks(groups), 32 * wpb, 0, stream>>>(m, w, io);
+  ++nl;
+  for (int k = 0; k <= max_newton; ++k) {
+    nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w);
+    nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w);
+    e = cudaMemsetAsync(w.n_active, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    nr_check_kernel<<<blocks(groups), 32 * wpb, 0, stream>>>(w, io.batch, k, max_newton, tol);
+    nl += 3;
+    e = cudaMemcpyAsync(w.host_active, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return e;
+    if (*w.host_active == 0) break;
+    for (int l = 0; l < hs.n_levels; ++l) {
+      const int r0 = hs.level_ptr[l], nr = hs.level_ptr[l + 1] - r0;
+      nr_factor_kernel<<<(unsigned)(groups * nr), 32, nr_smem_bytes(hs.level_maxl[l]), stream>>>(m, w, r0);
+    }
+    for (int l = 0; l < hs.n_blevels; ++l) {
+      const int b0 = hs.blevel_ptr[l], nr = hs.blevel_ptr[l + 1] - b0;
+      nr_back_kernel<<<(unsigned)(groups * nr), 32, pipe_smem(), stream>>>(m, w, b0);
+    }
+    nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
+    nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);
+    nl += hs.n_levels + hs.n_blevels + 2;
+  }
+  nr_output_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, io);
+  ++nl;
+  if (launches) *launches = nl;
   return cudaGetLastError();
 }
 

@@ -266,7 +266,7 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
 }
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
-                       const double* y_re, const double* y_im, int cap_limit, NrSchedule& o) {
+                       const double* y_re, const double* y_im, NrSchedule& o) {
   const int nj = s.n_j, nb = s.n_bus;
   // ---- arena layout
   int64_t e = 0;
@@ -279,22 +279,18 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   o.off_spec = e;  e += nj;
   o.off_th = e;    e += nb;
   o.off_vm = e;    e += nb;
-  o.max_l = 0;
-  for (int p = 0; p < nj; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
-  o.cap = std::min(o.max_l, cap_limit);
-  o.off_spill = e; e += std::max(0, o.max_l - o.cap);
   o.n_elem = e;
   if (o.n_elem >= (1 << 22)) throw std::length_error("arena exceeds 22-bit gather index");
+  o.max_l = 0;
+  for (int p = 0; p < nj; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
   if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 entries");
 
-  // ---- per-bus assembly lists (phase B of the kernel): for every Ybus entry
-  // (i, j) plus the diagonal bus block, the LU slots of the H, N, M, L
-  // derivatives it feeds (-1 where the unknown/equation does not exist)
+  // ---- per-bus assembly lists: every Ybus entry (i, j) plus the diagonal
+  // bus block feeds the LU slots of the H, N, M, L derivatives
   std::vector<int64_t> where(nj, -1);
   std::vector<int> tpos(nb, -1), qpos(nb, -1);
   for (int p = 0; p < nj; ++p) {
-    const int var = s.perm[p];
-    if (var < s.n_theta) tpos[s.row_bus[p]] = p; else qpos[s.row_bus[p]] = p;
+    if (s.perm[p] < s.n_theta) tpos[s.row_bus[p]] = p; else qpos[s.row_bus[p]] = p;
   }
   o.asm_ptr.assign(nb + 1, 0);
   o.asm_y.clear();
@@ -330,64 +326,46 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     o.asm_ptr[i + 1] = (int32_t)o.asm_j.size();
   }
 
-  // ---- levels
-  std::vector<int> lev(nj, 0);
+  // ---- levels (rows must already be level-sorted)
+  std::vector<int> lev(nj, 0), blev(nj, 0);
   for (int p = 0; p < nj; ++p) {
     int l = 0;
     for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) l = std::max(l, lev[s.col[t]] + 1);
     lev[p] = l;
+    if (p && lev[p] < lev[p - 1]) throw std::logic_error("rows not level-sorted");
   }
-  std::vector<int> blev(nj, 0);
   for (int p = nj - 1; p >= 0; --p) {
     int l = 0;
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) l = std::max(l, blev[s.col[t]] + 1);
     blev[p] = l;
   }
-  o.n_levels = 0;
+  o.n_levels = lev[nj - 1] + 1;
   o.n_blevels = 0;
+  for (int p = 0; p < nj; ++p) o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
+  o.level_ptr.assign(o.n_levels + 1, 0);
+  o.level_maxl.assign(o.n_levels, 0);
   for (int p = 0; p < nj; ++p) {
-    o.n_levels = std::max(o.n_levels, lev[p] + 1);
-    o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
-    if (p && lev[p] < lev[p - 1]) throw std::logic_error("rows not level-sorted");
+    o.level_ptr[lev[p] + 1] = p + 1;
+    o.level_maxl[lev[p]] = std::max<int>(o.level_maxl[lev[p]], (int)(s.diag[p] - s.rowptr[p]));
   }
 
-  // ---- stream: a list of "units" (one per LU slot, one per back row); a
-  // unit's gathers never straddle a segment when it has <= kSeg of them
+  // ---- factor stream: per row b_p, then per slot: assembled value (unless
+  // fill), the Crout updates' U operands (with the L position), and for an
+  // L slot the pivot inverse and y of its column
   o.stream.clear();
-  o.segmeta.clear();
-  std::vector<uint32_t> seg;
-  int seg_epoch = -1;
-  auto close = [&]() {
-    if (seg.empty()) return;
-    o.segmeta.push_back((uint32_t)seg.size() | ((uint32_t)seg_epoch << 6));
-    for (uint32_t w : seg) o.stream.push_back(w);
-    for (size_t k = seg.size(); k < (size_t)kSeg; ++k) o.stream.push_back(0u);
-    seg.clear();
+  auto gw = [&](int64_t gidx, int lpos) {
+    o.stream.push_back((uint32_t)gidx | ((uint32_t)lpos << 22));
   };
-  std::vector<uint32_t> unit;
-  auto flush_unit = [&](int epoch) {
-    if (epoch != seg_epoch) {
-      close();
-      seg_epoch = epoch;
-    }
-    if (unit.size() <= (size_t)kSeg && seg.size() + unit.size() > (size_t)kSeg) close();
-    for (uint32_t w : unit) {
-      if (seg.size() == (size_t)kSeg) close();
-      seg.push_back(w);
-    }
-    unit.clear();
-  };
-  auto gw = [&](int64_t gidx, int lpos) { unit.push_back((uint32_t)gidx | ((uint32_t)lpos << 22)); };
   o.slot_info.assign(s.nnz_lu, 0);
-  o.n_stream = 0;
+  o.row_slot.assign(nj + 1, 0);
+  o.row_sptr.assign(nj + 1, 0);
   for (int p = 0; p < nj; ++p) {
     const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
+    o.row_slot[p + 1] = (int32_t)r1;
+    gw(o.off_yx + p, 0);
     for (int64_t t = r0; t < r1; ++t) {
       uint32_t info = 0;
-      if (t == r0) info |= kSlotRowStart;
-      if (t == r0 && p > 0 && lev[p] != lev[p - 1]) info |= kSlotNewEpoch;
       if (t == s.diag[p]) info |= kSlotDiag;
-      if (t == r1 - 1) info |= kSlotRowEnd;
       if (t < s.diag[p]) info |= kSlotL;
       const bool fill = s.slot_type[t] == 8;
       if (fill) info |= kSlotFill;
@@ -395,45 +373,42 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
       if (cnt >= 65536) throw std::length_error("too many updates for one slot");
       info |= (uint32_t)cnt << 16;
       o.slot_info[t] = info;
-      if (t == r0) gw(o.off_yx + p, 0);          // b_p (rhs, written by the mismatch phase)
-      if (!fill) gw(o.off_lu + t, 0);            // assembled Jacobian value
+      if (!fill) gw(o.off_lu + t, 0);
       for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
         gw(o.off_lu + s.pair_u[q], (int)(s.pair_l[q] - r0));
       if (t < s.diag[p]) {
         gw(o.off_invd + s.col[t], 0);
         gw(o.off_yx + s.col[t], 0);
       }
-      o.n_stream += (int64_t)unit.size();
-      flush_unit(lev[p]);
     }
+    o.row_sptr[p + 1] = (int32_t)o.stream.size();
   }
+  // ---- back stream: rows by back level; per row y_p, 1/u_pp, then (u_pc, x_c)
   std::vector<int32_t> border(nj);
   for (int p = 0; p < nj; ++p) border[p] = p;
   std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
     return blev[a] != blev[b] ? blev[a] < blev[b] : a > b;
   });
   o.brow.resize(nj);
+  o.brow_sptr.assign(nj + 1, 0);
+  o.blevel_ptr.assign(o.n_blevels + 1, 0);
+  o.brow_sptr[0] = (int32_t)o.stream.size();
   for (int r = 0; r < nj; ++r) {
     const int p = border[r];
-    const int ep = o.n_levels + blev[p];
     const int64_t cnt = s.rowptr[p + 1] - s.diag[p] - 1;
     if (p >= (1 << 20) || cnt >= 2048) throw std::length_error("back row too large");
-    o.brow[r] = (uint32_t)p | ((uint32_t)cnt << 20) |
-                ((r > 0 && blev[p] != blev[border[r - 1]]) ? (1u << 31) : 0u);
+    o.brow[r] = (uint32_t)p | ((uint32_t)cnt << 20);
+    o.blevel_ptr[blev[p] + 1] = r + 1;
     gw(o.off_yx + p, 0);
     gw(o.off_invd + p, 0);
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
       gw(o.off_lu + t, 0);
       gw(o.off_yx + s.col[t], 0);
     }
-    o.n_stream += (int64_t)unit.size();
-    flush_unit(ep);
+    o.brow_sptr[r + 1] = (int32_t)o.stream.size();
   }
-  close();
-  o.n_seg = (int64_t)o.segmeta.size();
-  // sentinel segment (never issued): epoch beyond every consumer epoch
-  for (int k = 0; k < kSeg; ++k) o.stream.push_back(0u);
-  o.segmeta.push_back(0u | (0x3ffffffu << 6));
+  o.n_stream = (int64_t)o.stream.size();
+  if (o.n_stream >= INT32_MAX) throw std::length_error("stream too long");
 }
 
 }  // namespace acpf

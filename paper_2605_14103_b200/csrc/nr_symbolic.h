@@ -25,13 +25,12 @@ struct NrSymbolic {
   std::vector<int32_t> pair_l, pair_u;
 };
 
-// Per-step gather stream for the streaming Crout kernel (see nr_kernel.cu).
+// Level-synchronous Crout schedule (see nr_kernel.cu).
 // Arena: one contiguous block of elements per scenario group; element e of
-// lane l lives at arena[e * 32 + l].
+// scenario l lives at arena[e * kGroup + l].
 struct NrSchedule {
   int64_t off_lu = 0, off_invd = 0, off_yx = 0, off_u = 0, off_e = 0, off_i = 0, off_spec = 0,
-          off_th = 0, off_vm = 0, off_spill = 0, n_elem = 0;
-  int cap = 0;       // L entries kept in shared memory per row
+          off_th = 0, off_vm = 0, n_elem = 0;
   int max_l = 0;     // longest L part of any row
   int n_levels = 0;  // factor levels (etree height)
   int n_blevels = 0; // back-substitution levels
@@ -40,28 +39,26 @@ struct NrSchedule {
   std::vector<double> asm_y;      // [entries][2] Ybus value (0 for a missing diagonal)
   std::vector<int32_t> asm_j;     // [entries] column bus
   std::vector<int32_t> asm_slot;  // [entries][4] LU slot of H, N, M, L (or -1)
-  // factor slots in slot order
-  std::vector<uint32_t> slot_info;  // flags | cnt << 16
-  // back rows in back order: p | cnt << 20 | new_epoch << 31
+  // factor: rows are level-sorted; level l = rows level_ptr[l]..level_ptr[l+1]
+  std::vector<int32_t> level_ptr, level_maxl;
+  std::vector<uint32_t> slot_info;  // [nnz_lu] flags | cnt << 16
+  std::vector<int32_t> row_slot;    // [n_j+1] = LU rowptr
+  std::vector<int32_t> row_sptr;    // [n_j+1] factor-row stream ranges
+  // back substitution: rows in back order brow[r] = p | cnt << 20, grouped by
+  // back level blevel_ptr; stream ranges brow_sptr (indexed by back position)
   std::vector<uint32_t> brow;
-  // segmented stream: 32 words per segment, word = gidx | lpos << 22
+  std::vector<int32_t> blevel_ptr, brow_sptr;
+  // gather stream, word = element index | lpos << 22
   std::vector<uint32_t> stream;
-  std::vector<uint32_t> segmeta;  // len | epoch << 6
-  int64_t n_seg = 0;
-  int64_t n_stream = 0;  // live elements (without padding)
+  int64_t n_stream = 0;
 };
 
-// slot_info flag bits
-constexpr uint32_t kSlotRowStart = 1u << 4;
 constexpr uint32_t kSlotDiag = 1u << 5;
-constexpr uint32_t kSlotRowEnd = 1u << 6;
-constexpr uint32_t kSlotNewEpoch = 1u << 7;
 constexpr uint32_t kSlotL = 1u << 8;
 constexpr uint32_t kSlotFill = 1u << 9;
-constexpr int kSeg = 32;
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
-                       const double* y_re, const double* y_im, int cap_limit, NrSchedule& out);
+                       const double* y_re, const double* y_im, NrSchedule& out);
 
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
