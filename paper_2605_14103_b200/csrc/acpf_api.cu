@@ -366,7 +366,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     const int64_t have_groups = p->ws_groups;
     const int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
     int64_t groups = std::max<int64_t>(1, budget / std::max<int64_t>(1, p->bytes_per_group));
-    groups = std::min<int64_t>(groups, 4096);
+    groups = std::min<int64_t>(groups, 16384);
     chunk = groups * kGroup;
   }
   chunk = std::min<int64_t>(chunk, batch);

@@ -12,7 +12,7 @@ namespace acpf {
 
 void set_error(const std::string& msg);
 
-constexpr int kGroup = 32;  // NR: scenarios per warp (one lane each)
+constexpr int kGroup = 8;  // NR: scenarios per warp (a quad of lanes each)
 
 // ---------------------------------------------------------------------------
 // Newton plan (device side view passed to the kernel by value)

@@ -1,10 +1,12 @@
 // Batched polar Newton-Raphson on sm_100a: level-synchronous sparse LU.
 //
-// Data layout: scenarios are processed in groups of kGroup = 32 (one lane
-// each); every per-scenario quantity lives in a per-group arena of
-// "elements", element e of lane l at arena[e*32 + l], so every warp access to
-// one element is a single coalesced 256-byte transaction. The schedule
-// (Ybus, LU pattern, Crout updates) is shared by all groups.
+// Data layout: scenarios are processed in groups of kGroup = 8; each
+// scenario owns a quad of lanes (lane = r*8 + sc, sub-lane r = 0..3). Every
+// per-scenario quantity lives in a per-group arena of "elements", element e of
+// scenario sc at arena[e*8 + sc], so one element of a group is 64 contiguous
+// bytes and a warp instruction touching 4 elements moves four fully used
+// 64-byte segments. The schedule (Ybus, LU pattern, Crout updates) is shared
+// by all groups.
 //
 // One Newton step of the reference `_newton_loop` (transmission.py:333-380)
 // for the whole batch is a short sequence of launches on one stream:
@@ -27,8 +29,10 @@
 // Inside a factor/back task every operand that is not produced by the task
 // itself (earlier U rows, pivots, y/x, assembled J values) is a precomputed
 // element index in a gather stream; the warp runs a cp.async (LDGSTS)
-// multistage pipeline over its stream (8 elements per stage, 7 stages in
-// flight) into a shared-memory ring. No stream element of a task can be
+// multistage pipeline over its stream (16 elements per stage, 15 stages =
+// 240 elements in flight) into a shared-memory ring, and the quad of a
+// scenario splits every dot product 4 ways (partial sums combined by a fixed
+// shuffle butterfly). No stream element of a task can be
 // produced by another task of the same level, so the pipeline needs no
 // hazard checks. The task's own L values stay in shared memory (later rows
 // only read U), so global traffic is the U gathers plus one write per U slot.
@@ -40,9 +44,10 @@ namespace acpf {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCh = 8;     // elements per pipeline stage
-constexpr int kNBuf = 8;   // stages in the ring (kNBuf-1 in flight)
-constexpr int kElemBytes = kGroup * 8;
+constexpr int kCh = 16;    // elements per pipeline stage
+constexpr int kNBuf = 16;  // stages in the ring (kNBuf-1 in flight)
+constexpr int kRing = kCh * kNBuf;
+constexpr int kElemBytes = kGroup * 8;  // 64
 constexpr int kBusChunk = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -89,17 +94,25 @@ __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
   return make_double2(u.x * a.x + u.y * a.y, u.y * a.x - u.x * a.y);
 }
 
+// sum over the quad of a scenario (lanes sc, sc+8, sc+16, sc+24), fixed order
+__device__ __forceinline__ double quad_sum(double x) {
+  x = x + __shfl_xor_sync(kFull, x, 8);
+  x = x + __shfl_xor_sync(kFull, x, 16);
+  return x;
+}
+
 // Per-warp gather pipeline over the stream range [s0, s0 + n).
 struct Pipe {
   const uint32_t* stream;
-  const double* arena;  // this lane's arena base (element e at arena[e*32])
-  uint32_t ring;        // smem [kNBuf*kCh][32] doubles
-  uint32_t wring;       // smem [kNBuf*kCh] u32 stream words
-  int lane;
+  const double* arena;  // group arena base (element e, scenario sc at arena[e*8 + sc])
+  uint32_t ring;        // smem [kRing][8] doubles
+  uint32_t wring;       // smem [kRing] u32 stream words
+  int lane, r, sc;
   int s0, n;            // first stream index, element count
   int issued;           // stages issued
+  int ready_upto;       // elements [0, ready_upto) are resident
   int q;                // next element to consume (relative)
-  uint32_t wcur, wnext; // stream-word windows: lane j holds word of element (wbase + j)
+  uint32_t wcur, wnext; // word windows: lane j holds the word of element (wbase + j)
   int wbase;
 
   __device__ __forceinline__ uint32_t load_window(int base) const {
@@ -118,14 +131,15 @@ struct Pipe {
       }
       const int slot = (c % kNBuf) * kCh;
       const int lim = min(kCh, n - e0);
-      const int jw = e0 - wbase;
+      const int jw = e0 - wbase;  // 0 or 16
       const uint32_t mine = __shfl_sync(kFull, wcur, (jw + lane) & 31);
       if (lane < lim) sts_u32(wring + (slot + lane) * 4, mine);
 #pragma unroll
-      for (int j = 0; j < kCh; ++j) {
-        const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
-        if (j < lim)
-          cp_async8(ring + ((slot + j) * 32 + lane) * 8, arena + (size_t)(w & 0x3fffffu) * kGroup);
+      for (int j = 0; j < kCh / 4; ++j) {
+        const int e = 4 * j + r;
+        const uint32_t w = __shfl_sync(kFull, wcur, (jw + e) & 31);
+        if (e < lim)
+          cp_async8(ring + ((slot + e) * kGroup + sc) * 8, arena + (size_t)(w & 0x3fffffu) * kGroup + sc);
       }
     }
     cp_commit();
@@ -136,6 +150,7 @@ struct Pipe {
     s0 = start;
     n = end - start;
     issued = 0;
+    ready_upto = 0;
     q = 0;
     wbase = 0;
     wcur = load_window(0);
@@ -144,30 +159,26 @@ struct Pipe {
     for (int k = 0; k < kNBuf - 1; ++k) issue_stage();
   }
 
-  // make element q resident (call before reading it)
-  __device__ __forceinline__ void ready() {
-    if ((q & (kCh - 1)) == 0) {
+  // make element e resident; elements < q must already be consumed
+  __device__ __forceinline__ void ensure(int e) {
+    while (e >= ready_upto) {
       cp_wait<kNBuf - 2>();
       __syncwarp();
       issue_stage();
+      ready_upto += kCh;
     }
   }
 
-  __device__ __forceinline__ uint32_t addr() const {
-    return ring + ((q % (kNBuf * kCh)) * 32 + lane) * 8;
+  __device__ __forceinline__ uint32_t addr(int e) const {
+    return ring + (((e % kRing) * kGroup) + sc) * 8;
   }
 
+  __device__ __forceinline__ uint32_t word(int e) const { return lds_u32(wring + (e % kRing) * 4); }
+
+  // scalar element: every sub-lane reads its scenario's value
   __device__ __forceinline__ double get() {
-    ready();
-    const double v = lds_f64(addr());
-    ++q;
-    return v;
-  }
-
-  __device__ __forceinline__ double get(uint32_t& word) {
-    ready();
-    word = lds_u32(wring + (q % (kNBuf * kCh)) * 4);
-    const double v = lds_f64(addr());
+    ensure(q);
+    const double v = lds_f64(addr(q));
     ++q;
     return v;
   }
@@ -181,21 +192,22 @@ struct Pipe {
 #define EL(A, e) (A)[(size_t)(e) * kGroup]
 
 __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= w.groups) return;
-  const int64_t s = g * kGroup + lane;
+  const int64_t s = g * kGroup + sc;
   const bool valid = s < io.batch;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
-  for (int i = 0; i < m.n_bus; ++i) {
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  for (int i = r; i < m.n_bus; i += 4) {
     EL(A, m.off_th + i) = m.theta_init[i];
     EL(A, m.off_vm + i) = m.vmag_init[i];
   }
-  for (int k = 0; k < m.n_j; ++k) {
+  for (int k = r; k < m.n_j; k += 4) {
     double v = 0.0;
     if (valid) v = k < m.n_theta ? io.p_spec[s * m.n_theta + k] : io.q_spec[s * m.n_q + (k - m.n_theta)];
     EL(A, m.off_spec + k) = v;
   }
+  if (r) return;
   w.active[s] = valid;
   w.status[s] = 0;
   w.iters[s] = 0;
@@ -206,15 +218,15 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
 }
 
 __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
   bool neg = false;
-  for (int i = i0; i < i1; ++i) {
+  for (int i = i0 + r; i < i1; i += 4) {
     const double t = EL(A, m.off_th + i), v = EL(A, m.off_vm + i);
     double sn, cs;
     sincos(t, &sn, &cs);
@@ -224,20 +236,20 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
     EL(A, m.off_u + 2 * i + 1) = v * sn;
     neg |= v <= 0.0;
   }
-  if (neg) atomicOr(&w.flags[g * kGroup + lane], 4);
+  if (neg) atomicOr(&w.flags[g * kGroup + sc], 4);
 }
 
 __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
-  for (int i = i0; i < i1; ++i) {
+  for (int i = i0 + r; i < i1; i += 4) {
     double2 acc = make_double2(0.0, 0.0);
     const int e1 = m.y_rowptr[i + 1];
     for (int e = m.y_rowptr[i]; e < e1; ++e) {
@@ -292,7 +304,7 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
       if (sl.w >= 0) EL(A, m.off_lu + sl.w) = dv.y;
     }
   }
-  const int64_t s = g * kGroup + lane;
+  const int64_t s = g * kGroup + sc;
   // fmax of non-negative doubles is the max of their bit patterns
   if (fmx > 0.0) atomicMax(&w.fmax_bits[s], (unsigned long long)__double_as_longlong(fmx));
   if (bad) atomicOr(&w.flags[s], bad);
@@ -302,8 +314,8 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= w.groups) return;
-  const int64_t s = g * kGroup + lane;
-  bool act = s < batch && w.active[s];
+  const int64_t s = g * kGroup + (lane & 7);
+  bool act = lane < kGroup && s < batch && w.active[s];
   if (act) {
     const double fmx = __longlong_as_double((long long)w.fmax_bits[s]);
     const int fl = w.flags[s];
@@ -328,7 +340,7 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
       act = false;
     }
   }
-  if (s < batch) {
+  if (lane < kGroup && s < batch) {
     w.fmax_bits[s] = 0ull;
     w.flags[s] = 0;
   }
@@ -342,20 +354,22 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
 // One elimination level: task = (row of the level, group).
 __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int r0) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
   const int p = r0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
   const uint32_t ring = su32(smem);
-  const uint32_t wring = ring + kNBuf * kCh * kElemBytes;
-  const uint32_t lbuf = wring + kNBuf * kCh * 4 + lane * 8;
+  const uint32_t wring = ring + kRing * kElemBytes;
+  const uint32_t lbuf = wring + kRing * 4 + sc * 8;
   Pipe pp;
-  pp.arena = A;
+  pp.arena = w.arena + (size_t)g * m.n_elem * kGroup;
   pp.ring = ring;
   pp.wring = wring;
   pp.lane = lane;
+  pp.r = r;
+  pp.sc = sc;
   pp.begin(m.stream, m.row_sptr[p], m.row_sptr[p + 1]);
   const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
   double yacc = pp.get();  // b_p
@@ -367,95 +381,103 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
     const uint32_t info = __shfl_sync(kFull, winfo, j);
     const int cnt = (int)(info >> 16);
     double a = (info & kSlotFill) ? 0.0 : pp.get();
-    double a2 = 0.0;
-    int q = 0;
-    for (; q + 1 < cnt; q += 2) {
-      uint32_t w0, w1;
-      const double u0 = pp.get(w0);
-      const double u1 = pp.get(w1);
-      a = fma(-lds_f64(lbuf + (w0 >> 22) * kElemBytes), u0, a);
-      a2 = fma(-lds_f64(lbuf + (w1 >> 22) * kElemBytes), u1, a2);
+    if (cnt) {
+      // Crout updates split over the quad: sub-lane r takes pairs r, r+4, ...
+      double part = 0.0;
+      int done = 0;
+      while (done < cnt) {
+        pp.ensure(pp.q);
+        const int nb = min(cnt - done, pp.ready_upto - pp.q);
+#pragma unroll 2
+        for (int k = r; k < nb; k += 4) {
+          const int e = pp.q + k;
+          const uint32_t wd = pp.word(e);
+          part = fma(-lds_f64(lbuf + (wd >> 22) * kElemBytes), lds_f64(pp.addr(e)), part);
+        }
+        pp.q += nb;
+        done += nb;
+      }
+      a = a + quad_sum(part);
     }
-    if (q < cnt) {
-      uint32_t w0;
-      const double u0 = pp.get(w0);
-      a = fma(-lds_f64(lbuf + (w0 >> 22) * kElemBytes), u0, a);
-    }
-    a = a + a2;
     if (info & kSlotL) {
       const double inv = pp.get();
       const double yc = pp.get();
       a *= inv;
       yacc = fma(-a, yc, yacc);
+      // all quad lanes hold the same value and each writes it, so later
+      // reads by a lane depend only on its own store
       sts_f64(lbuf + (t - t0) * kElemBytes, a);
     } else {
       if (info & kSlotDiag) {
         zero |= a == 0.0;
-        EL(A, m.off_invd + p) = 1.0 / a;
+        if (r == 0) EL(A, m.off_invd + p) = 1.0 / a;
       }
-      EL(A, m.off_lu + t) = a;
+      if (r == 0) EL(A, m.off_lu + t) = a;
     }
   }
-  EL(A, m.off_yx + p) = yacc;
+  if (r == 0) EL(A, m.off_yx + p) = yacc;
   pp.finish();
-  if (zero) atomicOr(&w.flags[g * kGroup + lane], 8);
+  if (zero && r == 0) atomicOr(&w.flags[g * kGroup + sc], 8);
 }
 
 // One back-substitution level: task = (row of the level, group).
 __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int b0) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
-  const int r = b0 + (int)(task / w.groups);
+  const int rr = b0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
   const uint32_t ring = su32(smem);
   Pipe pp;
-  pp.arena = A;
+  pp.arena = w.arena + (size_t)g * m.n_elem * kGroup;
   pp.ring = ring;
-  pp.wring = ring + kNBuf * kCh * kElemBytes;
+  pp.wring = ring + kRing * kElemBytes;
   pp.lane = lane;
-  pp.begin(m.stream, m.brow_sptr[r], m.brow_sptr[r + 1]);
-  const uint32_t b = m.brow[r];
+  pp.r = r;
+  pp.sc = sc;
+  pp.begin(m.stream, m.brow_sptr[rr], m.brow_sptr[rr + 1]);
+  const uint32_t b = m.brow[rr];
   const int p = (int)(b & 0xfffffu);
   const int cnt = (int)(b >> 20);
-  double acc = pp.get();
+  const double y0 = pp.get();
   const double inv = pp.get();
-  double acc2 = 0.0;
-  int q = 0;
-  for (; q + 1 < cnt; q += 2) {
-    const double u0 = pp.get(), x0 = pp.get();
-    const double u1 = pp.get(), x1 = pp.get();
-    acc = fma(-u0, x0, acc);
-    acc2 = fma(-u1, x1, acc2);
+  double part = 0.0;
+  int done = 0;  // (u, x) pairs consumed
+  while (done < cnt) {
+    pp.ensure(pp.q + 1);  // both elements of the next pair resident
+    const int nb = min(cnt - done, (pp.ready_upto - pp.q) >> 1);
+    for (int k = r; k < nb; k += 4) {
+      const int e = pp.q + 2 * k;
+      part = fma(-lds_f64(pp.addr(e)), lds_f64(pp.addr(e + 1)), part);
+    }
+    pp.q += 2 * nb;
+    done += nb;
   }
-  if (q < cnt) {
-    const double u0 = pp.get(), x0 = pp.get();
-    acc = fma(-u0, x0, acc);
-  }
-  EL(A, m.off_yx + p) = (acc + acc2) * inv;
+  const double x = (y0 + quad_sum(part)) * inv;
+  if (r == 0) EL(A, m.off_yx + p) = x;
   pp.finish();
 }
 
 __global__ void nr_update_kernel(NrDeviceModel m, NrWorkspace w, int k) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
-  const int64_t s = g * kGroup + lane;
+  const int64_t s = g * kGroup + sc;
   if (!w.active[s]) return;
   if (w.flags[s] & 8) {  // zero pivot in this step's factorisation: stop here
-    if (item % nch == 0) {
+    if (item % nch == 0 && r == 0) {
       w.status[s] = ACPF_NR_ZERO_PIVOT;
       w.iters[s] = k;
     }
     return;
   }
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
-  for (int i = i0; i < i1; ++i) {
+  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  for (int i = i0 + r; i < i1; i += 4) {
     const int tp = m.tpos[i], qp = m.qpos[i];
     if (tp >= 0) EL(A, m.off_th + i) = EL(A, m.off_th + i) + EL(A, m.off_yx + m.ipos[tp]);
     if (qp >= 0) EL(A, m.off_vm + i) = EL(A, m.off_vm + i) + EL(A, m.off_yx + m.ipos[qp]);
@@ -470,20 +492,20 @@ __global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch) {
 }
 
 __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int64_t g = item / nch;
   if (g >= w.groups) return;
-  const int64_t s = g * kGroup + lane;
+  const int64_t s = g * kGroup + sc;
   if (s >= io.batch) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  const double* A = w.arena + (size_t)g * m.n_elem * kGroup + lane;
-  for (int i = i0; i < i1; ++i) {
+  const double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  for (int i = i0 + r; i < i1; i += 4) {
     io.theta_out[s * m.n_bus + i] = EL(A, m.off_th + i);
     io.vmag_out[s * m.n_bus + i] = EL(A, m.off_vm + i);
   }
-  if (item % nch == 0) {
+  if (item % nch == 0 && r == 0) {
     const int st = w.status[s];
     if (io.converged) io.converged[s] = st == ACPF_NR_CONVERGED;
     if (io.iterations) io.iterations[s] = w.iters[s];
@@ -492,7 +514,7 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
-size_t pipe_smem() { return (size_t)kNBuf * kCh * (kElemBytes + 4); }
+size_t pipe_smem() { return (size_t)kRing * (kElemBytes + 4); }
 
 }  // namespace
 
