@@ -167,11 +167,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     return ACPF_ENOMEM;
   }
   try {
+    // symbolic analysis on the bus graph: one 2x2 block unknown per non-slack
+    // bus (theta_block order), Jacobian block pattern = Ybus pattern
     NrSymbolic first;
-    build_nr_symbolic(first, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+    build_nr_symbolic(first, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, perm);
     const std::vector<int32_t> lperm = level_sorted_perm(first);
-    build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block,
-                      lperm.data());
+    build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, lperm.data());
     build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
@@ -182,27 +183,33 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   DeviceGuard dg(device);
   const NrSymbolic& s = p->sym;
   const NrSchedule& sc = p->sch;
-  const int nj = s.n_j;
   const int64_t nnz = y_rowptr[n_bus];
   std::vector<double2> yv(nnz);
   for (int64_t e = 0; e < nnz; ++e) yv[e] = make_double2(y_re[e], y_im[e]);
-  std::vector<int32_t> tpos(n_bus, -1), qpos(n_bus, -1);
+  std::vector<int32_t> tpos(n_bus, -1), qidx(n_bus, -1);
   for (int k = 0; k < n_theta; ++k) tpos[theta_block[k]] = k;
-  for (int k = 0; k < n_q; ++k) qpos[q_block[k]] = n_theta + k;
+  for (int k = 0; k < n_q; ++k) {
+    if (q_block[k] < 0 || q_block[k] >= n_bus || tpos[q_block[k]] < 0) {
+      set_error("acpf_nr_plan_create: q_block bus must be in theta_block");
+      delete p;
+      return ACPF_EINVAL;
+    }
+    qidx[q_block[k]] = k;
+  }
 
   NrDeviceModel& d = p->dm;
   d.n_bus = n_bus;
   d.n_theta = n_theta;
   d.n_q = n_q;
-  d.n_j = nj;
+  d.n_rows = s.n_j;
   d.nnz_lu = s.nnz_lu;
-  d.n_elem = sc.n_elem;
+  d.n_block = sc.n_block;
+  d.n_scalar = sc.n_scalar;
   d.off_lu = sc.off_lu;
   d.off_invd = sc.off_invd;
   d.off_yx = sc.off_yx;
   d.off_u = sc.off_u;
   d.off_e = sc.off_e;
-  d.off_i = sc.off_i;
   d.off_spec = sc.off_spec;
   d.off_th = sc.off_th;
   d.off_vm = sc.off_vm;
@@ -222,14 +229,13 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<double**>(&d.theta_init), theta_init, (size_t)n_bus);
   up(const_cast<double**>(&d.vmag_init), vmag_init, (size_t)n_bus);
   up(const_cast<int32_t**>(&d.tpos), tpos.data(), (size_t)n_bus);
-  up(const_cast<int32_t**>(&d.qpos), qpos.data(), (size_t)n_bus);
-  up(const_cast<int32_t**>(&d.ipos), s.ipos.data(), (size_t)nj);
+  up(const_cast<int32_t**>(&d.qidx), qidx.data(), (size_t)n_bus);
+  up(const_cast<int32_t**>(&d.bus_row), sc.bus_row.data(), sc.bus_row.size());
   up(const_cast<int32_t**>(&d.asm_ptr), sc.asm_ptr.data(), sc.asm_ptr.size());
   up(const_cast<double2**>(&d.asm_y), reinterpret_cast<const double2*>(sc.asm_y.data()),
      sc.asm_y.size() / 2);
   up(const_cast<int32_t**>(&d.asm_j), sc.asm_j.data(), sc.asm_j.size());
-  up(const_cast<int4**>(&d.asm_slot), reinterpret_cast<const int4*>(sc.asm_slot.data()),
-     sc.asm_slot.size() / 4);
+  up(const_cast<int32_t**>(&d.asm_slot), sc.asm_slot.data(), sc.asm_slot.size());
   up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
   up(const_cast<int32_t**>(&d.row_slot), sc.row_slot.data(), sc.row_slot.size());
   up(const_cast<int32_t**>(&d.row_sptr), sc.row_sptr.data(), sc.row_sptr.size());
@@ -243,7 +249,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     delete p;
     return e == cudaErrorMemoryAllocation ? ACPF_ENOMEM : ACPF_ECUDA;
   }
-  p->bytes_per_group = sc.n_elem * kGroup * 8 + (int64_t)nr_group_state_bytes();
+  p->bytes_per_group =
+      (sc.n_block * 4 * kGroup + sc.n_scalar * kGroup) * 8 + (int64_t)nr_group_state_bytes();
   *out = p;
   return ACPF_OK;
 }
@@ -257,7 +264,9 @@ acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_
   }
   try {
     NrSymbolic s;
-    build_nr_symbolic(s, n_bus, y_rowptr, y_col, n_theta, theta_block, n_q, q_block, perm);
+    (void)n_q;
+    (void)q_block;
+    build_nr_symbolic(s, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, perm);
     fill_info(s, info);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
@@ -301,7 +310,7 @@ static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
     }
     return ptr;
   };
-  w.arena = (double*)get((size_t)groups * p->sch.n_elem * kGroup * 8);
+  w.arena = (double*)get((size_t)groups * (p->sch.n_block * 4 + p->sch.n_scalar) * kGroup * 8);
   w.fmax_bits = (unsigned long long*)get(S * 8);
   w.flags = (int*)get(S * 4);
   w.status = (int*)get(S * 4);

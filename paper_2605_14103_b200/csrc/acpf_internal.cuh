@@ -18,29 +18,30 @@ constexpr int kGroup = 8;  // NR: scenarios per warp (a quad of lanes each)
 // Newton plan (device side view passed to the kernel by value)
 // ---------------------------------------------------------------------------
 struct NrDeviceModel {
-  int n_bus, n_theta, n_q, n_j;
+  int n_bus, n_theta, n_q, n_rows;
   const int32_t* y_rowptr;
   const int32_t* y_col;
   const double2* y_val;
   const double* theta_init;
   const double* vmag_init;
-  const int32_t* tpos;  // [n_bus] packed theta index or -1
-  const int32_t* qpos;  // [n_bus] packed V index (>= n_theta) or -1
-  const int32_t* ipos;  // [n_j] packed -> elimination position
-  // level-synchronous Crout schedule (nr_symbolic.h NrSchedule)
+  const int32_t* tpos;     // [n_bus] index into p_spec (theta block) or -1
+  const int32_t* qidx;     // [n_bus] index into q_spec (q block) or -1
+  const int32_t* bus_row;  // [n_bus] block row of the bus or -1 (slack)
+  // level-synchronous 2x2-block Crout schedule (nr_symbolic.h NrSchedule)
   const int32_t* asm_ptr;     // [n_bus+1] Jacobian assembly list per bus
   const double2* asm_y;       // [entries]
   const int32_t* asm_j;       // [entries]
-  const int4* asm_slot;       // [entries] H, N, M, L slots (-1 absent)
+  const int32_t* asm_slot;    // [entries] LU block slot (-1 slack column)
   const uint32_t* slot_info;  // [nnz_lu]
-  const int32_t* row_slot;    // [n_j+1]
-  const int32_t* row_sptr;    // [n_j+1]
-  const uint32_t* brow;       // [n_j]
-  const int32_t* brow_sptr;   // [n_j+1]
+  const int32_t* row_slot;    // [n_rows+1]
+  const int32_t* row_sptr;    // [n_rows+1]
+  const uint32_t* brow;       // [n_rows]
+  const int32_t* brow_sptr;   // [n_rows+1]
   const uint32_t* stream;     // [n_stream]
   int64_t nnz_lu;
-  int64_t n_elem;
-  int64_t off_lu, off_invd, off_yx, off_u, off_e, off_i, off_spec, off_th, off_vm;
+  int64_t n_block, n_scalar;  // arena elements per group (block / scalar region)
+  int64_t off_lu, off_invd, off_yx;                   // block region
+  int64_t off_u, off_e, off_spec, off_th, off_vm;     // scalar region
 };
 
 struct NrHostSchedule {
@@ -51,7 +52,7 @@ struct NrHostSchedule {
 };
 
 struct NrWorkspace {
-  double* arena;  // [groups][n_elem][kGroup]
+  double* arena;  // [groups][block region | scalar region]
   int64_t groups;
   // per scenario [groups*kGroup]
   unsigned long long* fmax_bits;

@@ -1,41 +1,42 @@
-// Batched polar Newton-Raphson on sm_100a: level-synchronous sparse LU.
+// Batched polar Newton-Raphson on sm_100a: level-synchronous 2x2-block sparse LU.
 //
-// Data layout: scenarios are processed in groups of kGroup = 8; each
-// scenario owns a quad of lanes (lane = r*8 + sc, sub-lane r = 0..3). Every
-// per-scenario quantity lives in a per-group arena of "elements", element e of
-// scenario sc at arena[e*8 + sc], so one element of a group is 64 contiguous
-// bytes and a warp instruction touching 4 elements moves four fully used
-// 64-byte segments. The schedule (Ybus, LU pattern, Crout updates) is shared
-// by all groups.
+// Unknowns are grouped per non-slack bus into 2x2 blocks (theta_i, V_i); a PV
+// bus carries a padded V_i with the identity equation dV_i = 0, which leaves
+// theta and the PQ magnitudes of the Newton step unchanged. The Jacobian is
+// then a block matrix with the Ybus pattern and every stream element, every
+// Crout update and every store moves a whole 2x2 block.
+//
+// Data layout: scenarios are processed in groups of kGroup = 8 and each
+// scenario owns a quad of lanes (lane = r*8 + sc): in block operations lane r
+// owns entry (r/2, r%2) of every 2x2 block of scenario sc. A per-group arena
+// holds a block region (element = 4 entries x 8 scenarios = 256 contiguous
+// bytes, entry-major, so one LDGSTS/STG per lane moves a whole element for the
+// group) followed by a scalar region (element = 8 scenarios = 64 bytes).
 //
 // One Newton step of the reference `_newton_loop` (transmission.py:333-380)
 // for the whole batch is a short sequence of launches on one stream:
 //   nr_phasor    u = V e^{j theta}, E = e^{j theta}; V <= 0 flag  (transmission.py:196, :355)
 //   nr_mismatch  I = Y u, S = u conj(I), F -> rhs, ||F||inf, non-finite flags
-//                (transmission.py:194-215), and the Jacobian blocks H, N, M, L
-//                of every Ybus entry straight into their LU slots
+//                (transmission.py:194-215), and the 2x2 Jacobian block
+//                [[H, N], [M, L]] of every Ybus entry straight into its LU slot
 //                (dense_jacobian formulas, transmission.py:383-407)
 //   nr_check     the reference exit checks in order: non-finite -> converged
 //                -> min V <= 0 -> k == max_newton (transmission.py:347-359)
-//   nr_factor    one launch per elimination level: every (row of the level,
-//                group) pair is an independent warp task that computes the
-//                row by Crout (dot-product) updates + fused forward
-//                substitution; rows of one level never read each other
+//   nr_factor    one launch per elimination level: every (block row of the
+//                level, group) pair is an independent warp task computing the
+//                row by block Crout updates + fused forward substitution
 //   nr_back      one launch per back-substitution level
 //   nr_update    x += dx (transmission.py:378)
 // This replaces the reference's FD-preconditioned GMRES step
-// (transmission.py:361-369) by an exact static-pivot sparse LU solve.
+// (transmission.py:361-369) by an exact sparse LU solve (static 2x2 pivots).
 //
-// Inside a factor/back task every operand that is not produced by the task
-// itself (earlier U rows, pivots, y/x, assembled J values) is a precomputed
-// element index in a gather stream; the warp runs a cp.async (LDGSTS)
-// multistage pipeline over its stream (16 elements per stage, 15 stages =
-// 240 elements in flight) into a shared-memory ring, and the quad of a
-// scenario splits every dot product 4 ways (partial sums combined by a fixed
-// shuffle butterfly). No stream element of a task can be
-// produced by another task of the same level, so the pipeline needs no
-// hazard checks. The task's own L values stay in shared memory (later rows
-// only read U), so global traffic is the U gathers plus one write per U slot.
+// Inside a factor/back task every operand not produced by the task itself
+// (earlier U blocks, pivot-block inverses, y/x, assembled J blocks) is a
+// precomputed element index in a gather stream; the warp runs a cp.async
+// (LDGSTS) multistage pipeline over it (8 elements per stage, 6 stages in
+// flight) into a shared-memory ring. No element of a task can be produced by
+// another task of the same level, so the pipeline needs no hazard checks.
+// The row's own L blocks stay in shared memory (later rows only read U).
 
 #include "acpf_internal.cuh"
 
@@ -44,10 +45,11 @@ namespace acpf {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCh = 16;    // elements per pipeline stage
-constexpr int kNBuf = 16;  // stages in the ring (kNBuf-1 in flight)
+constexpr int kCh = 8;     // elements per pipeline stage
+constexpr int kNBuf = 8;   // stages in the ring (kNBuf-1 in flight)
 constexpr int kRing = kCh * kNBuf;
-constexpr int kElemBytes = kGroup * 8;  // 64
+constexpr int kBlk = 4 * kGroup;      // doubles per block element (32)
+constexpr int kBlkBytes = kBlk * 8;   // 256
 constexpr int kBusChunk = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -94,25 +96,15 @@ __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
   return make_double2(u.x * a.x + u.y * a.y, u.y * a.x - u.x * a.y);
 }
 
-// sum over the quad of a scenario (lanes sc, sc+8, sc+16, sc+24), fixed order
-__device__ __forceinline__ double quad_sum(double x) {
-  x = x + __shfl_xor_sync(kFull, x, 8);
-  x = x + __shfl_xor_sync(kFull, x, 16);
-  return x;
-}
-
 // Per-warp gather pipeline over the stream range [s0, s0 + n).
 struct Pipe {
   const uint32_t* stream;
-  const double* arena;  // group arena base (element e, scenario sc at arena[e*8 + sc])
-  uint32_t ring;        // smem [kRing][8] doubles
-  uint32_t wring;       // smem [kRing] u32 stream words
-  int lane, r, sc;
-  int s0, n;            // first stream index, element count
-  int issued;           // stages issued
-  int ready_upto;       // elements [0, ready_upto) are resident
-  int q;                // next element to consume (relative)
-  uint32_t wcur, wnext; // word windows: lane j holds the word of element (wbase + j)
+  const double* blocks;  // group block region (element e at blocks + e*32)
+  uint32_t ring;         // smem [kRing] elements of 256 B
+  uint32_t wring;        // smem [kRing] u32 stream words
+  int lane;
+  int s0, n, issued, ready_upto, q;
+  uint32_t wcur, wnext;  // word windows: lane j holds the word of element (wbase + j)
   int wbase;
 
   __device__ __forceinline__ uint32_t load_window(int base) const {
@@ -131,15 +123,14 @@ struct Pipe {
       }
       const int slot = (c % kNBuf) * kCh;
       const int lim = min(kCh, n - e0);
-      const int jw = e0 - wbase;  // 0 or 16
+      const int jw = e0 - wbase;
       const uint32_t mine = __shfl_sync(kFull, wcur, (jw + lane) & 31);
       if (lane < lim) sts_u32(wring + (slot + lane) * 4, mine);
 #pragma unroll
-      for (int j = 0; j < kCh / 4; ++j) {
-        const int e = 4 * j + r;
-        const uint32_t w = __shfl_sync(kFull, wcur, (jw + e) & 31);
-        if (e < lim)
-          cp_async8(ring + ((slot + e) * kGroup + sc) * 8, arena + (size_t)(w & 0x3fffffu) * kGroup + sc);
+      for (int j = 0; j < kCh; ++j) {
+        const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
+        if (j < lim)
+          cp_async8(ring + (slot + j) * kBlkBytes + lane * 8, blocks + (size_t)(w & 0x3fffffu) * kBlk + lane);
       }
     }
     cp_commit();
@@ -156,32 +147,27 @@ struct Pipe {
     wcur = load_window(0);
     wnext = load_window(32);
 #pragma unroll 1
-    for (int k = 0; k < kNBuf - 1; ++k) issue_stage();
+    for (int k = 0; k < kNBuf - 2; ++k) issue_stage();
   }
 
-  // make element e resident; elements < q must already be consumed
+  // Make element e resident. Callers keep e <= q + 1 (q = first element not
+  // yet consumed). kNBuf-2 stages are in flight, so the stage issued here
+  // reuses the slot of stage (e/kCh - 2), which is fully consumed.
   __device__ __forceinline__ void ensure(int e) {
     while (e >= ready_upto) {
-      cp_wait<kNBuf - 2>();
+      cp_wait<kNBuf - 3>();
       __syncwarp();
       issue_stage();
       ready_upto += kCh;
     }
   }
 
-  __device__ __forceinline__ uint32_t addr(int e) const {
-    return ring + (((e % kRing) * kGroup) + sc) * 8;
+  // smem address of entry `ent` (0..3) of element e for scenario sc
+  __device__ __forceinline__ uint32_t addr(int e, int ent, int sc) const {
+    return ring + (e % kRing) * kBlkBytes + (ent * kGroup + sc) * 8;
   }
 
   __device__ __forceinline__ uint32_t word(int e) const { return lds_u32(wring + (e % kRing) * 4); }
-
-  // scalar element: every sub-lane reads its scenario's value
-  __device__ __forceinline__ double get() {
-    ensure(q);
-    const double v = lds_f64(addr(q));
-    ++q;
-    return v;
-  }
 
   __device__ __forceinline__ void finish() {
     cp_wait<0>();
@@ -189,7 +175,21 @@ struct Pipe {
   }
 };
 
-#define EL(A, e) (A)[(size_t)(e) * kGroup]
+// block-region entry `ent` of block element e, scenario sc (B = group block base + sc)
+#define BL(B, e, ent) (B)[((size_t)(e) * 4 + (ent)) * kGroup]
+// scalar-region element e, scenario sc (S = group scalar base + sc)
+#define SL(S, e) (S)[(size_t)(e) * kGroup]
+
+struct GroupBase {
+  double* b;  // block region + sc
+  double* s;  // scalar region + sc
+};
+
+__device__ __forceinline__ GroupBase group_base(const NrDeviceModel& m, const NrWorkspace& w, int64_t g,
+                                                int sc) {
+  double* base = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
+  return GroupBase{base + sc, base + m.n_block * kBlk + sc};
+}
 
 __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
@@ -197,15 +197,16 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   if (g >= w.groups) return;
   const int64_t s = g * kGroup + sc;
   const bool valid = s < io.batch;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   for (int i = r; i < m.n_bus; i += 4) {
-    EL(A, m.off_th + i) = m.theta_init[i];
-    EL(A, m.off_vm + i) = m.vmag_init[i];
-  }
-  for (int k = r; k < m.n_j; k += 4) {
-    double v = 0.0;
-    if (valid) v = k < m.n_theta ? io.p_spec[s * m.n_theta + k] : io.q_spec[s * m.n_q + (k - m.n_theta)];
-    EL(A, m.off_spec + k) = v;
+    SL(gb.s, m.off_th + i) = m.theta_init[i];
+    SL(gb.s, m.off_vm + i) = m.vmag_init[i];
+    const int p = m.bus_row[i];
+    if (p >= 0) {
+      const int tp = m.tpos[i], qi = m.qidx[i];
+      SL(gb.s, m.off_spec + 2 * p) = valid ? io.p_spec[s * m.n_theta + tp] : 0.0;
+      SL(gb.s, m.off_spec + 2 * p + 1) = (valid && qi >= 0) ? io.q_spec[s * m.n_q + qi] : 0.0;
+    }
   }
   if (r) return;
   w.active[s] = valid;
@@ -214,7 +215,7 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   w.fout[s] = 0.0;
   w.fmax_bits[s] = 0ull;
   w.flags[s] = 0;
-  if (lane == 0) w.gactive[g] = 1;
+  if (sc == 0) w.gactive[g] = 1;
 }
 
 __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
@@ -224,16 +225,16 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   bool neg = false;
   for (int i = i0 + r; i < i1; i += 4) {
-    const double t = EL(A, m.off_th + i), v = EL(A, m.off_vm + i);
+    const double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
     double sn, cs;
     sincos(t, &sn, &cs);
-    EL(A, m.off_e + 2 * i) = cs;
-    EL(A, m.off_e + 2 * i + 1) = sn;
-    EL(A, m.off_u + 2 * i) = v * cs;
-    EL(A, m.off_u + 2 * i + 1) = v * sn;
+    SL(gb.s, m.off_e + 2 * i) = cs;
+    SL(gb.s, m.off_e + 2 * i + 1) = sn;
+    SL(gb.s, m.off_u + 2 * i) = v * cs;
+    SL(gb.s, m.off_u + 2 * i + 1) = v * sn;
     neg |= v <= 0.0;
   }
   if (neg) atomicOr(&w.flags[g * kGroup + sc], 4);
@@ -246,49 +247,52 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
   for (int i = i0 + r; i < i1; i += 4) {
+    const int p = m.bus_row[i];
+    if (p < 0) continue;  // slack: no equations
     double2 acc = make_double2(0.0, 0.0);
     const int e1 = m.y_rowptr[i + 1];
     for (int e = m.y_rowptr[i]; e < e1; ++e) {
       const double2 y = m.y_val[e];
       const int c = m.y_col[e];
-      const double ur = EL(A, m.off_u + 2 * c), ui = EL(A, m.off_u + 2 * c + 1);
+      const double ur = SL(gb.s, m.off_u + 2 * c), ui = SL(gb.s, m.off_u + 2 * c + 1);
       acc.x += y.x * ur - y.y * ui;
       acc.y += y.x * ui + y.y * ur;
     }
-    const double2 u = make_double2(EL(A, m.off_u + 2 * i), EL(A, m.off_u + 2 * i + 1));
+    const double2 u = make_double2(SL(gb.s, m.off_u + 2 * i), SL(gb.s, m.off_u + 2 * i + 1));
     const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
-    const int tp = m.tpos[i], qp = m.qpos[i];
-    if (tp >= 0) {
-      const double f = sv.x - EL(A, m.off_spec + tp);
-      bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
-      fmx = fmx < fabs(f) ? fabs(f) : fmx;
-      EL(A, m.off_yx + m.ipos[tp]) = -f;
+    const bool pq = m.qidx[i] >= 0;
+    const double fp = sv.x - SL(gb.s, m.off_spec + 2 * p);
+    bad |= isnan(fp) ? 1 : (isinf(fp) ? 2 : 0);
+    fmx = fmx < fabs(fp) ? fabs(fp) : fmx;
+    BL(gb.b, m.off_yx + p, 0) = -fp;
+    double fq = 0.0;
+    if (pq) {
+      fq = sv.y - SL(gb.s, m.off_spec + 2 * p + 1);
+      bad |= isnan(fq) ? 1 : (isinf(fq) ? 2 : 0);
+      fmx = fmx < fabs(fq) ? fabs(fq) : fmx;
     }
-    if (qp >= 0) {
-      const double f = sv.y - EL(A, m.off_spec + qp);
-      bad |= isnan(f) ? 1 : (isinf(f) ? 2 : 0);
-      fmx = fmx < fabs(f) ? fabs(f) : fmx;
-      EL(A, m.off_yx + m.ipos[qp]) = -f;
-    }
-    // Jacobian blocks of row bus i into their LU slots:
+    BL(gb.b, m.off_yx + p, 1) = -fq;
+    // 2x2 Jacobian block of every Ybus entry (i, j) into its LU slot:
     //   dS_i/dth_j = -j u_i conj(y u_j)  (j != i);  dS_i/dth_i = j u_i conj(I_i - y u_i)
     //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
-    //   H = Re dS/dth, N = Re dS/dV, M = Im dS/dth, L = Im dS/dV
-    const double2 ei = make_double2(EL(A, m.off_e + 2 * i), EL(A, m.off_e + 2 * i + 1));
+    //   [[H, N], [M, L]] = [[Re dS/dth, Re dS/dV], [Im dS/dth, Im dS/dV]]
+    // with the PV padding rows/columns of the identity equation dV = 0.
+    const double2 ei = make_double2(SL(gb.s, m.off_e + 2 * i), SL(gb.s, m.off_e + 2 * i + 1));
     const int a1 = m.asm_ptr[i + 1];
     for (int a = m.asm_ptr[i]; a < a1; ++a) {
+      const int slot = m.asm_slot[a];
+      if (slot < 0) continue;  // slack column
       const double2 y = m.asm_y[a];
       const int jb = m.asm_j[a];
-      const int4 sl = m.asm_slot[a];
-      const double2 ej = make_double2(EL(A, m.off_e + 2 * jb), EL(A, m.off_e + 2 * jb + 1));
+      const double2 ej = make_double2(SL(gb.s, m.off_e + 2 * jb), SL(gb.s, m.off_e + 2 * jb + 1));
       const double2 wv = mul_conj(u, cmul(y, ej));
       double2 dth, dv;
       if (jb != i) {
-        const double2 uj = make_double2(EL(A, m.off_u + 2 * jb), EL(A, m.off_u + 2 * jb + 1));
+        const double2 uj = make_double2(SL(gb.s, m.off_u + 2 * jb), SL(gb.s, m.off_u + 2 * jb + 1));
         const double2 wt = mul_conj(u, cmul(y, uj));
         dth = make_double2(wt.y, -wt.x);
         dv = wv;
@@ -298,10 +302,11 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
         dth = make_double2(-wt.y, wt.x);
         dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
       }
-      if (sl.x >= 0) EL(A, m.off_lu + sl.x) = dth.x;
-      if (sl.y >= 0) EL(A, m.off_lu + sl.y) = dv.x;
-      if (sl.z >= 0) EL(A, m.off_lu + sl.z) = dth.y;
-      if (sl.w >= 0) EL(A, m.off_lu + sl.w) = dv.y;
+      const bool pqj = m.qidx[jb] >= 0;
+      BL(gb.b, m.off_lu + slot, 0) = dth.x;                      // H
+      BL(gb.b, m.off_lu + slot, 1) = pqj ? dv.x : 0.0;           // N
+      BL(gb.b, m.off_lu + slot, 2) = pq ? dth.y : 0.0;           // M
+      BL(gb.b, m.off_lu + slot, 3) = (pq && pqj) ? dv.y : (jb == i && !(pq && pqj) ? 1.0 : 0.0);  // L
     }
   }
   const int64_t s = g * kGroup + sc;
@@ -351,112 +356,135 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
   }
 }
 
-// One elimination level: task = (row of the level, group).
+// One elimination level: task = (block row of the level, group).
+// Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every block of scenario sc.
 __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int r0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
+  const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
   const int p = r0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   const uint32_t ring = su32(smem);
-  const uint32_t wring = ring + kRing * kElemBytes;
-  const uint32_t lbuf = wring + kRing * 4 + sc * 8;
+  const uint32_t wring = ring + kRing * kBlkBytes;
+  const uint32_t lbuf = wring + kRing * 4;
+  // lbuf entry (i, k) of L block at row position pos, scenario sc
+  auto lb = [&](int pos, int ent) { return lbuf + pos * kBlkBytes + (ent * kGroup + sc) * 8; };
   Pipe pp;
-  pp.arena = w.arena + (size_t)g * m.n_elem * kGroup;
+  pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
   pp.ring = ring;
   pp.wring = wring;
   pp.lane = lane;
-  pp.r = r;
-  pp.sc = sc;
   pp.begin(m.stream, m.row_sptr[p], m.row_sptr[p + 1]);
   const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
-  double yacc = pp.get();  // b_p
+  pp.ensure(0);
+  double yacc = lds_f64(pp.addr(0, bi, sc));  // b_p[i]
+  pp.q = 1;
   bool zero = false;
   uint32_t winfo = 0;
   for (int t = t0; t < t1; ++t) {
-    const int j = (t - t0) & 31;
-    if (j == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
-    const uint32_t info = __shfl_sync(kFull, winfo, j);
+    const int jj = (t - t0) & 31;
+    if (jj == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
+    const uint32_t info = __shfl_sync(kFull, winfo, jj);
     const int cnt = (int)(info >> 16);
-    double a = (info & kSlotFill) ? 0.0 : pp.get();
-    if (cnt) {
-      // Crout updates split over the quad: sub-lane r takes pairs r, r+4, ...
-      double part = 0.0;
-      int done = 0;
-      while (done < cnt) {
-        pp.ensure(pp.q);
-        const int nb = min(cnt - done, pp.ready_upto - pp.q);
-#pragma unroll 2
-        for (int k = r; k < nb; k += 4) {
-          const int e = pp.q + k;
-          const uint32_t wd = pp.word(e);
-          part = fma(-lds_f64(lbuf + (wd >> 22) * kElemBytes), lds_f64(pp.addr(e)), part);
-        }
-        pp.q += nb;
-        done += nb;
-      }
-      a = a + quad_sum(part);
+    double a = 0.0, a2 = 0.0;
+    if (!(info & kSlotFill)) {
+      pp.ensure(pp.q);
+      a = lds_f64(pp.addr(pp.q, r, sc));
+      ++pp.q;
     }
+    // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j)
+    for (int q = 0; q < cnt;) {
+      pp.ensure(pp.q);
+      const int nb = min(cnt - q, pp.ready_upto - pp.q);
+#pragma unroll 2
+      for (int k = 0; k < nb; ++k) {
+        const int e = pp.q + k;
+        const int pos = (int)(pp.word(e) >> 22);
+        a = fma(-lds_f64(lb(pos, 2 * bi)), lds_f64(pp.addr(e, bj, sc)), a);
+        a2 = fma(-lds_f64(lb(pos, 2 * bi + 1)), lds_f64(pp.addr(e, 2 + bj, sc)), a2);
+      }
+      pp.q += nb;
+      q += nb;
+    }
+    a = a + a2;
     if (info & kSlotL) {
-      const double inv = pp.get();
-      const double yc = pp.get();
-      a *= inv;
-      yacc = fma(-a, yc, yacc);
-      // all quad lanes hold the same value and each writes it, so later
-      // reads by a lane depend only on its own store
-      sts_f64(lbuf + (t - t0) * kElemBytes, a);
+      pp.ensure(pp.q + 1);
+      const int e = pp.q;
+      // L_pt = A' inv(U_tt); y_p -= L_pt y_t
+      const double o = __shfl_xor_sync(kFull, a, 8);  // entry (i, 1-j)
+      const double ai0 = bj ? o : a, ai1 = bj ? a : o;
+      const double l = ai0 * lds_f64(pp.addr(e, bj, sc)) + ai1 * lds_f64(pp.addr(e, 2 + bj, sc));
+      sts_f64(lb(t - t0, r), l);
+      const double lo = __shfl_xor_sync(kFull, l, 8);
+      const double li0 = bj ? lo : l, li1 = bj ? l : lo;
+      yacc = fma(-li1, lds_f64(pp.addr(e + 1, 1, sc)), fma(-li0, lds_f64(pp.addr(e + 1, 0, sc)), yacc));
+      pp.q += 2;
     } else {
       if (info & kSlotDiag) {
-        zero |= a == 0.0;
-        if (r == 0) EL(A, m.off_invd + p) = 1.0 / a;
+        const double a00 = __shfl_sync(kFull, a, sc), a01 = __shfl_sync(kFull, a, 8 + sc);
+        const double a10 = __shfl_sync(kFull, a, 16 + sc), a11 = __shfl_sync(kFull, a, 24 + sc);
+        const double det = a00 * a11 - a01 * a10;
+        zero |= det == 0.0;
+        const double rd = 1.0 / det;
+        const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
+        BL(gb.b, m.off_invd + p, r) = inv;
       }
-      if (r == 0) EL(A, m.off_lu + t) = a;
+      BL(gb.b, m.off_lu + t, r) = a;
     }
   }
-  if (r == 0) EL(A, m.off_yx + p) = yacc;
+  if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
   pp.finish();
   if (zero && r == 0) atomicOr(&w.flags[g * kGroup + sc], 8);
 }
 
-// One back-substitution level: task = (row of the level, group).
+// One back-substitution level: task = (block row of the level, group).
 __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int b0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
+  const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
   const int rr = b0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   const uint32_t ring = su32(smem);
   Pipe pp;
-  pp.arena = w.arena + (size_t)g * m.n_elem * kGroup;
+  pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
   pp.ring = ring;
-  pp.wring = ring + kRing * kElemBytes;
+  pp.wring = ring + kRing * kBlkBytes;
   pp.lane = lane;
-  pp.r = r;
-  pp.sc = sc;
   pp.begin(m.stream, m.brow_sptr[rr], m.brow_sptr[rr + 1]);
   const uint32_t b = m.brow[rr];
   const int p = (int)(b & 0xfffffu);
   const int cnt = (int)(b >> 20);
-  const double y0 = pp.get();
-  const double inv = pp.get();
-  double part = 0.0;
-  int done = 0;  // (u, x) pairs consumed
-  while (done < cnt) {
-    pp.ensure(pp.q + 1);  // both elements of the next pair resident
-    const int nb = min(cnt - done, (pp.ready_upto - pp.q) >> 1);
-    for (int k = r; k < nb; k += 4) {
+  pp.ensure(1);
+  const double yi = lds_f64(pp.addr(0, bi, sc));
+  const double inv0 = lds_f64(pp.addr(1, 2 * bi, sc)), inv1 = lds_f64(pp.addr(1, 2 * bi + 1, sc));
+  pp.q = 2;
+  double part = 0.0;  // sum_c U_pc[i][j] x_c[j]
+  for (int q = 0; q < cnt;) {
+    pp.ensure(pp.q + 1);
+    const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
+    if (nb == 0) {  // a (U, x) pair straddles the ready range
+      pp.ensure(pp.q + 1);
+      continue;
+    }
+    for (int k = 0; k < nb; ++k) {
       const int e = pp.q + 2 * k;
-      part = fma(-lds_f64(pp.addr(e)), lds_f64(pp.addr(e + 1)), part);
+      part = fma(lds_f64(pp.addr(e, r, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
     }
     pp.q += 2 * nb;
-    done += nb;
+    q += nb;
   }
-  const double x = (y0 + quad_sum(part)) * inv;
-  if (r == 0) EL(A, m.off_yx + p) = x;
+  const double po = __shfl_xor_sync(kFull, part, 8);
+  const double acc = yi - (bj ? po + part : part + po);        // (y_p - sum)[i]
+  const double ao = __shfl_xor_sync(kFull, acc, 16);           // the other row
+  const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
+  const double x = inv0 * acc0 + inv1 * acc1;                  // x_p[i]
+  if (bj == 0) BL(gb.b, m.off_yx + p, bi) = x;
   pp.finish();
 }
 
@@ -476,11 +504,12 @@ __global__ void nr_update_kernel(NrDeviceModel m, NrWorkspace w, int k) {
     return;
   }
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   for (int i = i0 + r; i < i1; i += 4) {
-    const int tp = m.tpos[i], qp = m.qpos[i];
-    if (tp >= 0) EL(A, m.off_th + i) = EL(A, m.off_th + i) + EL(A, m.off_yx + m.ipos[tp]);
-    if (qp >= 0) EL(A, m.off_vm + i) = EL(A, m.off_vm + i) + EL(A, m.off_yx + m.ipos[qp]);
+    const int p = m.bus_row[i];
+    if (p < 0) continue;
+    SL(gb.s, m.off_th + i) = SL(gb.s, m.off_th + i) + BL(gb.b, m.off_yx + p, 0);
+    if (m.qidx[i] >= 0) SL(gb.s, m.off_vm + i) = SL(gb.s, m.off_vm + i) + BL(gb.b, m.off_yx + p, 1);
   }
 }
 
@@ -500,10 +529,10 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   const int64_t s = g * kGroup + sc;
   if (s >= io.batch) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  const double* A = w.arena + (size_t)g * m.n_elem * kGroup + sc;
+  const GroupBase gb = group_base(m, w, g, sc);
   for (int i = i0 + r; i < i1; i += 4) {
-    io.theta_out[s * m.n_bus + i] = EL(A, m.off_th + i);
-    io.vmag_out[s * m.n_bus + i] = EL(A, m.off_vm + i);
+    io.theta_out[s * m.n_bus + i] = SL(gb.s, m.off_th + i);
+    io.vmag_out[s * m.n_bus + i] = SL(gb.s, m.off_vm + i);
   }
   if (item % nch == 0 && r == 0) {
     const int st = w.status[s];
@@ -514,11 +543,11 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
-size_t pipe_smem() { return (size_t)kRing * (kElemBytes + 4); }
+size_t pipe_smem() { return (size_t)kRing * (kBlkBytes + 4); }
 
 }  // namespace
 
-size_t nr_smem_bytes(int cap) { return pipe_smem() + (size_t)cap * kElemBytes; }
+size_t nr_smem_bytes(int cap) { return pipe_smem() + (size_t)cap * kBlkBytes; }
 
 size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
 

@@ -267,99 +267,92 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
                        const double* y_re, const double* y_im, NrSchedule& o) {
-  const int nj = s.n_j, nb = s.n_bus;
+  const int nr = s.n_j, nb = s.n_bus;
+  if (s.n_q != 0) throw std::logic_error("block schedule expects a bus-level symbolic analysis");
   // ---- arena layout
+  o.off_lu = 0;
+  o.off_invd = s.nnz_lu;
+  o.off_yx = o.off_invd + nr;
+  o.n_block = o.off_yx + nr;
   int64_t e = 0;
-  o.off_lu = e;    e += s.nnz_lu;
-  o.off_invd = e;  e += nj;
-  o.off_yx = e;    e += nj;
   o.off_u = e;     e += 2 * (int64_t)nb;
   o.off_e = e;     e += 2 * (int64_t)nb;
-  o.off_i = e;     e += 2 * (int64_t)nb;
-  o.off_spec = e;  e += nj;
+  o.off_spec = e;  e += 2 * (int64_t)nr;   // p_spec, q_spec per block row (0 for PV's q)
   o.off_th = e;    e += nb;
   o.off_vm = e;    e += nb;
-  o.n_elem = e;
-  if (o.n_elem >= (1 << 22)) throw std::length_error("arena exceeds 22-bit gather index");
+  o.n_scalar = e;
+  if (o.n_block >= (1 << 22)) throw std::length_error("block arena exceeds 22-bit gather index");
   o.max_l = 0;
-  for (int p = 0; p < nj; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
-  if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 entries");
+  for (int p = 0; p < nr; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
+  if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 blocks");
 
-  // ---- per-bus assembly lists: every Ybus entry (i, j) plus the diagonal
-  // bus block feeds the LU slots of the H, N, M, L derivatives
-  std::vector<int64_t> where(nj, -1);
-  std::vector<int> tpos(nb, -1), qpos(nb, -1);
-  for (int p = 0; p < nj; ++p) {
-    if (s.perm[p] < s.n_theta) tpos[s.row_bus[p]] = p; else qpos[s.row_bus[p]] = p;
-  }
+  // ---- bus -> block row, and per-bus assembly lists
+  o.bus_row.assign(nb, -1);
+  for (int p = 0; p < nr; ++p) o.bus_row[s.row_bus[p]] = p;
+  std::vector<int64_t> where(nr, -1);
   o.asm_ptr.assign(nb + 1, 0);
   o.asm_y.clear();
   o.asm_j.clear();
   o.asm_slot.clear();
   for (int i = 0; i < nb; ++i) {
-    bool have_diag = false;
-    for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) have_diag |= (y_col[k] == i);
-    auto emit = [&](int j, double yr, double yi) {
-      int32_t sl[4] = {-1, -1, -1, -1};  // H (P,theta) N (P,V) M (Q,theta) L (Q,V)
-      const int rows[2] = {tpos[i], qpos[i]};
-      const int cols[2] = {tpos[j], qpos[j]};
-      for (int a = 0; a < 2; ++a) {
-        if (rows[a] < 0) continue;
-        const int p = rows[a];
-        for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
-        for (int b = 0; b < 2; ++b)
-          if (cols[b] >= 0) {
-            const int64_t t = where[cols[b]];
-            if (t < 0) throw std::logic_error("assembly slot missing");
-            sl[a * 2 + b] = (int32_t)t;
-          }
-        for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = -1;
-      }
-      if (sl[0] < 0 && sl[1] < 0 && sl[2] < 0 && sl[3] < 0) return;
-      o.asm_y.push_back(yr);
-      o.asm_y.push_back(yi);
-      o.asm_j.push_back(j);
-      for (int a = 0; a < 4; ++a) o.asm_slot.push_back(sl[a]);
-    };
-    if (!have_diag) emit(i, 0.0, 0.0);
-    for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) emit(y_col[k], y_re[k], y_im[k]);
+    const int p = o.bus_row[i];
+    if (p >= 0) {
+      for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
+      bool have_diag = false;
+      for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) have_diag |= (y_col[k] == i);
+      auto emit = [&](int j, double yr, double yi) {
+        int32_t slot = -1;
+        if (o.bus_row[j] >= 0) {
+          const int64_t t = where[o.bus_row[j]];
+          if (t < 0) throw std::logic_error("assembly slot missing");
+          slot = (int32_t)t;
+        }
+        o.asm_y.push_back(yr);
+        o.asm_y.push_back(yi);
+        o.asm_j.push_back(j);
+        o.asm_slot.push_back(slot);
+      };
+      if (!have_diag) emit(i, 0.0, 0.0);
+      for (int k = y_rowptr[i]; k < y_rowptr[i + 1]; ++k) emit(y_col[k], y_re[k], y_im[k]);
+      for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = -1;
+    }
     o.asm_ptr[i + 1] = (int32_t)o.asm_j.size();
   }
 
   // ---- levels (rows must already be level-sorted)
-  std::vector<int> lev(nj, 0), blev(nj, 0);
-  for (int p = 0; p < nj; ++p) {
+  std::vector<int> lev(nr, 0), blev(nr, 0);
+  for (int p = 0; p < nr; ++p) {
     int l = 0;
     for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) l = std::max(l, lev[s.col[t]] + 1);
     lev[p] = l;
     if (p && lev[p] < lev[p - 1]) throw std::logic_error("rows not level-sorted");
   }
-  for (int p = nj - 1; p >= 0; --p) {
+  for (int p = nr - 1; p >= 0; --p) {
     int l = 0;
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) l = std::max(l, blev[s.col[t]] + 1);
     blev[p] = l;
   }
-  o.n_levels = lev[nj - 1] + 1;
+  o.n_levels = lev[nr - 1] + 1;
   o.n_blevels = 0;
-  for (int p = 0; p < nj; ++p) o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
+  for (int p = 0; p < nr; ++p) o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
   o.level_ptr.assign(o.n_levels + 1, 0);
   o.level_maxl.assign(o.n_levels, 0);
-  for (int p = 0; p < nj; ++p) {
+  for (int p = 0; p < nr; ++p) {
     o.level_ptr[lev[p] + 1] = p + 1;
     o.level_maxl[lev[p]] = std::max<int>(o.level_maxl[lev[p]], (int)(s.diag[p] - s.rowptr[p]));
   }
 
-  // ---- factor stream: per row b_p, then per slot: assembled value (unless
-  // fill), the Crout updates' U operands (with the L position), and for an
-  // L slot the pivot inverse and y of its column
+  // ---- factor stream: per block row b_p, then per slot: assembled block
+  // (unless fill), the Crout updates' U blocks (with the L position), and for
+  // an L slot the pivot-block inverse and y of its column
   o.stream.clear();
   auto gw = [&](int64_t gidx, int lpos) {
     o.stream.push_back((uint32_t)gidx | ((uint32_t)lpos << 22));
   };
   o.slot_info.assign(s.nnz_lu, 0);
-  o.row_slot.assign(nj + 1, 0);
-  o.row_sptr.assign(nj + 1, 0);
-  for (int p = 0; p < nj; ++p) {
+  o.row_slot.assign(nr + 1, 0);
+  o.row_sptr.assign(nr + 1, 0);
+  for (int p = 0; p < nr; ++p) {
     const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
     o.row_slot[p + 1] = (int32_t)r1;
     gw(o.off_yx + p, 0);
@@ -383,17 +376,17 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     }
     o.row_sptr[p + 1] = (int32_t)o.stream.size();
   }
-  // ---- back stream: rows by back level; per row y_p, 1/u_pp, then (u_pc, x_c)
-  std::vector<int32_t> border(nj);
-  for (int p = 0; p < nj; ++p) border[p] = p;
+  // ---- back stream: rows by back level; per row y_p, inv(U_pp), then (U_pc, x_c)
+  std::vector<int32_t> border(nr);
+  for (int p = 0; p < nr; ++p) border[p] = p;
   std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
     return blev[a] != blev[b] ? blev[a] < blev[b] : a > b;
   });
-  o.brow.resize(nj);
-  o.brow_sptr.assign(nj + 1, 0);
+  o.brow.resize(nr);
+  o.brow_sptr.assign(nr + 1, 0);
   o.blevel_ptr.assign(o.n_blevels + 1, 0);
   o.brow_sptr[0] = (int32_t)o.stream.size();
-  for (int r = 0; r < nj; ++r) {
+  for (int r = 0; r < nr; ++r) {
     const int p = border[r];
     const int64_t cnt = s.rowptr[p + 1] - s.diag[p] - 1;
     if (p >= (1 << 20) || cnt >= 2048) throw std::length_error("back row too large");

@@ -25,30 +25,38 @@ struct NrSymbolic {
   std::vector<int32_t> pair_l, pair_u;
 };
 
-// Level-synchronous Crout schedule (see nr_kernel.cu).
-// Arena: one contiguous block of elements per scenario group; element e of
-// scenario l lives at arena[e * kGroup + l].
+// Level-synchronous 2x2-block Crout schedule (see nr_kernel.cu).
+//
+// Unknowns are grouped per non-slack bus into 2x2 blocks [theta_i, V_i]
+// (PV buses carry a padded V_i with the identity equation dV_i = 0), so the
+// Jacobian is a block matrix with the Ybus pattern. The symbolic analysis
+// (NrSymbolic) is run on that bus graph; its rows/slots are block rows/slots.
+//
+// Arena per scenario group: a block region of 4*kGroup-double elements
+// (LU blocks, pivot-block inverses, y/x 2-vectors padded to 4) followed by a
+// scalar region of kGroup-double elements (per-bus phasors, state, specs).
 struct NrSchedule {
-  int64_t off_lu = 0, off_invd = 0, off_yx = 0, off_u = 0, off_e = 0, off_i = 0, off_spec = 0,
-          off_th = 0, off_vm = 0, n_elem = 0;
-  int max_l = 0;     // longest L part of any row
+  int64_t off_lu = 0, off_invd = 0, off_yx = 0, n_block = 0;          // block region
+  int64_t off_u = 0, off_e = 0, off_spec = 0, off_th = 0, off_vm = 0, n_scalar = 0;
+  int max_l = 0;     // longest L part (blocks) of any row
   int n_levels = 0;  // factor levels (etree height)
   int n_blevels = 0; // back-substitution levels
-  // per-bus Jacobian assembly lists: entries asm_ptr[i]..asm_ptr[i+1]
+  // per-bus assembly lists: entries asm_ptr[i]..asm_ptr[i+1]
   std::vector<int32_t> asm_ptr;
   std::vector<double> asm_y;      // [entries][2] Ybus value (0 for a missing diagonal)
   std::vector<int32_t> asm_j;     // [entries] column bus
-  std::vector<int32_t> asm_slot;  // [entries][4] LU slot of H, N, M, L (or -1)
+  std::vector<int32_t> asm_slot;  // [entries] LU block slot (-1: slack column)
+  std::vector<int32_t> bus_row;   // [n_bus] block row of the bus (-1 slack)
   // factor: rows are level-sorted; level l = rows level_ptr[l]..level_ptr[l+1]
   std::vector<int32_t> level_ptr, level_maxl;
   std::vector<uint32_t> slot_info;  // [nnz_lu] flags | cnt << 16
-  std::vector<int32_t> row_slot;    // [n_j+1] = LU rowptr
-  std::vector<int32_t> row_sptr;    // [n_j+1] factor-row stream ranges
+  std::vector<int32_t> row_slot;    // [n_rows+1] = LU rowptr
+  std::vector<int32_t> row_sptr;    // [n_rows+1] factor-row stream ranges
   // back substitution: rows in back order brow[r] = p | cnt << 20, grouped by
   // back level blevel_ptr; stream ranges brow_sptr (indexed by back position)
   std::vector<uint32_t> brow;
   std::vector<int32_t> blevel_ptr, brow_sptr;
-  // gather stream, word = element index | lpos << 22
+  // gather stream, word = block element index | lpos << 22
   std::vector<uint32_t> stream;
   int64_t n_stream = 0;
 };
@@ -57,6 +65,7 @@ constexpr uint32_t kSlotDiag = 1u << 5;
 constexpr uint32_t kSlotL = 1u << 8;
 constexpr uint32_t kSlotFill = 1u << 9;
 
+// s: NrSymbolic built on the non-slack buses (n_theta = #non-slack, n_q = 0)
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
                        const double* y_re, const double* y_im, NrSchedule& out);
 

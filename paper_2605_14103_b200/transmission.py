@@ -156,48 +156,31 @@ def base_scenario(net: TransmissionNetwork, part: BusPartition) -> TransmissionS
     return TransmissionScenario(p[part.theta_block], q[part.q_block])
 
 
-def jacobian_pattern(model: TransmissionModel):
-    """Structural Jacobian pattern (packed unknowns) as a scipy CSR of ones."""
+def bus_pattern(model: TransmissionModel):
+    """Pattern of the 2x2-block Jacobian: the Ybus pattern over the non-slack
+    buses (theta-block order) plus the diagonal."""
     import scipy.sparse as sp
-    part = model.part
-    n = model.net.n
-    tpos = np.full(n, -1)
-    qpos = np.full(n, -1)
-    tpos[part.theta_block] = np.arange(part.n_theta)
-    qpos[part.q_block] = part.n_theta + np.arange(part.n_q)
-    y = model.y.csr.tocoo()
-    rows = np.r_[y.row, np.arange(n)]
-    cols = np.r_[y.col, np.arange(n)]
-    rr, cc = [], []
-    for a in (tpos, qpos):
-        for b in (tpos, qpos):
-            m = (a[rows] >= 0) & (b[cols] >= 0)
-            rr.append(a[rows][m])
-            cc.append(b[cols][m])
-    nj = part.n_theta + part.n_q
-    j = sp.coo_matrix((np.ones(sum(map(len, rr))), (np.concatenate(rr), np.concatenate(cc))),
-                      shape=(nj, nj)).tocsc()
-    j.sum_duplicates()
-    return j
+    tb = model.part.theta_block
+    y = model.y.csr[tb][:, tb].tocsc()
+    j = (abs(y) > 0).astype(np.float64) + sp.identity(tb.size, format="csc")
+    j.data[:] = 1.0
+    return j.tocsc()
 
 
 def jacobian_ordering(model: TransmissionModel) -> np.ndarray:
-    """MMD(A^T + A) column ordering from SuperLU (host, once per network).
+    """MMD(A^T + A) ordering of the non-slack bus graph (host, once).
 
-    This is the ordering the survey pinned the structure constants to
-    (74,280 LU slots for gb2224). Only the permutation is
-    taken from SuperLU; the factorisation runs on the device.
+    The engine factors the Jacobian as a matrix of 2x2 bus blocks
+    [theta_i, V_i], so the fill-reducing ordering is computed on buses. Only
+    the permutation is taken from SuperLU; the factorisation runs on the
+    device. perm[k] = theta-block position of the bus eliminated k-th.
     """
     import scipy.sparse as sp
     import scipy.sparse.linalg as spl
-    j = jacobian_pattern(model)
-    # a diagonally dominant matrix of the same pattern keeps SuperLU from pivoting
-    j = j.copy()
-    j.data[:] = 1.0
+    j = bus_pattern(model)
     j = j + j.shape[0] * 4.0 * sp.identity(j.shape[0], format="csc")
     lu = spl.splu(j.tocsc(), permc_spec="MMD_AT_PLUS_A", diag_pivot_thresh=0.0,
                   options={"SymmetricMode": True})
-    # perm_c[i] = position of column i  -> order[k] = column at position k
     order = np.empty_like(lu.perm_c)
     order[lu.perm_c] = np.arange(lu.perm_c.size)
     return order.astype(np.int32)

@@ -117,3 +117,32 @@ def test_zbus_batch_position_independent(zb_models, golden):
     b = engine.zbus_solve_arrays(model, sw[perm], sd[perm], 1e-9, 100)
     np.testing.assert_array_equal(a["v"][perm], b["v"])
     np.testing.assert_array_equal(a["iterations"][perm], b["iterations"])
+
+
+def test_nr_large_batch_consistent(tx_models, golden):
+    """A large batch (many groups per level launch, long pipelines) gives the
+    reference iteration count everywhere and the same bits as a small batch."""
+    g = golden("nr_gb2224")
+    model = tx_models["gb2224"]
+    base = pf.transmission_base(model.net, model.part)
+    p, q = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=2048, seed=10010))
+    out = model.plan().solve(p, q, 1e-8, 20)
+    assert out["converged"].all() and (out["iterations"] == 4).all()
+    np.testing.assert_array_equal(p[:8], g["p_spec"])
+    small = model.plan().solve(np.ascontiguousarray(p[:8]), np.ascontiguousarray(q[:8]), 1e-8, 20)
+    np.testing.assert_array_equal(small["theta"], out["theta"][:8])
+    np.testing.assert_array_equal(small["vmag"], out["vmag"][:8])
+    assert np.abs(out["vmag"][:8] - g["vmag"]).max() <= TOL_V
+
+
+def test_zbus_large_batch_consistent(zb_models, golden):
+    g = golden("zb_eulv")
+    model = zb_models["eulv"]
+    base = pf.distribution_base(model)
+    sw, sd = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=4096, seed=10011,
+                                                           target="distribution"))
+    out = engine.zbus_solve_arrays(model, sw, sd, 1e-9, 100)
+    np.testing.assert_array_equal(out["iterations"][:64], g["iterations"])
+    assert out["converged"].all() and (out["residual_inf"] <= 1e-6).all()
+    small = engine.zbus_solve_arrays(model, sw[:8], sd[:8], 1e-9, 100)
+    np.testing.assert_array_equal(small["v"], out["v"][:8])
