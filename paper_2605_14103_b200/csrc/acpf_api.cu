@@ -173,7 +173,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     build_nr_symbolic(first, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, perm);
     const std::vector<int32_t> lperm = level_sorted_perm(first);
     build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, lperm.data());
-    build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch);
+    build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch,
+                      (int)env_int("ACPF_NR_TASK_ELEMS", 512));
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;
@@ -213,9 +214,9 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.off_spec = sc.off_spec;
   d.off_th = sc.off_th;
   d.off_vm = sc.off_vm;
-  p->hs.level_ptr = sc.level_ptr.data();
+  p->hs.level_task_ptr = sc.level_task_ptr.data();
   p->hs.level_maxl = sc.level_maxl.data();
-  p->hs.blevel_ptr = sc.blevel_ptr.data();
+  p->hs.blevel_task_ptr = sc.blevel_task_ptr.data();
   p->hs.n_levels = sc.n_levels;
   p->hs.n_blevels = sc.n_blevels;
   p->hs.max_l = sc.max_l;
@@ -239,6 +240,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
   up(const_cast<int32_t**>(&d.row_slot), sc.row_slot.data(), sc.row_slot.size());
   up(const_cast<int32_t**>(&d.row_sptr), sc.row_sptr.data(), sc.row_sptr.size());
+  up(const_cast<int32_t**>(&d.task_row), sc.task_row.data(), sc.task_row.size());
+  up(const_cast<int32_t**>(&d.btask_row), sc.btask_row.data(), sc.btask_row.size());
   up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
   up(const_cast<int32_t**>(&d.brow_sptr), sc.brow_sptr.data(), sc.brow_sptr.size());
   up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());

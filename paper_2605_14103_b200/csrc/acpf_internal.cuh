@@ -34,6 +34,8 @@ struct NrDeviceModel {
   const int32_t* asm_slot;    // [entries] LU block slot (-1 slack column)
   const uint32_t* slot_info;  // [nnz_lu]
   const int32_t* row_slot;    // [n_rows+1]
+  const int32_t* task_row;    // [n_tasks+1] factor warp tasks (row ranges)
+  const int32_t* btask_row;   // [n_btasks+1] back warp tasks (back-order row ranges)
   const int32_t* row_sptr;    // [n_rows+1]
   const uint32_t* brow;       // [n_rows]
   const int32_t* brow_sptr;   // [n_rows+1]
@@ -45,9 +47,9 @@ struct NrDeviceModel {
 };
 
 struct NrHostSchedule {
-  const int32_t* level_ptr;   // [n_levels+1]
-  const int32_t* level_maxl;  // [n_levels]
-  const int32_t* blevel_ptr;  // [n_blevels+1]
+  const int32_t* level_task_ptr;   // [n_levels+1]
+  const int32_t* level_maxl;       // [n_levels]
+  const int32_t* blevel_task_ptr;  // [n_blevels+1]
   int n_levels, n_blevels, max_l;
 };
 

@@ -356,135 +356,139 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
   }
 }
 
-// One elimination level: task = (block row of the level, group).
+// One elimination level: task = (run of block rows of the level, group).
 // Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every block of scenario sc.
-__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int r0) {
+__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
-  const int p = r0 + (int)(task / w.groups);
+  const int tk = task0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
   const GroupBase gb = group_base(m, w, g, sc);
   const uint32_t ring = su32(smem);
   const uint32_t wring = ring + kRing * kBlkBytes;
   const uint32_t lbuf = wring + kRing * 4;
-  // lbuf entry (i, k) of L block at row position pos, scenario sc
+  // lbuf entry `ent` of the L block at row position pos, scenario sc
   auto lb = [&](int pos, int ent) { return lbuf + pos * kBlkBytes + (ent * kGroup + sc) * 8; };
+  const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
   Pipe pp;
   pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
   pp.ring = ring;
   pp.wring = wring;
   pp.lane = lane;
-  pp.begin(m.stream, m.row_sptr[p], m.row_sptr[p + 1]);
-  const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
-  pp.ensure(0);
-  double yacc = lds_f64(pp.addr(0, bi, sc));  // b_p[i]
-  pp.q = 1;
+  pp.begin(m.stream, m.row_sptr[p0], m.row_sptr[p1]);
   bool zero = false;
-  uint32_t winfo = 0;
-  for (int t = t0; t < t1; ++t) {
-    const int jj = (t - t0) & 31;
-    if (jj == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
-    const uint32_t info = __shfl_sync(kFull, winfo, jj);
-    const int cnt = (int)(info >> 16);
-    double a = 0.0, a2 = 0.0;
-    if (!(info & kSlotFill)) {
-      pp.ensure(pp.q);
-      a = lds_f64(pp.addr(pp.q, r, sc));
-      ++pp.q;
-    }
-    // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j)
-    for (int q = 0; q < cnt;) {
-      pp.ensure(pp.q);
-      const int nb = min(cnt - q, pp.ready_upto - pp.q);
+  for (int p = p0; p < p1; ++p) {
+    const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
+    pp.ensure(pp.q);
+    double yacc = lds_f64(pp.addr(pp.q, bi, sc));  // b_p[i]
+    ++pp.q;
+    uint32_t winfo = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int jj = (t - t0) & 31;
+      if (jj == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
+      const uint32_t info = __shfl_sync(kFull, winfo, jj);
+      const int cnt = (int)(info >> 16);
+      double a = 0.0, a2 = 0.0;
+      if (!(info & kSlotFill)) {
+        pp.ensure(pp.q);
+        a = lds_f64(pp.addr(pp.q, r, sc));
+        ++pp.q;
+      }
+      // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j)
+      for (int q = 0; q < cnt;) {
+        pp.ensure(pp.q);
+        const int nb = min(cnt - q, pp.ready_upto - pp.q);
 #pragma unroll 2
-      for (int k = 0; k < nb; ++k) {
-        const int e = pp.q + k;
-        const int pos = (int)(pp.word(e) >> 22);
-        a = fma(-lds_f64(lb(pos, 2 * bi)), lds_f64(pp.addr(e, bj, sc)), a);
-        a2 = fma(-lds_f64(lb(pos, 2 * bi + 1)), lds_f64(pp.addr(e, 2 + bj, sc)), a2);
+        for (int k = 0; k < nb; ++k) {
+          const int e = pp.q + k;
+          const int pos = (int)(pp.word(e) >> 22);
+          a = fma(-lds_f64(lb(pos, 2 * bi)), lds_f64(pp.addr(e, bj, sc)), a);
+          a2 = fma(-lds_f64(lb(pos, 2 * bi + 1)), lds_f64(pp.addr(e, 2 + bj, sc)), a2);
+        }
+        pp.q += nb;
+        q += nb;
       }
-      pp.q += nb;
-      q += nb;
-    }
-    a = a + a2;
-    if (info & kSlotL) {
-      pp.ensure(pp.q + 1);
-      const int e = pp.q;
-      // L_pt = A' inv(U_tt); y_p -= L_pt y_t
-      const double o = __shfl_xor_sync(kFull, a, 8);  // entry (i, 1-j)
-      const double ai0 = bj ? o : a, ai1 = bj ? a : o;
-      const double l = ai0 * lds_f64(pp.addr(e, bj, sc)) + ai1 * lds_f64(pp.addr(e, 2 + bj, sc));
-      sts_f64(lb(t - t0, r), l);
-      const double lo = __shfl_xor_sync(kFull, l, 8);
-      const double li0 = bj ? lo : l, li1 = bj ? l : lo;
-      yacc = fma(-li1, lds_f64(pp.addr(e + 1, 1, sc)), fma(-li0, lds_f64(pp.addr(e + 1, 0, sc)), yacc));
-      pp.q += 2;
-    } else {
-      if (info & kSlotDiag) {
-        const double a00 = __shfl_sync(kFull, a, sc), a01 = __shfl_sync(kFull, a, 8 + sc);
-        const double a10 = __shfl_sync(kFull, a, 16 + sc), a11 = __shfl_sync(kFull, a, 24 + sc);
-        const double det = a00 * a11 - a01 * a10;
-        zero |= det == 0.0;
-        const double rd = 1.0 / det;
-        const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
-        BL(gb.b, m.off_invd + p, r) = inv;
+      a = a + a2;
+      if (info & kSlotL) {
+        pp.ensure(pp.q + 1);
+        const int e = pp.q;
+        // L_pt = A' inv(U_tt); y_p -= L_pt y_t
+        const double o = __shfl_xor_sync(kFull, a, 8);  // entry (i, 1-j)
+        const double ai0 = bj ? o : a, ai1 = bj ? a : o;
+        const double l = ai0 * lds_f64(pp.addr(e, bj, sc)) + ai1 * lds_f64(pp.addr(e, 2 + bj, sc));
+        sts_f64(lb(t - t0, r), l);
+        const double lo = __shfl_xor_sync(kFull, l, 8);
+        const double li0 = bj ? lo : l, li1 = bj ? l : lo;
+        yacc = fma(-li1, lds_f64(pp.addr(e + 1, 1, sc)), fma(-li0, lds_f64(pp.addr(e + 1, 0, sc)), yacc));
+        pp.q += 2;
+      } else {
+        if (info & kSlotDiag) {
+          const double a00 = __shfl_sync(kFull, a, sc), a01 = __shfl_sync(kFull, a, 8 + sc);
+          const double a10 = __shfl_sync(kFull, a, 16 + sc), a11 = __shfl_sync(kFull, a, 24 + sc);
+          const double det = a00 * a11 - a01 * a10;
+          zero |= det == 0.0;
+          const double rd = 1.0 / det;
+          const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
+          BL(gb.b, m.off_invd + p, r) = inv;
+        }
+        BL(gb.b, m.off_lu + t, r) = a;
       }
-      BL(gb.b, m.off_lu + t, r) = a;
     }
+    if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
+    __syncwarp();  // lbuf of this row complete before the next row of the task reuses it
   }
-  if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
   pp.finish();
   if (zero && r == 0) atomicOr(&w.flags[g * kGroup + sc], 8);
 }
 
-// One back-substitution level: task = (block row of the level, group).
-__global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int b0) {
+// One back-substitution level: task = (run of back rows of the level, group).
+__global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int task0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
   const int64_t g = task % w.groups;
-  const int rr = b0 + (int)(task / w.groups);
+  const int tk = task0 + (int)(task / w.groups);
   if (!w.gactive[g]) return;
   const GroupBase gb = group_base(m, w, g, sc);
   const uint32_t ring = su32(smem);
+  const int r0 = m.btask_row[tk], r1 = m.btask_row[tk + 1];
   Pipe pp;
   pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
   pp.ring = ring;
   pp.wring = ring + kRing * kBlkBytes;
   pp.lane = lane;
-  pp.begin(m.stream, m.brow_sptr[rr], m.brow_sptr[rr + 1]);
-  const uint32_t b = m.brow[rr];
-  const int p = (int)(b & 0xfffffu);
-  const int cnt = (int)(b >> 20);
-  pp.ensure(1);
-  const double yi = lds_f64(pp.addr(0, bi, sc));
-  const double inv0 = lds_f64(pp.addr(1, 2 * bi, sc)), inv1 = lds_f64(pp.addr(1, 2 * bi + 1, sc));
-  pp.q = 2;
-  double part = 0.0;  // sum_c U_pc[i][j] x_c[j]
-  for (int q = 0; q < cnt;) {
+  pp.begin(m.stream, m.brow_sptr[r0], m.brow_sptr[r1]);
+  for (int rr = r0; rr < r1; ++rr) {
+    const uint32_t b = m.brow[rr];
+    const int p = (int)(b & 0xfffffu);
+    const int cnt = (int)(b >> 20);
     pp.ensure(pp.q + 1);
-    const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
-    if (nb == 0) {  // a (U, x) pair straddles the ready range
+    const double yi = lds_f64(pp.addr(pp.q, bi, sc));
+    const double inv0 = lds_f64(pp.addr(pp.q + 1, 2 * bi, sc));
+    const double inv1 = lds_f64(pp.addr(pp.q + 1, 2 * bi + 1, sc));
+    pp.q += 2;
+    double part = 0.0;  // sum_c U_pc[i][j] x_c[j]
+    for (int q = 0; q < cnt;) {
       pp.ensure(pp.q + 1);
-      continue;
+      const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
+      for (int k = 0; k < nb; ++k) {
+        const int e = pp.q + 2 * k;
+        part = fma(lds_f64(pp.addr(e, r, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
+      }
+      pp.q += 2 * nb;
+      q += nb;
     }
-    for (int k = 0; k < nb; ++k) {
-      const int e = pp.q + 2 * k;
-      part = fma(lds_f64(pp.addr(e, r, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
-    }
-    pp.q += 2 * nb;
-    q += nb;
+    const double po = __shfl_xor_sync(kFull, part, 8);
+    const double acc = yi - (bj ? po + part : part + po);  // (y_p - sum)[i]
+    const double ao = __shfl_xor_sync(kFull, acc, 16);     // the other row
+    const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
+    const double x = inv0 * acc0 + inv1 * acc1;            // x_p[i]
+    if (bj == 0) BL(gb.b, m.off_yx + p, bi) = x;
   }
-  const double po = __shfl_xor_sync(kFull, part, 8);
-  const double acc = yi - (bj ? po + part : part + po);        // (y_p - sum)[i]
-  const double ao = __shfl_xor_sync(kFull, acc, 16);           // the other row
-  const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
-  const double x = inv0 * acc0 + inv1 * acc1;                  // x_p[i]
-  if (bj == 0) BL(gb.b, m.off_yx + p, bi) = x;
   pp.finish();
 }
 
@@ -577,12 +581,12 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
     for (int l = 0; l < hs.n_levels; ++l) {
-      const int r0 = hs.level_ptr[l], nr = hs.level_ptr[l + 1] - r0;
-      nr_factor_kernel<<<(unsigned)(groups * nr), 32, nr_smem_bytes(hs.level_maxl[l]), stream>>>(m, w, r0);
+      const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
+      nr_factor_kernel<<<(unsigned)(groups * nt), 32, nr_smem_bytes(hs.level_maxl[l]), stream>>>(m, w, k0);
     }
     for (int l = 0; l < hs.n_blevels; ++l) {
-      const int b0 = hs.blevel_ptr[l], nr = hs.blevel_ptr[l + 1] - b0;
-      nr_back_kernel<<<(unsigned)(groups * nr), 32, pipe_smem(), stream>>>(m, w, b0);
+      const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
+      nr_back_kernel<<<(unsigned)(groups * nt), 32, pipe_smem(), stream>>>(m, w, k0);
     }
     nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
     nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);

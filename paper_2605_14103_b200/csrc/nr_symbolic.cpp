@@ -266,7 +266,7 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
 }
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
-                       const double* y_re, const double* y_im, NrSchedule& o) {
+                       const double* y_re, const double* y_im, NrSchedule& o, int task_elems) {
   const int nr = s.n_j, nb = s.n_bus;
   if (s.n_q != 0) throw std::logic_error("block schedule expects a bus-level symbolic analysis");
   // ---- arena layout
@@ -402,6 +402,30 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   }
   o.n_stream = (int64_t)o.stream.size();
   if (o.n_stream >= INT32_MAX) throw std::length_error("stream too long");
+
+  // ---- warp tasks: greedy runs of consecutive rows of one level with about
+  // task_elems stream elements (a long row is a task on its own)
+  auto make_tasks = [&](const std::vector<int32_t>& lptr, const std::vector<int32_t>& sptr,
+                        std::vector<int32_t>& tptr, std::vector<int32_t>& trow) {
+    const int nl = (int)lptr.size() - 1;
+    tptr.assign(nl + 1, 0);
+    trow.clear();
+    for (int l = 0; l < nl; ++l) {
+      int r = lptr[l];
+      while (r < lptr[l + 1]) {
+        trow.push_back(r);
+        int64_t acc = 0;
+        do {
+          acc += sptr[r + 1] - sptr[r];
+          ++r;
+        } while (r < lptr[l + 1] && acc + (sptr[r + 1] - sptr[r]) <= task_elems);
+      }
+      tptr[l + 1] = (int32_t)trow.size();
+    }
+    trow.push_back(lptr[nl]);
+  };
+  make_tasks(o.level_ptr, o.row_sptr, o.level_task_ptr, o.task_row);
+  make_tasks(o.blevel_ptr, o.brow_sptr, o.blevel_task_ptr, o.btask_row);
 }
 
 }  // namespace acpf

@@ -49,6 +49,10 @@ struct NrSchedule {
   std::vector<int32_t> bus_row;   // [n_bus] block row of the bus (-1 slack)
   // factor: rows are level-sorted; level l = rows level_ptr[l]..level_ptr[l+1]
   std::vector<int32_t> level_ptr, level_maxl;
+  // warp tasks: consecutive rows of one level whose streams are processed by
+  // one pipeline; tasks of level l are level_task_ptr[l]..level_task_ptr[l+1],
+  // task k covers rows task_row[k]..task_row[k+1]
+  std::vector<int32_t> level_task_ptr, task_row;
   std::vector<uint32_t> slot_info;  // [nnz_lu] flags | cnt << 16
   std::vector<int32_t> row_slot;    // [n_rows+1] = LU rowptr
   std::vector<int32_t> row_sptr;    // [n_rows+1] factor-row stream ranges
@@ -56,6 +60,7 @@ struct NrSchedule {
   // back level blevel_ptr; stream ranges brow_sptr (indexed by back position)
   std::vector<uint32_t> brow;
   std::vector<int32_t> blevel_ptr, brow_sptr;
+  std::vector<int32_t> blevel_task_ptr, btask_row;  // same for back rows (back order)
   // gather stream, word = block element index | lpos << 22
   std::vector<uint32_t> stream;
   int64_t n_stream = 0;
@@ -67,7 +72,8 @@ constexpr uint32_t kSlotFill = 1u << 9;
 
 // s: NrSymbolic built on the non-slack buses (n_theta = #non-slack, n_q = 0)
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
-                       const double* y_re, const double* y_im, NrSchedule& out);
+                       const double* y_re, const double* y_im, NrSchedule& out,
+                       int task_elems = 512);
 
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
