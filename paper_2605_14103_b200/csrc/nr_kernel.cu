@@ -169,6 +169,8 @@ struct Pipe {
 
   __device__ __forceinline__ uint32_t word(int e) const { return lds_u32(wring + (e % kRing) * 4); }
 
+  __device__ __forceinline__ uint32_t slot_base(int e) const { return ring + (e % kRing) * kBlkBytes; }
+
   __device__ __forceinline__ void finish() {
     cp_wait<0>();
     __syncwarp();
@@ -372,6 +374,9 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   const uint32_t lbuf = wring + kRing * 4;
   // lbuf entry `ent` of the L block at row position pos, scenario sc
   auto lb = [&](int pos, int ent) { return lbuf + pos * kBlkBytes + (ent * kGroup + sc) * 8; };
+  // per-lane byte offsets inside a block element: L[i][0], L[i][1], U[0][j], U[1][j]
+  const uint32_t offL0 = ((2 * bi) * kGroup + sc) * 8, offL1 = offL0 + kGroup * 8;
+  const uint32_t offU0 = (bj * kGroup + sc) * 8, offU1 = offU0 + 2 * kGroup * 8;
   const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
   Pipe pp;
   pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
@@ -397,21 +402,34 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         a = lds_f64(pp.addr(pp.q, r, sc));
         ++pp.q;
       }
-      // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j)
+      // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j); two
+      // interleaved accumulator pairs keep four independent FMA chains
+      double a3 = 0.0, a4 = 0.0;
       for (int q = 0; q < cnt;) {
         pp.ensure(pp.q);
         const int nb = min(cnt - q, pp.ready_upto - pp.q);
-#pragma unroll 2
-        for (int k = 0; k < nb; ++k) {
+        int k = 0;
+        for (; k + 1 < nb; k += 2) {
           const int e = pp.q + k;
-          const int pos = (int)(pp.word(e) >> 22);
-          a = fma(-lds_f64(lb(pos, 2 * bi)), lds_f64(pp.addr(e, bj, sc)), a);
-          a2 = fma(-lds_f64(lb(pos, 2 * bi + 1)), lds_f64(pp.addr(e, 2 + bj, sc)), a2);
+          const uint32_t w0 = pp.word(e), w1 = pp.word(e + 1);
+          const uint32_t l0 = lbuf + (w0 >> 22) * kBlkBytes, l1 = lbuf + (w1 >> 22) * kBlkBytes;
+          const uint32_t u0 = pp.slot_base(e), u1 = pp.slot_base(e + 1);
+          a = fma(-lds_f64(l0 + offL0), lds_f64(u0 + offU0), a);
+          a2 = fma(-lds_f64(l0 + offL1), lds_f64(u0 + offU1), a2);
+          a3 = fma(-lds_f64(l1 + offL0), lds_f64(u1 + offU0), a3);
+          a4 = fma(-lds_f64(l1 + offL1), lds_f64(u1 + offU1), a4);
+        }
+        if (k < nb) {
+          const int e = pp.q + k;
+          const uint32_t l0 = lbuf + (pp.word(e) >> 22) * kBlkBytes;
+          const uint32_t u0 = pp.slot_base(e);
+          a = fma(-lds_f64(l0 + offL0), lds_f64(u0 + offU0), a);
+          a2 = fma(-lds_f64(l0 + offL1), lds_f64(u0 + offU1), a2);
         }
         pp.q += nb;
         q += nb;
       }
-      a = a + a2;
+      a = (a + a3) + (a2 + a4);
       if (info & kSlotL) {
         pp.ensure(pp.q + 1);
         const int e = pp.q;
