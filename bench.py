@@ -240,20 +240,26 @@ def run_ours(args, rank, local, world):
     n_conv_all = shard.sum_over_ranks(conv, dev)
     info = plan.info
     value = n_conv_all * args.steps / t
-    kern_s = launches[1] / 1e3 / max(1, launches[0])  # avg launch duration
-    per_launch_scen = args.nr_batch / max(1, launches[0] / args.steps)
-    alg_bytes = float(roofline.nr_bytes_per_scenario(its, info["n_bus"], info["n_j"],
-                                                     info["nnz_lu"]).mean()) * per_launch_scen
+    # roofline unit = one batched solve: a launch sequence (phasor, mismatch,
+    # check, one factor launch per elimination level, one back launch per
+    # level, update) dominated by nr_factor_kernel; its device time comes
+    # from CUDA events on the solve stream (acpf_nr_last_timing)
+    solve_s = launches[1] / 1e3 / args.steps
+    alg_bytes = float(roofline.nr_bytes_per_scenario(its, model.net.n,
+                                                     model.part.n_theta + model.part.n_q,
+                                                     info["nnz_lu"]).sum())
     hbm, hbm_src = peaks.hbm_gbs()
-    achieved = alg_bytes / kern_s / 1e9
-    traffic = traffic_from_profiles("nr_stream_kernel", args.nr_batch)
+    achieved = alg_bytes / solve_s / 1e9
+    traffic = traffic_from_profiles("nr_solve", args.nr_batch)
     res["nr"] = dict(value=value, t=t, steps=args.steps, launches=launches[0], clocks=clk.summary(),
                      iterations=np.unique(its).tolist(), conv_frac=conv / args.nr_batch,
                      roofline={"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                                "frac": achieved / hbm, "traffic": traffic,
-                               "kernel": "nr_stream_kernel",
+                               "kernel": "nr_factor_kernel (+ back/mismatch launches of one solve)",
                                "algorithmic_bytes_per_launch": alg_bytes,
-                               "avg_launch_ms": kern_s * 1e3, "peak_source": hbm_src})
+                               "launch_unit": "one batched Newton solve "
+                                              f"({launches[0] // max(1, args.steps)} launches)",
+                               "avg_launch_ms": solve_s * 1e3, "peak_source": hbm_src})
     # e2e through the C-ABI with pinned host buffers
     hp, hq = pinned_like(p).numpy(), pinned_like(q).numpy()
     hout = pinned_outputs(plan.alloc_outputs(args.nr_batch))
