@@ -62,6 +62,12 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
@@ -76,8 +82,8 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
 
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -126,11 +132,15 @@ struct Pipe {
       const int jw = e0 - wbase;
       const uint32_t mine = __shfl_sync(kFull, wcur, (jw + lane) & 31);
       if (lane < lim) sts_u32(wring + (slot + lane) * 4, mine);
+      // 16 B per lane: lanes 0-15 copy element j, lanes 16-31 element j+1
+      const int half = lane >> 4, chunk = lane & 15;
 #pragma unroll
-      for (int j = 0; j < kCh; ++j) {
-        const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
-        if (j < lim)
-          cp_async8(ring + (slot + j) * kBlkBytes + lane * 8, blocks + (size_t)(w & 0x3fffffu) * kBlk + lane);
+      for (int j = 0; j < kCh; j += 2) {
+        const int jj = j + half;
+        const uint32_t w = __shfl_sync(kFull, wcur, (jw + jj) & 31);
+        if (jj < lim)
+          cp_async16(ring + (slot + jj) * kBlkBytes + chunk * 16,
+                     blocks + (size_t)(w & 0x3fffffu) * kBlk + chunk * 2);
       }
     }
     cp_commit();
@@ -164,7 +174,7 @@ struct Pipe {
 
   // smem address of entry `ent` (0..3) of element e for scenario sc
   __device__ __forceinline__ uint32_t addr(int e, int ent, int sc) const {
-    return ring + (e % kRing) * kBlkBytes + (ent * kGroup + sc) * 8;
+    return ring + (e % kRing) * kBlkBytes + (sc * 4 + ent) * 8;
   }
 
   __device__ __forceinline__ uint32_t word(int e) const { return lds_u32(wring + (e % kRing) * 4); }
@@ -177,8 +187,10 @@ struct Pipe {
   }
 };
 
-// block-region entry `ent` of block element e, scenario sc (B = group block base + sc)
-#define BL(B, e, ent) (B)[((size_t)(e) * 4 + (ent)) * kGroup]
+// block-region entry `ent` of block element e, scenario sc (B = group block base + 4*sc).
+// Elements are scenario-major (4 consecutive entries per scenario). Matrix
+// blocks are stored column-major: entry (i, j) at 2*j + i.
+#define BL(B, e, ent) (B)[(size_t)(e) * kBlk + (ent)]
 // scalar-region element e, scenario sc (S = group scalar base + sc)
 #define SL(S, e) (S)[(size_t)(e) * kGroup]
 
@@ -190,7 +202,7 @@ struct GroupBase {
 __device__ __forceinline__ GroupBase group_base(const NrDeviceModel& m, const NrWorkspace& w, int64_t g,
                                                 int sc) {
   double* base = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
-  return GroupBase{base + sc, base + m.n_block * kBlk + sc};
+  return GroupBase{base + 4 * sc, base + m.n_block * kBlk + sc};
 }
 
 __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
@@ -305,10 +317,11 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
         dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
       }
       const bool pqj = m.qidx[jb] >= 0;
-      BL(gb.b, m.off_lu + slot, 0) = dth.x;                      // H
-      BL(gb.b, m.off_lu + slot, 1) = pqj ? dv.x : 0.0;           // N
-      BL(gb.b, m.off_lu + slot, 2) = pq ? dth.y : 0.0;           // M
-      BL(gb.b, m.off_lu + slot, 3) = (pq && pqj) ? dv.y : (jb == i && !(pq && pqj) ? 1.0 : 0.0);  // L
+      // column-major [[H, N], [M, L]]: H (0,0)->0, M (1,0)->1, N (0,1)->2, L (1,1)->3
+      BL(gb.b, m.off_lu + slot, 0) = dth.x;
+      BL(gb.b, m.off_lu + slot, 1) = pq ? dth.y : 0.0;
+      BL(gb.b, m.off_lu + slot, 2) = pqj ? dv.x : 0.0;
+      BL(gb.b, m.off_lu + slot, 3) = (pq && pqj) ? dv.y : (jb == i ? 1.0 : 0.0);
     }
   }
   const int64_t s = g * kGroup + sc;
@@ -372,11 +385,12 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   const uint32_t ring = su32(smem);
   const uint32_t wring = ring + kRing * kBlkBytes;
   const uint32_t lbuf = wring + kRing * 4;
-  // lbuf entry `ent` of the L block at row position pos, scenario sc
-  auto lb = [&](int pos, int ent) { return lbuf + pos * kBlkBytes + (ent * kGroup + sc) * 8; };
-  // per-lane byte offsets inside a block element: L[i][0], L[i][1], U[0][j], U[1][j]
-  const uint32_t offL0 = ((2 * bi) * kGroup + sc) * 8, offL1 = offL0 + kGroup * 8;
-  const uint32_t offU0 = (bj * kGroup + sc) * 8, offU1 = offU0 + 2 * kGroup * 8;
+  // lbuf holds the row's L blocks row-major: entry (i, j) of scenario sc at
+  // lbuf + pos*256 + (4*sc + 2*i + j)*8, so L[i][0..1] is one 16-byte load;
+  // U blocks are column-major so U[0..1][j] is one 16-byte load too
+  const uint32_t offL = (4 * sc + 2 * bi) * 8;   // L[i][0], L[i][1]
+  const uint32_t offU = (4 * sc + 2 * bj) * 8;   // U[0][j], U[1][j] (column j)
+  const int ce = 2 * bj + bi;                     // this lane's column-major entry
   const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
   Pipe pp;
   pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
@@ -399,7 +413,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
       double a = 0.0, a2 = 0.0;
       if (!(info & kSlotFill)) {
         pp.ensure(pp.q);
-        a = lds_f64(pp.addr(pp.q, r, sc));
+        a = lds_f64(pp.addr(pp.q, ce, sc));
         ++pp.q;
       }
       // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j); two
@@ -412,19 +426,21 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         for (; k + 1 < nb; k += 2) {
           const int e = pp.q + k;
           const uint32_t w0 = pp.word(e), w1 = pp.word(e + 1);
-          const uint32_t l0 = lbuf + (w0 >> 22) * kBlkBytes, l1 = lbuf + (w1 >> 22) * kBlkBytes;
-          const uint32_t u0 = pp.slot_base(e), u1 = pp.slot_base(e + 1);
-          a = fma(-lds_f64(l0 + offL0), lds_f64(u0 + offU0), a);
-          a2 = fma(-lds_f64(l0 + offL1), lds_f64(u0 + offU1), a2);
-          a3 = fma(-lds_f64(l1 + offL0), lds_f64(u1 + offU0), a3);
-          a4 = fma(-lds_f64(l1 + offL1), lds_f64(u1 + offU1), a4);
+          const double2 l0 = lds_f64x2(lbuf + (w0 >> 22) * kBlkBytes + offL);
+          const double2 l1 = lds_f64x2(lbuf + (w1 >> 22) * kBlkBytes + offL);
+          const double2 u0 = lds_f64x2(pp.slot_base(e) + offU);
+          const double2 u1 = lds_f64x2(pp.slot_base(e + 1) + offU);
+          a = fma(-l0.x, u0.x, a);
+          a2 = fma(-l0.y, u0.y, a2);
+          a3 = fma(-l1.x, u1.x, a3);
+          a4 = fma(-l1.y, u1.y, a4);
         }
         if (k < nb) {
           const int e = pp.q + k;
-          const uint32_t l0 = lbuf + (pp.word(e) >> 22) * kBlkBytes;
-          const uint32_t u0 = pp.slot_base(e);
-          a = fma(-lds_f64(l0 + offL0), lds_f64(u0 + offU0), a);
-          a2 = fma(-lds_f64(l0 + offL1), lds_f64(u0 + offU1), a2);
+          const double2 l0 = lds_f64x2(lbuf + (pp.word(e) >> 22) * kBlkBytes + offL);
+          const double2 u0 = lds_f64x2(pp.slot_base(e) + offU);
+          a = fma(-l0.x, u0.x, a);
+          a2 = fma(-l0.y, u0.y, a2);
         }
         pp.q += nb;
         q += nb;
@@ -436,11 +452,13 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         // L_pt = A' inv(U_tt); y_p -= L_pt y_t
         const double o = __shfl_xor_sync(kFull, a, 8);  // entry (i, 1-j)
         const double ai0 = bj ? o : a, ai1 = bj ? a : o;
-        const double l = ai0 * lds_f64(pp.addr(e, bj, sc)) + ai1 * lds_f64(pp.addr(e, 2 + bj, sc));
-        sts_f64(lb(t - t0, r), l);
+        const double2 iv = lds_f64x2(pp.slot_base(e) + offU);  // inv[0][j], inv[1][j]
+        const double l = ai0 * iv.x + ai1 * iv.y;
+        sts_f64(lbuf + (t - t0) * kBlkBytes + (4 * sc + 2 * bi + bj) * 8, l);
         const double lo = __shfl_xor_sync(kFull, l, 8);
         const double li0 = bj ? lo : l, li1 = bj ? l : lo;
-        yacc = fma(-li1, lds_f64(pp.addr(e + 1, 1, sc)), fma(-li0, lds_f64(pp.addr(e + 1, 0, sc)), yacc));
+        const double2 yt = lds_f64x2(pp.slot_base(e + 1) + 4 * sc * 8);
+        yacc = fma(-li1, yt.y, fma(-li0, yt.x, yacc));
         pp.q += 2;
       } else {
         if (info & kSlotDiag) {
@@ -450,9 +468,9 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
           zero |= det == 0.0;
           const double rd = 1.0 / det;
           const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
-          BL(gb.b, m.off_invd + p, r) = inv;
+          BL(gb.b, m.off_invd + p, ce) = inv;
         }
-        BL(gb.b, m.off_lu + t, r) = a;
+        BL(gb.b, m.off_lu + t, ce) = a;
       }
     }
     if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
@@ -486,8 +504,8 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
     const int cnt = (int)(b >> 20);
     pp.ensure(pp.q + 1);
     const double yi = lds_f64(pp.addr(pp.q, bi, sc));
-    const double inv0 = lds_f64(pp.addr(pp.q + 1, 2 * bi, sc));
-    const double inv1 = lds_f64(pp.addr(pp.q + 1, 2 * bi + 1, sc));
+    const double inv0 = lds_f64(pp.addr(pp.q + 1, bi, sc));
+    const double inv1 = lds_f64(pp.addr(pp.q + 1, 2 + bi, sc));
     pp.q += 2;
     double part = 0.0;  // sum_c U_pc[i][j] x_c[j]
     for (int q = 0; q < cnt;) {
@@ -495,7 +513,7 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
       const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
       for (int k = 0; k < nb; ++k) {
         const int e = pp.q + 2 * k;
-        part = fma(lds_f64(pp.addr(e, r, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
+        part = fma(lds_f64(pp.addr(e, 2 * bj + bi, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
       }
       pp.q += 2 * nb;
       q += nb;
