@@ -181,6 +181,35 @@ acpf_status acpf_zbus_last_timing(acpf_zbus_plan_t plan, double* kernel_ms, int3
 
 acpf_status acpf_zbus_plan_destroy(acpf_zbus_plan_t plan);
 
+/* ------------------------------------------------------------------------
+ * Seeded scenario inputs generated on the device (bitwise the reference
+ * generator, batch.py:45-60 Philox4x64-10 keyed (seed, i), and its load
+ * scaling batch.py:121-151). Rows start..start+count-1 of the batch.
+ * ------------------------------------------------------------------------ */
+
+/* Multiplier table [count][n_elem] (generate_load_multipliers). */
+acpf_status acpf_philox_multipliers(uint64_t seed, int64_t start, int64_t count, int32_t n_elem,
+                                    double spread, double* out, uint32_t flags, void* cuda_stream);
+
+/* Transmission scenarios for a plan: element_bus [n_elem] = buses with a
+ * nonzero base load (transmission_base.load_elements); p_load, q_load,
+ * p_gen, q_gen [n_bus] host arrays (per unit). Writes p_spec [count][n_theta]
+ * and q_spec [count][n_q] (host or device per flags). */
+acpf_status acpf_nr_scenarios(acpf_nr_plan_t plan, uint64_t seed, int64_t start, int64_t count,
+                              double spread, int32_t n_elem, const int32_t* element_bus,
+                              const double* p_load, const double* q_load, const double* p_gen,
+                              const double* q_gen, double* p_spec, double* q_spec, uint32_t flags,
+                              void* cuda_stream);
+
+/* Distribution scenarios: multiplier k scales wye load elem_target[k] (>= 0)
+ * or delta load -elem_target[k]-1 (the reference load order); wye_s, delta_s
+ * host base powers (interleaved complex). Writes s_wye [count][n_wye] and
+ * s_delta [count][n_delta] complex. */
+acpf_status acpf_zbus_scenarios(acpf_zbus_plan_t plan, uint64_t seed, int64_t start, int64_t count,
+                                double spread, int32_t n_elem, const int32_t* elem_target,
+                                const double* wye_s, const double* delta_s, double* s_wye,
+                                double* s_delta, uint32_t flags, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,7 @@ struct acpf_nr_plan {
   size_t stage_bytes = 0;
   void* stage_base = nullptr;
   int* host_active = nullptr;
+  std::vector<int32_t> h_tpos, h_qidx;  // host copies for scenario generation
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
@@ -107,6 +108,7 @@ struct acpf_nr_plan {
 
 struct acpf_zbus_plan {
   int device = 0;
+  int n_wye = 0, n_delta = 0;
   ZbDeviceModel dm{};
   DevArena model;
   DevArena stage;
@@ -198,6 +200,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     qidx[q_block[k]] = k;
   }
 
+  p->h_tpos = tpos;
+  p->h_qidx = qidx;
   NrDeviceModel& d = p->dm;
   d.n_bus = n_bus;
   d.n_theta = n_theta;
@@ -536,6 +540,8 @@ acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const 
   }
   p->device = device;
   DeviceGuard dg(device);
+  p->n_wye = n_wye;
+  p->n_delta = n_delta;
   ZbDeviceModel& d = p->dm;
   d.n = n;
   d.n_l = n_l;
@@ -694,6 +700,163 @@ acpf_status acpf_zbus_plan_destroy(acpf_zbus_plan_t p) {
     p->model.release();
   }
   delete p;
+  return ACPF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Seeded scenario generation
+// ---------------------------------------------------------------------------
+
+namespace {
+// device staging for host-pointer outputs + small per-call uploads
+struct TmpArena {
+  acpf::DevArena a;
+};
+}  // namespace
+
+acpf_status acpf_philox_multipliers(uint64_t seed, int64_t start, int64_t count, int32_t n_elem,
+                                    double spread, double* out, uint32_t flags, void* cuda_stream) {
+  if (start < 0 || count < 0 || n_elem < 0 || !out || !(spread >= 0 && spread < 1) || flags > 1u) {
+    set_error("acpf_philox_multipliers: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (count == 0 || n_elem == 0) return ACPF_OK;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  TmpArena t;
+  double* d = out;
+  const size_t bytes = (size_t)count * n_elem * 8;
+  if (!(flags & ACPF_DEVICE_PTRS)) ACPF_CUDA(t.a.alloc((void**)&d, bytes));
+  ACPF_CUDA(launch_philox_multipliers(seed, start, count, n_elem, spread, d, st));
+  if (!(flags & ACPF_DEVICE_PTRS)) ACPF_CUDA(cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, st));
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_scenarios(acpf_nr_plan_t p, uint64_t seed, int64_t start, int64_t count,
+                              double spread, int32_t n_elem, const int32_t* element_bus,
+                              const double* p_load, const double* q_load, const double* p_gen,
+                              const double* q_gen, double* p_spec, double* q_spec, uint32_t flags,
+                              void* cuda_stream) {
+  if (!p || start < 0 || count < 0 || n_elem < 0 || (n_elem && !element_bus) || !p_load || !q_load ||
+      !p_gen || !q_gen || !(spread >= 0 && spread < 1) || flags > 1u ||
+      (p->dm.n_theta && !p_spec) || (p->dm.n_q && !q_spec)) {
+    set_error("acpf_nr_scenarios: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (count == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int nb = p->dm.n_bus, nt = p->dm.n_theta, nq = p->dm.n_q;
+  std::vector<double> pb(nt), qb(nq);
+  for (int b = 0; b < nb; ++b) {
+    if (p->h_tpos[b] >= 0) pb[p->h_tpos[b]] = p_gen[b] - p_load[b];
+    if (p->h_qidx[b] >= 0) qb[p->h_qidx[b]] = q_gen[b] - q_load[b];
+  }
+  std::vector<int32_t> et(n_elem), eq(n_elem);
+  std::vector<double> epl(n_elem), eql(n_elem), epg(n_elem), eqg(n_elem);
+  for (int e = 0; e < n_elem; ++e) {
+    const int b = element_bus[e];
+    if (b < 0 || b >= nb) {
+      set_error("acpf_nr_scenarios: element bus out of range");
+      return ACPF_EINVAL;
+    }
+    et[e] = p->h_tpos[b];
+    eq[e] = p->h_qidx[b];
+    epl[e] = p_load[b];
+    eql[e] = q_load[b];
+    epg[e] = p_gen[b];
+    eqg[e] = q_gen[b];
+  }
+  TmpArena t;
+  NrScenarioArgs a{};
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = t.a.upload(dst, src, cnt);
+  };
+  up(const_cast<double**>(&a.p_base), pb.data(), pb.size());
+  up(const_cast<double**>(&a.q_base), qb.data(), qb.size());
+  up(const_cast<int32_t**>(&a.elem_tpos), et.data(), et.size());
+  up(const_cast<int32_t**>(&a.elem_qidx), eq.data(), eq.size());
+  up(const_cast<double**>(&a.elem_pl), epl.data(), epl.size());
+  up(const_cast<double**>(&a.elem_ql), eql.data(), eql.size());
+  up(const_cast<double**>(&a.elem_pg), epg.data(), epg.size());
+  up(const_cast<double**>(&a.elem_qg), eqg.data(), eqg.size());
+  ACPF_CUDA(e);
+  a.seed = seed;
+  a.start = start;
+  a.count = count;
+  a.spread = spread;
+  a.n_elem = n_elem;
+  a.n_theta = nt;
+  a.n_q = nq;
+  a.p_spec = p_spec;
+  a.q_spec = q_spec;
+  const bool host = !(flags & ACPF_DEVICE_PTRS);
+  if (host) {
+    ACPF_CUDA(t.a.alloc((void**)&a.p_spec, (size_t)count * nt * 8));
+    ACPF_CUDA(t.a.alloc((void**)&a.q_spec, (size_t)count * nq * 8));
+  }
+  ACPF_CUDA(launch_nr_scenarios(a, st));
+  if (host) {
+    if (nt) ACPF_CUDA(cudaMemcpyAsync(p_spec, a.p_spec, (size_t)count * nt * 8, cudaMemcpyDeviceToHost, st));
+    if (nq) ACPF_CUDA(cudaMemcpyAsync(q_spec, a.q_spec, (size_t)count * nq * 8, cudaMemcpyDeviceToHost, st));
+  }
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_scenarios(acpf_zbus_plan_t p, uint64_t seed, int64_t start, int64_t count,
+                                double spread, int32_t n_elem, const int32_t* elem_target,
+                                const double* wye_s, const double* delta_s, double* s_wye,
+                                double* s_delta, uint32_t flags, void* cuda_stream) {
+  if (!p || start < 0 || count < 0 || n_elem < 0 || (n_elem && !elem_target) ||
+      (p->n_wye && (!wye_s || !s_wye)) || (p->n_delta && (!delta_s || !s_delta)) ||
+      !(spread >= 0 && spread < 1) || flags > 1u || n_elem != p->n_wye + p->n_delta) {
+    set_error("acpf_zbus_scenarios: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (count == 0) return ACPF_OK;
+  for (int k = 0; k < n_elem; ++k) {
+    const int tg = elem_target[k];
+    if ((tg >= 0 && tg >= p->n_wye) || (tg < 0 && -tg - 1 >= p->n_delta)) {
+      set_error("acpf_zbus_scenarios: element target out of range");
+      return ACPF_EINVAL;
+    }
+  }
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  TmpArena t;
+  ZbScenarioArgs a{};
+  cudaError_t e = cudaSuccess;
+  e = t.a.upload(const_cast<int32_t**>(&a.elem_target), elem_target, (size_t)n_elem);
+  if (e == cudaSuccess)
+    e = t.a.upload(const_cast<double2**>(&a.wye_s), reinterpret_cast<const double2*>(wye_s), (size_t)p->n_wye);
+  if (e == cudaSuccess)
+    e = t.a.upload(const_cast<double2**>(&a.delta_s), reinterpret_cast<const double2*>(delta_s),
+                   (size_t)p->n_delta);
+  ACPF_CUDA(e);
+  a.seed = seed;
+  a.start = start;
+  a.count = count;
+  a.spread = spread;
+  a.n_elem = n_elem;
+  a.n_wye = p->n_wye;
+  a.n_delta = p->n_delta;
+  a.s_wye = reinterpret_cast<double2*>(s_wye);
+  a.s_delta = reinterpret_cast<double2*>(s_delta);
+  const bool host = !(flags & ACPF_DEVICE_PTRS);
+  if (host) {
+    ACPF_CUDA(t.a.alloc((void**)&a.s_wye, (size_t)count * p->n_wye * 16));
+    ACPF_CUDA(t.a.alloc((void**)&a.s_delta, (size_t)count * p->n_delta * 16));
+  }
+  ACPF_CUDA(launch_zb_scenarios(a, st));
+  if (host) {
+    if (p->n_wye)
+      ACPF_CUDA(cudaMemcpyAsync(s_wye, a.s_wye, (size_t)count * p->n_wye * 16, cudaMemcpyDeviceToHost, st));
+    if (p->n_delta)
+      ACPF_CUDA(cudaMemcpyAsync(s_delta, a.s_delta, (size_t)count * p->n_delta * 16, cudaMemcpyDeviceToHost, st));
+  }
+  ACPF_CUDA(cudaStreamSynchronize(st));
   return ACPF_OK;
 }
 

@@ -126,4 +126,41 @@ cudaError_t launch_zbus(const ZbDeviceModel& m, const ZbBatchIO& io, double tol,
 size_t zbus_frag_doubles(int n_rb, int kpad);
 void zbus_pack_fragments(const double* zl, int n, int n_l, int n_rb, int kpad, double* out);
 
+// ---------------------------------------------------------------------------
+// Seeded scenario generation (scenario_kernel.cu)
+// ---------------------------------------------------------------------------
+struct NrScenarioArgs {
+  uint64_t seed;
+  int64_t start, count;
+  double spread;
+  int n_elem, n_theta, n_q;
+  const double* p_base;   // [n_theta] p_gen - p_load over the theta block
+  const double* q_base;   // [n_q]
+  const int32_t* elem_tpos;
+  const int32_t* elem_qidx;
+  const double* elem_pl;
+  const double* elem_ql;
+  const double* elem_pg;
+  const double* elem_qg;
+  double* p_spec;  // [count][n_theta]
+  double* q_spec;  // [count][n_q]
+};
+
+struct ZbScenarioArgs {
+  uint64_t seed;
+  int64_t start, count;
+  double spread;
+  int n_elem, n_wye, n_delta;
+  const int32_t* elem_target;  // >= 0 wye index, else -(delta index)-1
+  const double2* wye_s;
+  const double2* delta_s;
+  double2* s_wye;
+  double2* s_delta;
+};
+
+cudaError_t launch_philox_multipliers(uint64_t seed, int64_t start, int64_t count, int n_elem,
+                                      double spread, double* out, cudaStream_t st);
+cudaError_t launch_nr_scenarios(const NrScenarioArgs& a, cudaStream_t st);
+cudaError_t launch_zb_scenarios(const ZbScenarioArgs& a, cudaStream_t st);
+
 }  // namespace acpf

@@ -31,7 +31,8 @@ EXPORTED = (
     "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_plan_info_get", "acpf_nr_plan_structure",
     "acpf_nr_solve", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
-    "acpf_zbus_plan_destroy",
+    "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
+    "acpf_zbus_scenarios",
 )
 
 
@@ -93,6 +94,9 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_zbus_solve": (I32, [P, I64, P, P, D, I32, P, P, P, P, P, P, P, U32, P]),
         "acpf_zbus_last_timing": (I32, [P, P, P]),
         "acpf_zbus_plan_destroy": (I32, [P]),
+        "acpf_philox_multipliers": (I32, [C.c_uint64, I64, I64, I32, D, P, U32, P]),
+        "acpf_nr_scenarios": (I32, [P, C.c_uint64, I64, I64, D, I32, P, P, P, P, P, P, P, U32, P]),
+        "acpf_zbus_scenarios": (I32, [P, C.c_uint64, I64, I64, D, I32, P, P, P, P, P, U32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -155,6 +159,26 @@ def nr_analyze(y_csr, theta_block, q_block, perm=None) -> dict:
     _check(lib.acpf_nr_analyze(y.shape[0], _ptr(rowptr), _ptr(col), tb.size, _ptr(tb), qb.size,
                                _ptr(qb), _ptr(pm), C.byref(info)))
     return {f: getattr(info, f) for f, _ in NrPlanInfo._fields_}
+
+
+def _out_array(shape, dtype, device):
+    if device is None:
+        return np.empty(shape, dtype=dtype)
+    import torch
+    tdt = {np.float64: torch.float64, np.complex128: torch.complex128}[dtype]
+    return torch.empty(shape, dtype=tdt, device=device)
+
+
+def philox_multipliers(seed: int, start: int, count: int, n_elem: int, spread: float = 0.2,
+                       device=None):
+    """Rows start..start+count of generate_load_multipliers on the GPU
+    (bitwise numpy's Philox4x64-10 stream keyed (seed, i))."""
+    load_library()
+    out = _out_array((count, n_elem), np.float64, device)
+    flags = ACPF_DEVICE_PTRS if device is not None else ACPF_HOST_PTRS
+    _check(_lib.acpf_philox_multipliers(int(seed), int(start), int(count), int(n_elem), float(spread),
+                                        _ptr(out), flags, None))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -237,6 +261,20 @@ class NrPlan:
         _check(_lib.acpf_nr_last_timing(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def scenarios(self, base, seed: int, start: int, count: int, spread: float = 0.2, device=None):
+        """Seeded (p_spec, q_spec) rows generated on the GPU, bitwise
+        batch.make_scenario_arrays(base, ScenarioSpec(..., seed, spread))."""
+        el = np.ascontiguousarray(base.load_elements, dtype=np.int32)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64)
+                for a in (base.p_load, base.q_load, base.p_gen, base.q_gen)]
+        p = _out_array((count, self.n_theta), np.float64, device)
+        q = _out_array((count, self.n_q), np.float64, device)
+        flags = ACPF_DEVICE_PTRS if device is not None else ACPF_HOST_PTRS
+        _check(_lib.acpf_nr_scenarios(self._h, int(seed), int(start), int(count), float(spread),
+                                      el.size, _ptr(el), *[_ptr(a) for a in arrs], _ptr(p), _ptr(q),
+                                      flags, None))
+        return p, q
+
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.acpf_nr_plan_destroy(self._h)
@@ -311,6 +349,31 @@ class ZbusPlan:
         ms, n = D(), I32()
         _check(_lib.acpf_zbus_last_timing(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def scenarios(self, base, seed: int, start: int, count: int, spread: float = 0.2, device=None):
+        """Seeded (s_wye, s_delta) rows generated on the GPU, bitwise
+        batch.make_scenario_arrays(base, ScenarioSpec(..., target='distribution'))."""
+        kinds = list(base.load_kinds)
+        tgt, wi, di = [], 0, 0
+        for k in kinds:
+            if k == "wye":
+                tgt.append(wi)
+                wi += 1
+            else:
+                tgt.append(-di - 1)
+                di += 1
+        tgt = np.ascontiguousarray(tgt, dtype=np.int32)
+        ws = np.ascontiguousarray(base.wye_s, dtype=np.complex128)
+        ds = np.ascontiguousarray(base.delta_s, dtype=np.complex128)
+        sw = _out_array((count, self.n_wye), np.complex128, device)
+        sd = _out_array((count, self.n_delta), np.complex128, device)
+        flags = ACPF_DEVICE_PTRS if device is not None else ACPF_HOST_PTRS
+        _check(_lib.acpf_zbus_scenarios(self._h, int(seed), int(start), int(count), float(spread),
+                                        tgt.size, _ptr(tgt), _ptr(ws) if ws.size else None,
+                                        _ptr(ds) if ds.size else None,
+                                        _ptr(sw) if self.n_wye else None,
+                                        _ptr(sd) if self.n_delta else None, flags, None))
+        return sw, sd
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:

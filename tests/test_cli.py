@@ -1,0 +1,40 @@
+"""CLI contract (reference cli.py): exit codes and routing onto the engine."""
+
+import json
+
+import pytest
+
+from paper_2605_14103_b200 import cli
+
+
+def test_missing_case_is_input_error(capsys):
+    assert cli.main(["solve", "--case", "/nonexistent/x.m"]) == 1
+    assert "error: io" in capsys.readouterr().err
+
+
+def test_bad_schema_is_input_error(tmp_path, capsys):
+    p = tmp_path / "bad.json"
+    p.write_text(json.dumps({"schema": "acpflow-zbus-network/1", "buses": []}))
+    assert cli.main(["solve", "--case", str(p)]) == 1
+    assert "error: schema" in capsys.readouterr().err
+
+
+def test_unknown_kind_is_input_error(tmp_path):
+    p = tmp_path / "x.txt"
+    p.write_text("hello")
+    assert cli.main(["solve", "--case", str(p)]) == 1
+
+
+@pytest.mark.gpu
+def test_solve_and_verify_on_gpu(tmp_path):
+    out = tmp_path / "r.json"
+    assert cli.main(["solve", "--case", "case118", "--batch", "16", "--seed", "1010",
+                     "--out", str(out)]) == 0
+    doc = json.loads(out.read_text())
+    assert doc["report"]["aggregate"]["n_converged"] == 16
+    assert len(doc["solutions"]) == 16
+    assert cli.main(["verify", "--case", "case118"]) == 0
+    assert cli.main(["verify", "--case", "ieee13"]) == 0
+    csv = tmp_path / "b.csv"
+    assert cli.main(["bench", "--case", "ieee13", "--batch", "64", "--out", str(csv)]) == 0
+    assert csv.read_text().splitlines()[0].startswith("case,kind,batch_size")

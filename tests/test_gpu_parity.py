@@ -146,3 +146,44 @@ def test_zbus_large_batch_consistent(zb_models, golden):
     assert out["converged"].all() and (out["residual_inf"] <= 1e-6).all()
     small = engine.zbus_solve_arrays(model, sw[:8], sd[:8], 1e-9, 100)
     np.testing.assert_array_equal(small["v"], out["v"][:8])
+
+
+# ---------------------------------------------------------------------------
+# device scenario generation: bitwise the reference generator
+# ---------------------------------------------------------------------------
+
+
+def test_philox_multipliers_bitwise(golden):
+    g = golden("philox")
+    k = 0
+    while f"m{k}" in g:
+        seed, count, n = (int(x) for x in g[f"spec{k}"])
+        got = engine.philox_multipliers(seed, 0, count, n, float(g[f"spread{k}"]))
+        np.testing.assert_array_equal(got, g[f"m{k}"])
+        k += 1
+    # a shard of rows equals the same rows of the host table
+    host = pf.generate_load_multipliers(pf.ScenarioSpec(count=300, seed=77), 1625)
+    dev = engine.philox_multipliers(77, 200, 100, 1625, 0.2)
+    np.testing.assert_array_equal(dev, host[200:])
+
+
+@pytest.mark.parametrize("tag", ["case118", "gb2224"])
+def test_nr_device_scenarios_bitwise(tag, tx_models, golden):
+    g = golden(f"nr_{tag}")
+    model = tx_models[tag]
+    base = pf.transmission_base(model.net, model.part)
+    count = g["p_spec"].shape[0]
+    p, q = model.plan().scenarios(base, int(g["seed"]), 0, count)
+    np.testing.assert_array_equal(p, g["p_spec"])
+    np.testing.assert_array_equal(q, g["q_spec"])
+
+
+@pytest.mark.parametrize("tag", ["ieee13", "ieee123", "eulv"])
+def test_zbus_device_scenarios_bitwise(tag, zb_models, golden):
+    g = golden(f"zb_{tag}")
+    model = zb_models[tag]
+    base = pf.distribution_base(model)
+    count = min(256, g["s_wye"].shape[0])
+    sw, sd = engine.zbus_plan_for(model).scenarios(base, int(g["seed"]), 0, count)
+    np.testing.assert_array_equal(sw, g["s_wye"][:count])
+    np.testing.assert_array_equal(sd, g["s_delta"][:count])
