@@ -56,6 +56,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -145,12 +149,22 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
   };
 
+  // bars[0..1]: stage full (TMA tx count); bars[2..3]: stage empty (one
+  // arrive per warp once its DMMAs on the stage are issued and complete).
+  // Thread 0 refills a buffer only after all warps released it, so warps may
+  // drift by up to one stage and a warp's epilogue overlaps the DMMA work of
+  // the others. Empty-barrier parities live in bits 2..3 of phase_bits.
   if (tid == 0) {
     issue(0);
     if (n_stage > 1) issue(1);
   }
 
   double cr[2][CGW][2], ci[2][CGW][2];
+  // per-lane running column partials over all row blocks (rows lane/4 of the
+  // warp's two row groups); reduced across lanes/warps once per pass
+  double acc[CGW][2];
+#pragma unroll
+  for (int b = 0; b < CGW; ++b) acc[b][0] = acc[b][1] = 0.0;
   for (int sidx = 0; sidx < n_stage; ++sidx) {
     const int rb = sidx / n_kc, kc = sidx % n_kc;
     const int buf = sidx & 1;
@@ -191,11 +205,16 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
         }
       }
     }
+    // release the stage buffer (all lanes' shared reads of zb are done)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bars + 2 + buf);
+    if (tid == 0 && sidx + 2 < n_stage) {
+      mbar_wait(bars + 2 + buf, (phase_bits >> (2 + buf)) & 1u);
+      phase_bits ^= (1u << (2 + buf));
+      issue(sidx + 2);
+    }
     if (kc == n_kc - 1) {
-      // ---- epilogue for row block rb
-      double part[CGW][2];
-#pragma unroll
-      for (int b = 0; b < CGW; ++b) part[b][0] = part[b][1] = 0.0;
+      // ---- epilogue for row block rb (no CTA-wide synchronisation)
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
         const int row = rb * kZbRows + (rp * 2 + a) * 8 + (lane >> 2);
@@ -213,48 +232,57 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
                 contrib = sqrt(vr * vr + vi * vi);
                 if (st.run[col]) io.v_out[(tile_col0 + col) * m.n + row] = make_double2(vr, vi);
               }
-              part[b][j] = part[b][j] + contrib;
+              acc[b][j] = acc[b][j] + contrib;
             } else if (MODE == kMag0) {
               if (in) contrib = sqrt(vr * vr + vi * vi);
-              part[b][j] = part[b][j] + contrib;
+              acc[b][j] = acc[b][j] + contrib;
             } else {  // certificate: |v_final - (Z i(v_final) + v0)|
               if (in && st.cert[col]) {
                 const double2 vf = io.v_out[(tile_col0 + col) * m.n + row];
                 const double dr = vf.x - vr, di = vf.y - vi;
                 contrib = sqrt(dr * dr + di * di);
               }
-              part[b][j] = nanmax(part[b][j], contrib);
+              acc[b][j] = nanmax(acc[b][j], contrib);
             }
           }
         }
       }
-      // reduce over the 8 row lanes (lane bits 2..4), fixed order
-#pragma unroll
-      for (int b = 0; b < CGW; ++b)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          double x = part[b][j];
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            const double o = __shfl_xor_sync(0xffffffffu, x, off);
-            x = (MODE == kCert) ? nanmax(x, o) : x + o;
-          }
-          if (lane < 4) st.red[rp * NT + (ch * CGW + b) * 8 + 2 * lane + j] = x;
-        }
-      __syncthreads();
-      if (tid < NT) {
-        const double* r = st.red;
-        if (MODE == kCert) {
-          st.colsum[tid] = nanmax(nanmax(nanmax(st.colsum[tid], r[tid]), r[NT + tid]),
-                                  nanmax(r[2 * NT + tid], r[3 * NT + tid]));
-        } else {
-          st.colsum[tid] = st.colsum[tid] + (((r[tid] + r[NT + tid]) + r[2 * NT + tid]) + r[3 * NT + tid]);
-        }
-      }
     }
-    __syncthreads();  // everyone is done with zs[buf] (and red)
-    if (tid == 0 && sidx + 2 < n_stage) issue(sidx + 2);
   }
+  // the empty-barrier phases of the stages whose refill was not needed
+  // (the last two) still advance: keep thread 0's parity bits in sync
+  if (tid == 0) {
+    for (int sidx = (n_stage > 2 ? n_stage - 2 : 0); sidx < n_stage; ++sidx) {
+      const int buf = sidx & 1;
+      mbar_wait(bars + 2 + buf, (phase_bits >> (2 + buf)) & 1u);
+      phase_bits ^= (1u << (2 + buf));
+    }
+  }
+  // ---- per-pass column reduction: 8 row lanes (fixed butterfly), then the
+  // 4 row-pair warps in fixed order
+#pragma unroll
+  for (int b = 0; b < CGW; ++b)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double x = acc[b][j];
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, x, off);
+        x = (MODE == kCert) ? nanmax(x, o) : x + o;
+      }
+      if (lane < 4) st.red[rp * NT + (ch * CGW + b) * 8 + 2 * lane + j] = x;
+    }
+  __syncthreads();
+  if (tid < NT) {
+    const double* r = st.red;
+    if (MODE == kCert) {
+      st.colsum[tid] = nanmax(nanmax(nanmax(st.colsum[tid], r[tid]), r[NT + tid]),
+                              nanmax(r[2 * NT + tid], r[3 * NT + tid]));
+    } else {
+      st.colsum[tid] = st.colsum[tid] + (((r[tid] + r[NT + tid]) + r[2 * NT + tid]) + r[3 * NT + tid]);
+    }
+  }
+  __syncthreads();
 }
 
 // Column-owner work: build I_l for column `col` from v at the load rows.
@@ -339,6 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     mbar_init(bars + 0, 1);
     mbar_init(bars + 1, 1);
+    mbar_init(bars + 2, kThreads / 32);
+    mbar_init(bars + 3, kThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -451,7 +481,7 @@ size_t zbus_smem_bytes(int kpad) {
   const int ksteps = kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
   size_t d = 2 * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + 4 * NT + 3 * NT;
-  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 16 + 16;
+  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 32 + 16;
   return bytes;
 }
 
