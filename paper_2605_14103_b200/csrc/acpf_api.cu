@@ -109,6 +109,9 @@ struct acpf_nr_plan {
 struct acpf_zbus_plan {
   int device = 0;
   int n_wye = 0, n_delta = 0;
+  cudaStream_t copy_stream = nullptr;  // host-path H2D/D2H overlap
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_kend[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
   ZbDeviceModel dm{};
   DevArena model;
   DevArena stage;
@@ -584,6 +587,110 @@ acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const 
   return ACPF_OK;
 }
 
+static acpf_status zbus_solve_host(acpf_zbus_plan* p, int64_t batch, const double* s_wye,
+                                   const double* s_delta, double tol, int32_t max_iter, double* v_out,
+                                   uint8_t* converged, int32_t* iterations, double* final_delta,
+                                   double* residual_inf, int32_t* status, int32_t* floor_slot,
+                                   cudaStream_t st) {
+  // Two staging sets; chunk c+1's H2D and chunk c's D2H run on a copy stream
+  // while chunk c+1 computes, so the voltage read-back overlaps the solve.
+  const ZbDeviceModel& d = p->dm;
+  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(1, env_int("ACPF_ZBUS_CHUNK", 32768)));
+  const size_t in_b = (size_t)(d.n_wye + d.n_delta) * 16;
+  const size_t out_b = (size_t)d.n * 16 + 1 + 4 + 8 + 8 + 4 + 4;
+  const size_t set_b = (size_t)chunk * (in_b + out_b) + 256;
+  acpf_status rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, 2 * set_b);
+  if (rc != ACPF_OK) return rc;
+  if (!p->copy_stream) ACPF_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    if (!p->ev_h2d[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
+    if (!p->ev_kend[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_kend[k], cudaEventDisableTiming));
+    if (!p->ev_d2h[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_d2h[k], cudaEventDisableTiming));
+  }
+  cudaStream_t cs = p->copy_stream;
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  struct Set {
+    double2 *sw, *sd, *vo;
+    double *fd, *rs;
+    int32_t *it, *stt, *fs;
+    uint8_t* cv;
+  } sets[2];
+  for (int k = 0; k < 2; ++k) {
+    char* b = (char*)p->stage_base + k * set_b;
+    Set& S = sets[k];
+    S.sw = (double2*)b; b += (size_t)chunk * d.n_wye * 16;
+    S.sd = (double2*)b; b += (size_t)chunk * d.n_delta * 16;
+    S.vo = (double2*)b; b += (size_t)chunk * d.n * 16;
+    S.fd = (double*)b; b += (size_t)chunk * 8;
+    S.rs = (double*)b; b += (size_t)chunk * 8;
+    S.it = (int32_t*)b; b += (size_t)chunk * 4;
+    S.stt = (int32_t*)b; b += (size_t)chunk * 4;
+    S.fs = (int32_t*)b; b += (size_t)chunk * 4;
+    S.cv = (uint8_t*)b;
+  }
+  std::vector<cudaEvent_t> tev(2 * nchunks, nullptr);
+  for (auto& e : tev) ACPF_CUDA(cudaEventCreate(&e));
+  auto h2d = [&](int64_t c) -> acpf_status {
+    const int k = (int)(c & 1);
+    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    ACPF_CUDA(cudaStreamWaitEvent(cs, p->ev_kend[k], 0));  // inputs of chunk c-2 consumed
+    if (d.n_wye)
+      ACPF_CUDA(cudaMemcpyAsync(sets[k].sw, s_wye + 2 * s0 * d.n_wye, nb * d.n_wye * 16, cudaMemcpyHostToDevice, cs));
+    if (d.n_delta)
+      ACPF_CUDA(cudaMemcpyAsync(sets[k].sd, s_delta + 2 * s0 * d.n_delta, nb * d.n_delta * 16, cudaMemcpyHostToDevice, cs));
+    ACPF_CUDA(cudaEventRecord(p->ev_h2d[k], cs));
+    return ACPF_OK;
+  };
+  int launches = 0;
+  if ((rc = h2d(0)) != ACPF_OK) return rc;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int k = (int)(c & 1);
+    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    const Set& S = sets[k];
+    ZbBatchIO io{};
+    io.batch = nb;
+    io.s_wye = S.sw;
+    io.s_delta = S.sd;
+    io.v_out = S.vo;
+    io.final_delta = S.fd;
+    io.residual = S.rs;
+    io.iterations = S.it;
+    io.status = S.stt;
+    io.floor_slot = S.fs;
+    io.converged = S.cv;
+    ACPF_CUDA(cudaStreamWaitEvent(st, p->ev_h2d[k], 0));
+    if (c >= 2) ACPF_CUDA(cudaStreamWaitEvent(st, p->ev_d2h[k], 0));  // outputs of chunk c-2 read back
+    int nl = 0;
+    ACPF_CUDA(cudaEventRecord(tev[2 * c], st));
+    ACPF_CUDA(launch_zbus(d, io, tol, max_iter, false, nullptr, &nl, st));
+    ACPF_CUDA(cudaEventRecord(tev[2 * c + 1], st));
+    ACPF_CUDA(cudaEventRecord(p->ev_kend[k], st));
+    launches += nl;
+    if (c + 1 < nchunks && (rc = h2d(c + 1)) != ACPF_OK) return rc;
+    ACPF_CUDA(cudaStreamWaitEvent(cs, p->ev_kend[k], 0));
+    ACPF_CUDA(cudaMemcpyAsync(v_out + 2 * s0 * d.n, S.vo, nb * d.n * 16, cudaMemcpyDeviceToHost, cs));
+    if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, S.cv, nb, cudaMemcpyDeviceToHost, cs));
+    if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + s0, S.it, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (final_delta) ACPF_CUDA(cudaMemcpyAsync(final_delta + s0, S.fd, nb * 8, cudaMemcpyDeviceToHost, cs));
+    if (residual_inf) ACPF_CUDA(cudaMemcpyAsync(residual_inf + s0, S.rs, nb * 8, cudaMemcpyDeviceToHost, cs));
+    if (status) ACPF_CUDA(cudaMemcpyAsync(status + s0, S.stt, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (floor_slot) ACPF_CUDA(cudaMemcpyAsync(floor_slot + s0, S.fs, nb * 4, cudaMemcpyDeviceToHost, cs));
+    ACPF_CUDA(cudaEventRecord(p->ev_d2h[k], cs));
+  }
+  ACPF_CUDA(cudaStreamSynchronize(cs));
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  float total = 0.0f;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    float ms = 0.0f;
+    ACPF_CUDA(cudaEventElapsedTime(&ms, tev[2 * c], tev[2 * c + 1]));
+    total += ms;
+  }
+  for (auto& e : tev) cudaEventDestroy(e);
+  p->last_ms = total;
+  p->last_launches = launches;
+  return ACPF_OK;
+}
+
 acpf_status acpf_zbus_solve(acpf_zbus_plan_t p, int64_t batch, const double* s_wye,
                             const double* s_delta, double tol, int32_t max_iter, double* v_out,
                             uint8_t* converged, int32_t* iterations, double* final_delta,
@@ -599,7 +706,10 @@ acpf_status acpf_zbus_solve(acpf_zbus_plan_t p, int64_t batch, const double* s_w
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
-  int64_t chunk = dev_ptrs ? batch : std::min<int64_t>(batch, env_int("ACPF_ZBUS_CHUNK", 65536));
+  if (!dev_ptrs)
+    return zbus_solve_host(p, batch, s_wye, s_delta, tol, max_iter, v_out, converged, iterations,
+                           final_delta, residual_inf, status, floor_slot, st);
+  int64_t chunk = batch;
   const size_t in_b = (size_t)(d.n_wye + d.n_delta) * 16;
   const size_t out_b = (size_t)d.n * 16 + 1 + 4 + 8 + 8 + 4 + 4;
   if (!dev_ptrs) {
@@ -696,6 +806,12 @@ acpf_status acpf_zbus_plan_destroy(acpf_zbus_plan_t p) {
     DeviceGuard dg(p->device);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    for (int k = 0; k < 2; ++k) {
+      if (p->ev_h2d[k]) cudaEventDestroy(p->ev_h2d[k]);
+      if (p->ev_kend[k]) cudaEventDestroy(p->ev_kend[k]);
+      if (p->ev_d2h[k]) cudaEventDestroy(p->ev_d2h[k]);
+    }
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     p->stage.release();
     p->model.release();
   }
