@@ -399,16 +399,25 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   pp.lane = lane;
   pp.begin(m.stream, m.row_sptr[p0], m.row_sptr[p1]);
   bool zero = false;
+  // slot control words of the whole task (lane j holds slot tw + j), double
+  // buffered so the next window's load is in flight a window ahead
+  const int ts0 = m.row_slot[p0], ts1 = m.row_slot[p1];
+  int tw = ts0;
+  uint32_t winfo = ts0 + lane < ts1 ? m.slot_info[ts0 + lane] : 0u;
+  uint32_t ninfo = ts0 + 32 + lane < ts1 ? m.slot_info[ts0 + 32 + lane] : 0u;
+  int t = ts0;
   for (int p = p0; p < p1; ++p) {
-    const int t0 = m.row_slot[p], t1 = m.row_slot[p + 1];
+    const int t0 = t;
     pp.ensure(pp.q);
     double yacc = lds_f64(pp.addr(pp.q, bi, sc));  // b_p[i]
     ++pp.q;
-    uint32_t winfo = 0;
-    for (int t = t0; t < t1; ++t) {
-      const int jj = (t - t0) & 31;
-      if (jj == 0) winfo = t + lane < t1 ? m.slot_info[t + lane] : 0u;
-      const uint32_t info = __shfl_sync(kFull, winfo, jj);
+    for (;; ++t) {
+      if (t - tw == 32) {
+        tw += 32;
+        winfo = ninfo;
+        ninfo = tw + 32 + lane < ts1 ? m.slot_info[tw + 32 + lane] : 0u;
+      }
+      const uint32_t info = __shfl_sync(kFull, winfo, t - tw);
       const int cnt = (int)(info >> 16);
       double a = 0.0, a2 = 0.0;
       if (!(info & kSlotFill)) {
@@ -472,6 +481,10 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         }
         BL(gb.b, m.off_lu + t, ce) = a;
       }
+      if (info & kSlotRowEnd) {
+        ++t;
+        break;
+      }
     }
     if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
     __syncwarp();  // lbuf of this row complete before the next row of the task reuses it
@@ -498,8 +511,17 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
   pp.wring = ring + kRing * kBlkBytes;
   pp.lane = lane;
   pp.begin(m.stream, m.brow_sptr[r0], m.brow_sptr[r1]);
+  // back-row words of the task (lane j holds row rw + j), double buffered
+  int rw = r0;
+  uint32_t wrow = r0 + lane < r1 ? m.brow[r0 + lane] : 0u;
+  uint32_t nrow = r0 + 32 + lane < r1 ? m.brow[r0 + 32 + lane] : 0u;
   for (int rr = r0; rr < r1; ++rr) {
-    const uint32_t b = m.brow[rr];
+    if (rr - rw == 32) {
+      rw += 32;
+      wrow = nrow;
+      nrow = rw + 32 + lane < r1 ? m.brow[rw + 32 + lane] : 0u;
+    }
+    const uint32_t b = __shfl_sync(kFull, wrow, rr - rw);
     const int p = (int)(b & 0xfffffu);
     const int cnt = (int)(b >> 20);
     pp.ensure(pp.q + 1);

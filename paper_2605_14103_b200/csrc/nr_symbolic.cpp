@@ -359,6 +359,7 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     for (int64_t t = r0; t < r1; ++t) {
       uint32_t info = 0;
       if (t == s.diag[p]) info |= kSlotDiag;
+      if (t == r1 - 1) info |= kSlotRowEnd;
       if (t < s.diag[p]) info |= kSlotL;
       const bool fill = s.slot_type[t] == 8;
       if (fill) info |= kSlotFill;

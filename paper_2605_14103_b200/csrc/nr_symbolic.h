@@ -67,6 +67,7 @@ struct NrSchedule {
 };
 
 constexpr uint32_t kSlotDiag = 1u << 5;
+constexpr uint32_t kSlotRowEnd = 1u << 6;
 constexpr uint32_t kSlotL = 1u << 8;
 constexpr uint32_t kSlotFill = 1u << 9;
 
