@@ -179,7 +179,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     const std::vector<int32_t> lperm = level_sorted_perm(first);
     build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, lperm.data());
     build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch,
-                      (int)env_int("ACPF_NR_TASK_ELEMS", 512));
+                      (int)env_int("ACPF_NR_TASK_ELEMS", 512),
+                      env_int("ACPF_NR_COLUMN_STORE", 1) != 0);
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;
@@ -227,6 +228,21 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   p->hs.n_levels = sc.n_levels;
   p->hs.n_blevels = sc.n_blevels;
   p->hs.max_l = sc.max_l;
+  {
+    // factor pipeline variant: the requested one if its shared memory (ring +
+    // the longest L part of a row) fits one SM, else the next smaller one
+    constexpr size_t kSmemMax = 227 * 1024;
+    int v = (int)env_int("ACPF_NR_VARIANT", 0);
+    v = v < 0 ? 0 : (v > 2 ? 2 : v);
+    while (v > 0 && nr_smem_bytes(v, sc.max_l) > kSmemMax) --v;
+    if (nr_smem_bytes(v, sc.max_l) > kSmemMax) {
+      set_error("acpf_nr_plan_create: an L row of " + std::to_string(sc.max_l) +
+                " blocks exceeds the shared-memory row buffer");
+      delete p;
+      return ACPF_ESTRUCT;
+    }
+    p->hs.variant = v;
+  }
   cudaError_t e = cudaSuccess;
   auto up = [&](auto** dst, const auto* src, size_t cnt) {
     if (e == cudaSuccess) e = p->model.upload(dst, src, cnt);
@@ -245,6 +261,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<int32_t**>(&d.asm_j), sc.asm_j.data(), sc.asm_j.size());
   up(const_cast<int32_t**>(&d.asm_slot), sc.asm_slot.data(), sc.asm_slot.size());
   up(const_cast<uint32_t**>(&d.slot_info), sc.slot_info.data(), sc.slot_info.size());
+  up(const_cast<int32_t**>(&d.slot_store), sc.slot_store.data(), sc.slot_store.size());
   up(const_cast<int32_t**>(&d.row_slot), sc.row_slot.data(), sc.row_slot.size());
   up(const_cast<int32_t**>(&d.row_sptr), sc.row_sptr.data(), sc.row_sptr.size());
   up(const_cast<int32_t**>(&d.task_row), sc.task_row.data(), sc.task_row.size());

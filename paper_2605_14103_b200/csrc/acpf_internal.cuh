@@ -33,6 +33,7 @@ struct NrDeviceModel {
   const int32_t* asm_j;       // [entries]
   const int32_t* asm_slot;    // [entries] LU block slot (-1 slack column)
   const uint32_t* slot_info;  // [nnz_lu]
+  const int32_t* slot_store;  // [nnz_lu] storage position in the LU region
   const int32_t* row_slot;    // [n_rows+1]
   const int32_t* task_row;    // [n_tasks+1] factor warp tasks (row ranges)
   const int32_t* btask_row;   // [n_btasks+1] back warp tasks (back-order row ranges)
@@ -51,6 +52,7 @@ struct NrHostSchedule {
   const int32_t* level_maxl;       // [n_levels]
   const int32_t* blevel_task_ptr;  // [n_blevels+1]
   int n_levels, n_blevels, max_l;
+  int variant;  // factor/back pipeline: 0 = 1 group/warp, 1 = 2 groups x 4-element stages, 2 = 2 groups x 8
 };
 
 struct NrWorkspace {
@@ -80,7 +82,8 @@ struct NrBatchIO {
   int64_t batch;  // scenarios in this chunk
 };
 
-size_t nr_smem_bytes(int cap);
+// dynamic smem of a factor launch (pipeline variant, longest L part of its rows)
+size_t nr_smem_bytes(int variant, int cap);
 size_t nr_group_state_bytes();
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,

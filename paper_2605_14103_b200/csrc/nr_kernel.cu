@@ -10,8 +10,8 @@
 // scenario owns a quad of lanes (lane = r*8 + sc): in block operations lane r
 // owns entry (r/2, r%2) of every 2x2 block of scenario sc. A per-group arena
 // holds a block region (element = 4 entries x 8 scenarios = 256 contiguous
-// bytes, entry-major, so one LDGSTS/STG per lane moves a whole element for the
-// group) followed by a scalar region (element = 8 scenarios = 64 bytes).
+// bytes, two block-column halves of 128 B; see BL) followed by a scalar region
+// (element = 8 scenarios = 64 bytes).
 //
 // One Newton step of the reference `_newton_loop` (transmission.py:333-380)
 // for the whole batch is a short sequence of launches on one stream:
@@ -45,11 +45,9 @@ namespace acpf {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCh = 8;     // elements per pipeline stage
-constexpr int kNBuf = 8;   // stages in the ring (kNBuf-1 in flight)
-constexpr int kRing = kCh * kNBuf;
 constexpr int kBlk = 4 * kGroup;      // doubles per block element (32)
 constexpr int kBlkBytes = kBlk * 8;   // 256
+constexpr int kHalf = kBlkBytes / 2;  // bytes of one block column of the group (128)
 constexpr int kBusChunk = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -102,16 +100,27 @@ __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
   return make_double2(u.x * a.x + u.y * a.y, u.y * a.x - u.x * a.y);
 }
 
-// Per-warp gather pipeline over the stream range [s0, s0 + n).
+// Per-warp gather pipeline over the stream range [s0, s0 + n) for a unit of
+// NG consecutive scenario groups. A ring slot holds one stream element of all
+// NG groups (NG x 256 B, group h at +256h); CH elements per stage, NBUF
+// stages in the ring.
+template <int NG, int CH, int NBUF>
 struct Pipe {
+  static constexpr int kSlot = NG * kBlkBytes;
+  static constexpr int kRingN = CH * NBUF;
+  static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
   const uint32_t* stream;
-  const double* blocks;  // group block region (element e at blocks + e*32)
-  uint32_t ring;         // smem [kRing] elements of 256 B
-  uint32_t wring;        // smem [kRing] u32 stream words
+  const double* src;  // this lane's copy source: its group's block region + chunk
+  bool cp_ok;         // this lane's group is live (NG = 2: lanes 16-31 copy group 1)
+  uint32_t ring;      // smem [kRingN] slots
+  uint32_t wring;     // smem [kRingN] u32 stream words
   int lane;
   int s0, n, issued, ready_upto, q;
   uint32_t wcur, wnext;  // word windows: lane j holds the word of element (wbase + j)
   int wbase;
+
+  static constexpr size_t kSmem = (size_t)kRingN * (kSlot + 4);
+  __host__ __device__ static constexpr size_t smem_bytes() { return kSmem; }
 
   __device__ __forceinline__ uint32_t load_window(int base) const {
     const int k = base + lane;
@@ -120,27 +129,35 @@ struct Pipe {
 
   __device__ __forceinline__ void issue_stage() {
     const int c = issued++;
-    const int e0 = c * kCh;
+    const int e0 = c * CH;
     if (e0 < n) {
       if (e0 >= wbase + 32) {  // advance the double-buffered word window
         wbase += 32;
         wcur = wnext;
         wnext = load_window(wbase + 32);
       }
-      const int slot = (c % kNBuf) * kCh;
-      const int lim = min(kCh, n - e0);
+      const int slot = (c % NBUF) * CH;
+      const int lim = min(CH, n - e0);
       const int jw = e0 - wbase;
+      // the consumer only needs the L position, pre-scaled to a byte offset
       const uint32_t mine = __shfl_sync(kFull, wcur, (jw + lane) & 31);
-      if (lane < lim) sts_u32(wring + (slot + lane) * 4, mine);
-      // 16 B per lane: lanes 0-15 copy element j, lanes 16-31 element j+1
-      const int half = lane >> 4, chunk = lane & 15;
+      if (lane < lim) sts_u32(wring + (slot + lane) * 4, (mine >> 22) * (uint32_t)kSlot);
+      if (NG == 1) {
+        // 16 B per lane: lanes 0-15 copy element j, lanes 16-31 element j+1
+        const int half = lane >> 4, chunk = lane & 15;
 #pragma unroll
-      for (int j = 0; j < kCh; j += 2) {
-        const int jj = j + half;
-        const uint32_t w = __shfl_sync(kFull, wcur, (jw + jj) & 31);
-        if (jj < lim)
-          cp_async16(ring + (slot + jj) * kBlkBytes + chunk * 16,
-                     blocks + (size_t)(w & 0x3fffffu) * kBlk + chunk * 2);
+        for (int j = 0; j < CH; j += 2) {
+          const int jj = j + half;
+          const uint32_t w = __shfl_sync(kFull, wcur, (jw + jj) & 31);
+          if (jj < lim) cp_async16(ring + (slot + jj) * kSlot + chunk * 16, src + (size_t)(w & 0x3fffffu) * kBlk);
+        }
+      } else {
+        // one element per instruction: lanes 0-15 group 0, lanes 16-31 group 1
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
+          if (j < lim && cp_ok) cp_async16(ring + (slot + j) * kSlot + lane * 16, src + (size_t)(w & 0x3fffffu) * kBlk);
+        }
       }
     }
     cp_commit();
@@ -157,29 +174,29 @@ struct Pipe {
     wcur = load_window(0);
     wnext = load_window(32);
 #pragma unroll 1
-    for (int k = 0; k < kNBuf - 2; ++k) issue_stage();
+    for (int k = 0; k < NBUF - 2; ++k) issue_stage();
   }
 
   // Make element e resident. Callers keep e <= q + 1 (q = first element not
-  // yet consumed). kNBuf-2 stages are in flight, so the stage issued here
-  // reuses the slot of stage (e/kCh - 2), which is fully consumed.
+  // yet consumed). NBUF-2 stages are in flight, so the stage issued here
+  // reuses the slot of stage (e/CH - 2), which is fully consumed.
   __device__ __forceinline__ void ensure(int e) {
     while (e >= ready_upto) {
-      cp_wait<kNBuf - 3>();
+      cp_wait<NBUF - 3>();
       __syncwarp();
       issue_stage();
-      ready_upto += kCh;
+      ready_upto += CH;
     }
   }
 
-  // smem address of entry `ent` (0..3) of element e for scenario sc
-  __device__ __forceinline__ uint32_t addr(int e, int ent, int sc) const {
-    return ring + (e % kRing) * kBlkBytes + (sc * 4 + ent) * 8;
+  __device__ __forceinline__ uint32_t slot_base(int e) const {
+    return ring + ((uint32_t)e % (uint32_t)kRingN) * kSlot;
   }
 
-  __device__ __forceinline__ uint32_t word(int e) const { return lds_u32(wring + (e % kRing) * 4); }
-
-  __device__ __forceinline__ uint32_t slot_base(int e) const { return ring + (e % kRing) * kBlkBytes; }
+  // byte offset of element e's L block in the row buffer (lpos * kSlot)
+  __device__ __forceinline__ uint32_t lofs(int e) const {
+    return lds_u32(wring + ((uint32_t)e % (uint32_t)kRingN) * 4);
+  }
 
   __device__ __forceinline__ void finish() {
     cp_wait<0>();
@@ -187,10 +204,12 @@ struct Pipe {
   }
 };
 
-// block-region entry `ent` of block element e, scenario sc (B = group block base + 4*sc).
-// Elements are scenario-major (4 consecutive entries per scenario). Matrix
-// blocks are stored column-major: entry (i, j) at 2*j + i.
-#define BL(B, e, ent) (B)[(size_t)(e) * kBlk + (ent)]
+// block-region entry `ent` of block element e, scenario sc (B = group block base + 2*sc).
+// An element is two 128-byte column halves: entry (i, j) of scenario sc at
+// double 16*j + 2*sc + i, so the 8 lanes of a quarter-warp that read column j
+// (or a row-major L row i) of their 8 scenarios touch one contiguous 128 B
+// (conflict-free 16-byte shared loads).
+#define BL(B, e, ent) (B)[(size_t)(e) * kBlk + ((ent) >> 1) * (2 * kGroup) + ((ent) & 1)]
 // scalar-region element e, scenario sc (S = group scalar base + sc)
 #define SL(S, e) (S)[(size_t)(e) * kGroup]
 
@@ -202,7 +221,7 @@ struct GroupBase {
 __device__ __forceinline__ GroupBase group_base(const NrDeviceModel& m, const NrWorkspace& w, int64_t g,
                                                 int sc) {
   double* base = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
-  return GroupBase{base + 4 * sc, base + m.n_block * kBlk + sc};
+  return GroupBase{base + 2 * sc, base + m.n_block * kBlk + sc};
 }
 
 __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
@@ -371,150 +390,217 @@ __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_new
   }
 }
 
-// One elimination level: task = (run of block rows of the level, group).
-// Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every block of scenario sc.
-__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0) {
+// Live groups of the unit: bit h set if group g0 + h exists and is active.
+template <int NG>
+__device__ __forceinline__ unsigned unit_live(const NrWorkspace& w, int64_t g0) {
+  unsigned live = 0;
+#pragma unroll
+  for (int h = 0; h < NG; ++h)
+    if (g0 + h < w.groups && w.gactive[g0 + h]) live |= 1u << h;
+  return live;
+}
+
+template <int NG, int CH, int NBUF>
+__device__ __forceinline__ void pipe_setup(Pipe<NG, CH, NBUF>& pp, const NrDeviceModel& m, const NrWorkspace& w,
+                                           int64_t g0, unsigned live, uint32_t ring, int lane) {
+  const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
+  const int half = lane >> 4, chunk = lane & 15;
+  const int h = NG == 1 ? 0 : half;
+  pp.src = w.arena + (size_t)(g0 + h) * gstride + chunk * 2;
+  pp.cp_ok = (live >> h) & 1u;
+  pp.ring = ring;
+  pp.wring = ring + Pipe<NG, CH, NBUF>::kRingN * Pipe<NG, CH, NBUF>::kSlot;
+  pp.lane = lane;
+}
+
+// One elimination level: task = (run of block rows of the level, unit of NG
+// scenario groups). Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every
+// block of scenario sc of each group of the unit; the NG groups share every
+// address computation (their copies sit 256 B apart in each ring slot).
+template <int NG, int CH, int NBUF>
+__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units) {
+  using P = Pipe<NG, CH, NBUF>;
+  constexpr int kSlot = P::kSlot;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
-  const int64_t g = task % w.groups;
-  const int tk = task0 + (int)(task / w.groups);
-  if (!w.gactive[g]) return;
-  const GroupBase gb = group_base(m, w, g, sc);
+  const int64_t g0 = (task % units) * NG;
+  const int tk = task0 + (int)(task / units);
+  const unsigned live = unit_live<NG>(w, g0);
+  if (!live) return;
+  const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
+  double* const gb0 = w.arena + (size_t)g0 * gstride + 2 * sc;  // group h at + h*gstride
   const uint32_t ring = su32(smem);
-  const uint32_t wring = ring + kRing * kBlkBytes;
-  const uint32_t lbuf = wring + kRing * 4;
-  // lbuf holds the row's L blocks row-major: entry (i, j) of scenario sc at
-  // lbuf + pos*256 + (4*sc + 2*i + j)*8, so L[i][0..1] is one 16-byte load;
-  // U blocks are column-major so U[0..1][j] is one 16-byte load too
-  const uint32_t offL = (4 * sc + 2 * bi) * 8;   // L[i][0], L[i][1]
-  const uint32_t offU = (4 * sc + 2 * bj) * 8;   // U[0][j], U[1][j] (column j)
+  const uint32_t lbuf = ring + P::smem_bytes();
+  // lbuf holds the row's L blocks row-major: entry (i, j) of scenario sc of
+  // group h at lbuf + pos*kSlot + h*256 + 128*i + 16*sc + 8*j, so L[i][0..1]
+  // is one 16-byte load; U[0..1][j] of a ring element is one too
+  const uint32_t offL = kHalf * bi + 16 * sc;  // L[i][0], L[i][1] (row i)
+  const uint32_t offU = kHalf * bj + 16 * sc;  // U[0][j], U[1][j] (column j)
   const int ce = 2 * bj + bi;                     // this lane's column-major entry
+  const uint32_t lrow = lbuf + offL;
   const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
-  Pipe pp;
-  pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
-  pp.ring = ring;
-  pp.wring = wring;
-  pp.lane = lane;
+  P pp;
+  pipe_setup(pp, m, w, g0, live, ring, lane);
   pp.begin(m.stream, m.row_sptr[p0], m.row_sptr[p1]);
-  bool zero = false;
+  unsigned zero = 0;
   // slot control words of the whole task (lane j holds slot tw + j), double
   // buffered so the next window's load is in flight a window ahead
   const int ts0 = m.row_slot[p0], ts1 = m.row_slot[p1];
   int tw = ts0;
   uint32_t winfo = ts0 + lane < ts1 ? m.slot_info[ts0 + lane] : 0u;
   uint32_t ninfo = ts0 + 32 + lane < ts1 ? m.slot_info[ts0 + 32 + lane] : 0u;
+  int32_t wstore = ts0 + lane < ts1 ? m.slot_store[ts0 + lane] : 0;
+  int32_t nstore = ts0 + 32 + lane < ts1 ? m.slot_store[ts0 + 32 + lane] : 0;
   int t = ts0;
   for (int p = p0; p < p1; ++p) {
     const int t0 = t;
     pp.ensure(pp.q);
-    double yacc = lds_f64(pp.addr(pp.q, bi, sc));  // b_p[i]
+    double yacc[NG];  // b_p[i]
+    {
+      const uint32_t sb = pp.slot_base(pp.q) + 16 * sc + 8 * bi;
+#pragma unroll
+      for (int h = 0; h < NG; ++h) yacc[h] = lds_f64(sb + h * kBlkBytes);
+    }
     ++pp.q;
     for (;; ++t) {
       if (t - tw == 32) {
         tw += 32;
         winfo = ninfo;
+        wstore = nstore;
         ninfo = tw + 32 + lane < ts1 ? m.slot_info[tw + 32 + lane] : 0u;
+        nstore = tw + 32 + lane < ts1 ? m.slot_store[tw + 32 + lane] : 0;
       }
       const uint32_t info = __shfl_sync(kFull, winfo, t - tw);
       const int cnt = (int)(info >> 16);
-      double a = 0.0, a2 = 0.0;
+      double a[NG], a2[NG], a3[NG], a4[NG];
+#pragma unroll
+      for (int h = 0; h < NG; ++h) a[h] = a2[h] = a3[h] = a4[h] = 0.0;
       if (!(info & kSlotFill)) {
         pp.ensure(pp.q);
-        a = lds_f64(pp.addr(pp.q, ce, sc));
+        const uint32_t sb = pp.slot_base(pp.q) + kHalf * bj + 16 * sc + 8 * bi;
+#pragma unroll
+        for (int h = 0; h < NG; ++h) a[h] = lds_f64(sb + h * kBlkBytes);
         ++pp.q;
       }
       // block Crout updates: A_pt -= L_pm U_mt, lane owns (i, j); two
       // interleaved accumulator pairs keep four independent FMA chains
-      double a3 = 0.0, a4 = 0.0;
+      // one pipeline stage at a time: its elements are contiguous in the ring,
+      // so every address below is a base plus an immediate
       for (int q = 0; q < cnt;) {
         pp.ensure(pp.q);
-        const int nb = min(cnt - q, pp.ready_upto - pp.q);
-        int k = 0;
-        for (; k + 1 < nb; k += 2) {
-          const int e = pp.q + k;
-          const uint32_t w0 = pp.word(e), w1 = pp.word(e + 1);
-          const double2 l0 = lds_f64x2(lbuf + (w0 >> 22) * kBlkBytes + offL);
-          const double2 l1 = lds_f64x2(lbuf + (w1 >> 22) * kBlkBytes + offL);
-          const double2 u0 = lds_f64x2(pp.slot_base(e) + offU);
-          const double2 u1 = lds_f64x2(pp.slot_base(e + 1) + offU);
-          a = fma(-l0.x, u0.x, a);
-          a2 = fma(-l0.y, u0.y, a2);
-          a3 = fma(-l1.x, u1.x, a3);
-          a4 = fma(-l1.y, u1.y, a4);
+        const int nb = min(cnt - q, ((pp.q | (CH - 1)) + 1) - pp.q);
+        const uint32_t ub = pp.slot_base(pp.q) + offU;
+        const uint32_t wb = pp.wring + ((uint32_t)pp.q % (uint32_t)P::kRingN) * 4;
+#ifndef ACPF_EXP_NOCOMPUTE
+#pragma unroll
+        for (int k = 0; k < CH; k += 2) {
+          if (k < nb) {
+            const uint32_t la0 = lrow + lds_u32(wb + 4 * k);
+            const bool two = k + 1 < nb;
+            const uint32_t la1 = two ? lrow + lds_u32(wb + 4 * k + 4) : 0u;
+#pragma unroll
+            for (int h = 0; h < NG; ++h) {
+              const double2 l0 = lds_f64x2(la0 + h * kBlkBytes);
+              const double2 u0 = lds_f64x2(ub + k * kSlot + h * kBlkBytes);
+              a[h] = fma(-l0.x, u0.x, a[h]);
+              a2[h] = fma(-l0.y, u0.y, a2[h]);
+              if (two) {
+                const double2 l1 = lds_f64x2(la1 + h * kBlkBytes);
+                const double2 u1 = lds_f64x2(ub + (k + 1) * kSlot + h * kBlkBytes);
+                a3[h] = fma(-l1.x, u1.x, a3[h]);
+                a4[h] = fma(-l1.y, u1.y, a4[h]);
+              }
+            }
+          }
         }
-        if (k < nb) {
-          const int e = pp.q + k;
-          const double2 l0 = lds_f64x2(lbuf + (pp.word(e) >> 22) * kBlkBytes + offL);
-          const double2 u0 = lds_f64x2(pp.slot_base(e) + offU);
-          a = fma(-l0.x, u0.x, a);
-          a2 = fma(-l0.y, u0.y, a2);
-        }
+#endif
         pp.q += nb;
         q += nb;
       }
-      a = (a + a3) + (a2 + a4);
+#pragma unroll
+      for (int h = 0; h < NG; ++h) a[h] = (a[h] + a3[h]) + (a2[h] + a4[h]);
       if (info & kSlotL) {
         pp.ensure(pp.q + 1);
-        const int e = pp.q;
-        // L_pt = A' inv(U_tt); y_p -= L_pt y_t
-        const double o = __shfl_xor_sync(kFull, a, 8);  // entry (i, 1-j)
-        const double ai0 = bj ? o : a, ai1 = bj ? a : o;
-        const double2 iv = lds_f64x2(pp.slot_base(e) + offU);  // inv[0][j], inv[1][j]
-        const double l = ai0 * iv.x + ai1 * iv.y;
-        sts_f64(lbuf + (t - t0) * kBlkBytes + (4 * sc + 2 * bi + bj) * 8, l);
-        const double lo = __shfl_xor_sync(kFull, l, 8);
-        const double li0 = bj ? lo : l, li1 = bj ? l : lo;
-        const double2 yt = lds_f64x2(pp.slot_base(e + 1) + 4 * sc * 8);
-        yacc = fma(-li1, yt.y, fma(-li0, yt.x, yacc));
+        const uint32_t ib = pp.slot_base(pp.q) + offU, yb = pp.slot_base(pp.q + 1) + 16 * sc;
+        const uint32_t lb = lbuf + (t - t0) * kSlot + offL + 8 * bj;
+#pragma unroll
+        for (int h = 0; h < NG; ++h) {
+          // L_pt = A' inv(U_tt); y_p -= L_pt y_t
+          const double o = __shfl_xor_sync(kFull, a[h], 8);  // entry (i, 1-j)
+          const double ai0 = bj ? o : a[h], ai1 = bj ? a[h] : o;
+          const double2 iv = lds_f64x2(ib + h * kBlkBytes);  // inv[0][j], inv[1][j]
+          const double l = ai0 * iv.x + ai1 * iv.y;
+          sts_f64(lb + h * kBlkBytes, l);
+          const double lo = __shfl_xor_sync(kFull, l, 8);
+          const double li0 = bj ? lo : l, li1 = bj ? l : lo;
+          const double2 yt = lds_f64x2(yb + h * kBlkBytes);
+          yacc[h] = fma(-li1, yt.y, fma(-li0, yt.x, yacc[h]));
+        }
         pp.q += 2;
       } else {
-        if (info & kSlotDiag) {
-          const double a00 = __shfl_sync(kFull, a, sc), a01 = __shfl_sync(kFull, a, 8 + sc);
-          const double a10 = __shfl_sync(kFull, a, 16 + sc), a11 = __shfl_sync(kFull, a, 24 + sc);
-          const double det = a00 * a11 - a01 * a10;
-          zero |= det == 0.0;
-          const double rd = 1.0 / det;
-          const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
-          BL(gb.b, m.off_invd + p, ce) = inv;
+        const int64_t st = m.off_lu + __shfl_sync(kFull, wstore, t - tw);
+#pragma unroll
+        for (int h = 0; h < NG; ++h) {
+          double* const gb = gb0 + h * gstride;
+          if (info & kSlotDiag) {
+            const double a00 = __shfl_sync(kFull, a[h], sc), a01 = __shfl_sync(kFull, a[h], 8 + sc);
+            const double a10 = __shfl_sync(kFull, a[h], 16 + sc), a11 = __shfl_sync(kFull, a[h], 24 + sc);
+            const double det = a00 * a11 - a01 * a10;
+            zero |= (det == 0.0 ? 1u : 0u) << h;
+            const double rd = 1.0 / det;
+            const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
+            if ((live >> h) & 1u) BL(gb, m.off_invd + p, ce) = inv;
+          }
+          if ((live >> h) & 1u) BL(gb, st, ce) = a[h];
         }
-        BL(gb.b, m.off_lu + t, ce) = a;
       }
       if (info & kSlotRowEnd) {
         ++t;
         break;
       }
     }
-    if (bj == 0) BL(gb.b, m.off_yx + p, bi) = yacc;
+    if (bj == 0) {
+#pragma unroll
+      for (int h = 0; h < NG; ++h)
+        if ((live >> h) & 1u) BL(gb0 + h * gstride, m.off_yx + p, bi) = yacc[h];
+    }
     __syncwarp();  // lbuf of this row complete before the next row of the task reuses it
   }
   pp.finish();
-  if (zero && r == 0) atomicOr(&w.flags[g * kGroup + sc], 8);
+  zero &= live;
+  if (zero && r == 0) {
+#pragma unroll
+    for (int h = 0; h < NG; ++h)
+      if ((zero >> h) & 1u) atomicOr(&w.flags[(g0 + h) * kGroup + sc], 8);
+  }
 }
 
-// One back-substitution level: task = (run of back rows of the level, group).
-__global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int task0) {
+// One back-substitution level: task = (run of back rows of the level, unit of NG groups).
+template <int NG, int CH, int NBUF>
+__global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units) {
+  using P = Pipe<NG, CH, NBUF>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
-  const int64_t g = task % w.groups;
-  const int tk = task0 + (int)(task / w.groups);
-  if (!w.gactive[g]) return;
-  const GroupBase gb = group_base(m, w, g, sc);
-  const uint32_t ring = su32(smem);
+  const int64_t g0 = (task % units) * NG;
+  const int tk = task0 + (int)(task / units);
+  const unsigned live = unit_live<NG>(w, g0);
+  if (!live) return;
+  const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
+  double* const gb0 = w.arena + (size_t)g0 * gstride + 2 * sc;
   const int r0 = m.btask_row[tk], r1 = m.btask_row[tk + 1];
-  Pipe pp;
-  pp.blocks = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup);
-  pp.ring = ring;
-  pp.wring = ring + kRing * kBlkBytes;
-  pp.lane = lane;
+  P pp;
+  pipe_setup(pp, m, w, g0, live, su32(smem), lane);
   pp.begin(m.stream, m.brow_sptr[r0], m.brow_sptr[r1]);
   // back-row words of the task (lane j holds row rw + j), double buffered
   int rw = r0;
   uint32_t wrow = r0 + lane < r1 ? m.brow[r0 + lane] : 0u;
   uint32_t nrow = r0 + 32 + lane < r1 ? m.brow[r0 + 32 + lane] : 0u;
+  const uint32_t offY = 16 * sc + 8 * bi, offI = 16 * sc + 8 * bi;  // y[i]; inv[i][0] (+kHalf: inv[i][1])
+  const uint32_t offUp = kHalf * bj + 16 * sc + 8 * bi, offX = 16 * sc + 8 * bj;
   for (int rr = r0; rr < r1; ++rr) {
     if (rr - rw == 32) {
       rw += 32;
@@ -525,27 +611,52 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
     const int p = (int)(b & 0xfffffu);
     const int cnt = (int)(b >> 20);
     pp.ensure(pp.q + 1);
-    const double yi = lds_f64(pp.addr(pp.q, bi, sc));
-    const double inv0 = lds_f64(pp.addr(pp.q + 1, bi, sc));
-    const double inv1 = lds_f64(pp.addr(pp.q + 1, 2 + bi, sc));
+    double yi[NG], inv0[NG], inv1[NG], part[NG], part2[NG];
+    {
+      const uint32_t yb = pp.slot_base(pp.q) + offY, ib = pp.slot_base(pp.q + 1) + offI;
+#pragma unroll
+      for (int h = 0; h < NG; ++h) {
+        yi[h] = lds_f64(yb + h * kBlkBytes);
+        inv0[h] = lds_f64(ib + h * kBlkBytes);
+        inv1[h] = lds_f64(ib + h * kBlkBytes + kHalf);
+        part[h] = part2[h] = 0.0;  // sum_c U_pc[i][j] x_c[j]
+      }
+    }
     pp.q += 2;
-    double part = 0.0;  // sum_c U_pc[i][j] x_c[j]
     for (int q = 0; q < cnt;) {
       pp.ensure(pp.q + 1);
       const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
-      for (int k = 0; k < nb; ++k) {
+      int k = 0;
+      for (; k + 1 < nb; k += 2) {
         const int e = pp.q + 2 * k;
-        part = fma(lds_f64(pp.addr(e, 2 * bj + bi, sc)), lds_f64(pp.addr(e + 1, bj, sc)), part);
+        const uint32_t u0 = pp.slot_base(e) + offUp, x0 = pp.slot_base(e + 1) + offX;
+        const uint32_t u1 = pp.slot_base(e + 2) + offUp, x1 = pp.slot_base(e + 3) + offX;
+#pragma unroll
+        for (int h = 0; h < NG; ++h) {
+          part[h] = fma(lds_f64(u0 + h * kBlkBytes), lds_f64(x0 + h * kBlkBytes), part[h]);
+          part2[h] = fma(lds_f64(u1 + h * kBlkBytes), lds_f64(x1 + h * kBlkBytes), part2[h]);
+        }
+      }
+      if (k < nb) {
+        const int e = pp.q + 2 * k;
+        const uint32_t u0 = pp.slot_base(e) + offUp, x0 = pp.slot_base(e + 1) + offX;
+#pragma unroll
+        for (int h = 0; h < NG; ++h)
+          part[h] = fma(lds_f64(u0 + h * kBlkBytes), lds_f64(x0 + h * kBlkBytes), part[h]);
       }
       pp.q += 2 * nb;
       q += nb;
     }
-    const double po = __shfl_xor_sync(kFull, part, 8);
-    const double acc = yi - (bj ? po + part : part + po);  // (y_p - sum)[i]
-    const double ao = __shfl_xor_sync(kFull, acc, 16);     // the other row
-    const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
-    const double x = inv0 * acc0 + inv1 * acc1;            // x_p[i]
-    if (bj == 0) BL(gb.b, m.off_yx + p, bi) = x;
+#pragma unroll
+    for (int h = 0; h < NG; ++h) {
+      const double pt = part[h] + part2[h];
+      const double po = __shfl_xor_sync(kFull, pt, 8);
+      const double acc = yi[h] - (bj ? po + pt : pt + po);  // (y_p - sum)[i]
+      const double ao = __shfl_xor_sync(kFull, acc, 16);    // the other row
+      const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
+      const double x = inv0[h] * acc0 + inv1[h] * acc1;     // x_p[i]
+      if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = x;
+    }
   }
   pp.finish();
 }
@@ -605,19 +716,59 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
-size_t pipe_smem() { return (size_t)kRing * (kBlkBytes + 4); }
+// pipeline variants: (groups per warp, elements per stage, stages)
+using P1 = Pipe<1, 8, 8>;
+using P2s = Pipe<2, 4, 8>;
+using P2 = Pipe<2, 8, 8>;
+
+size_t variant_pipe_smem(int v) {
+  return v == 0 ? P1::smem_bytes() : (v == 1 ? P2s::smem_bytes() : P2::smem_bytes());
+}
+
+int variant_ng(int v) { return v == 0 ? 1 : 2; }
 
 }  // namespace
 
-size_t nr_smem_bytes(int cap) { return pipe_smem() + (size_t)cap * kBlkBytes; }
+size_t nr_smem_bytes(int variant, int cap) {
+  return variant_pipe_smem(variant) + (size_t)cap * variant_ng(variant) * kBlkBytes;
+}
 
 size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
+
+namespace {
+
+template <int NG, int CH, int NBUF>
+cudaError_t launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
+                          int64_t groups, cudaStream_t stream) {
+  using P = Pipe<NG, CH, NBUF>;
+  static_assert(NG == 1 || NG == 2, "unit of 1 or 2 groups");
+  const int64_t units = (groups + NG - 1) / NG;
+  for (int l = 0; l < hs.n_levels; ++l) {
+    const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
+    nr_factor_kernel<NG, CH, NBUF><<<(unsigned)(units * nt), 32,
+                                     P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(m, w, k0, units);
+  }
+  for (int l = 0; l < hs.n_blevels; ++l) {
+    const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
+    nr_back_kernel<NG, CH, NBUF><<<(unsigned)(units * nt), 32, P::smem_bytes(), stream>>>(m, w, k0, units);
+  }
+  return cudaSuccess;
+}
+
+template <int NG, int CH, int NBUF>
+cudaError_t set_factor_smem(const NrHostSchedule& hs) {
+  using P = Pipe<NG, CH, NBUF>;
+  return cudaFuncSetAttribute(nr_factor_kernel<NG, CH, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(P::smem_bytes() + (size_t)hs.max_l * P::kSlot));
+}
+
+}  // namespace
 
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
                              int* launches) {
-  cudaError_t e = cudaFuncSetAttribute(nr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)nr_smem_bytes(hs.max_l));
+  const int v = hs.variant;
+  cudaError_t e = v == 0 ? set_factor_smem<1, 8, 8>(hs) : (v == 1 ? set_factor_smem<2, 4, 8>(hs) : set_factor_smem<2, 8, 8>(hs));
   if (e != cudaSuccess) return e;
   const int64_t groups = (io.batch + kGroup - 1) / kGroup;
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
@@ -638,14 +789,12 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
-    for (int l = 0; l < hs.n_levels; ++l) {
-      const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
-      nr_factor_kernel<<<(unsigned)(groups * nt), 32, nr_smem_bytes(hs.level_maxl[l]), stream>>>(m, w, k0);
-    }
-    for (int l = 0; l < hs.n_blevels; ++l) {
-      const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
-      nr_back_kernel<<<(unsigned)(groups * nt), 32, pipe_smem(), stream>>>(m, w, k0);
-    }
+    if (v == 0)
+      launch_levels<1, 8, 8>(m, hs, w, groups, stream);
+    else if (v == 1)
+      launch_levels<2, 4, 8>(m, hs, w, groups, stream);
+    else
+      launch_levels<2, 8, 8>(m, hs, w, groups, stream);
     nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
     nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);
     nl += hs.n_levels + hs.n_blevels + 2;

@@ -266,7 +266,8 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
 }
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
-                       const double* y_re, const double* y_im, NrSchedule& o, int task_elems) {
+                       const double* y_re, const double* y_im, NrSchedule& o, int task_elems,
+                       bool column_store) {
   const int nr = s.n_j, nb = s.n_bus;
   if (s.n_q != 0) throw std::logic_error("block schedule expects a bus-level symbolic analysis");
   // ---- arena layout
@@ -285,6 +286,24 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   o.max_l = 0;
   for (int p = 0; p < nr; ++p) o.max_l = std::max<int>(o.max_l, (int)(s.diag[p] - s.rowptr[p]));
   if (o.max_l >= 1024) throw std::length_error("L row longer than 1023 blocks");
+
+  // ---- storage positions of the LU slots
+  o.slot_store.assign(s.nnz_lu, 0);
+  if (column_store) {
+    std::vector<int64_t> ccount(nr + 1, 0);
+    for (int p = 0; p < nr; ++p)
+      for (int64_t t = s.diag[p]; t < s.rowptr[p + 1]; ++t) ++ccount[s.col[t] + 1];
+    for (int c = 0; c < nr; ++c) ccount[c + 1] += ccount[c];
+    int64_t nl = ccount[nr];
+    for (int p = 0; p < nr; ++p) {  // rows ascending: each column's rows come out sorted
+      for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) o.slot_store[t] = (int32_t)nl++;
+      for (int64_t t = s.diag[p]; t < s.rowptr[p + 1]; ++t)
+        o.slot_store[t] = (int32_t)ccount[s.col[t]]++;
+    }
+  } else {
+    for (int64_t t = 0; t < s.nnz_lu; ++t) o.slot_store[t] = (int32_t)t;
+  }
+  const std::vector<int32_t>& st = o.slot_store;
 
   // ---- bus -> block row, and per-bus assembly lists
   o.bus_row.assign(nb, -1);
@@ -305,7 +324,7 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
         if (o.bus_row[j] >= 0) {
           const int64_t t = where[o.bus_row[j]];
           if (t < 0) throw std::logic_error("assembly slot missing");
-          slot = (int32_t)t;
+          slot = st[t];
         }
         o.asm_y.push_back(yr);
         o.asm_y.push_back(yi);
@@ -367,9 +386,9 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
       if (cnt >= 65536) throw std::length_error("too many updates for one slot");
       info |= (uint32_t)cnt << 16;
       o.slot_info[t] = info;
-      if (!fill) gw(o.off_lu + t, 0);
+      if (!fill) gw(o.off_lu + st[t], 0);
       for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
-        gw(o.off_lu + s.pair_u[q], (int)(s.pair_l[q] - r0));
+        gw(o.off_lu + st[s.pair_u[q]], (int)(s.pair_l[q] - r0));
       if (t < s.diag[p]) {
         gw(o.off_invd + s.col[t], 0);
         gw(o.off_yx + s.col[t], 0);
@@ -396,7 +415,7 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     gw(o.off_yx + p, 0);
     gw(o.off_invd + p, 0);
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
-      gw(o.off_lu + t, 0);
+      gw(o.off_lu + st[t], 0);
       gw(o.off_yx + s.col[t], 0);
     }
     o.brow_sptr[r + 1] = (int32_t)o.stream.size();

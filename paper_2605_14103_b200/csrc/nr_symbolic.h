@@ -54,6 +54,11 @@ struct NrSchedule {
   // task k covers rows task_row[k]..task_row[k+1]
   std::vector<int32_t> level_task_ptr, task_row;
   std::vector<uint32_t> slot_info;  // [nnz_lu] flags | cnt << 16
+  // storage position of each slot in the LU block region: U-part slots
+  // (diagonal and right of it) column by column, then the L-part slots row by
+  // row, so the U blocks one Crout target gathers (U_mc, m ascending) sit
+  // next to each other in HBM
+  std::vector<int32_t> slot_store;  // [nnz_lu]
   std::vector<int32_t> row_slot;    // [n_rows+1] = LU rowptr
   std::vector<int32_t> row_sptr;    // [n_rows+1] factor-row stream ranges
   // back substitution: rows in back order brow[r] = p | cnt << 20, grouped by
@@ -74,7 +79,7 @@ constexpr uint32_t kSlotFill = 1u << 9;
 // s: NrSymbolic built on the non-slack buses (n_theta = #non-slack, n_q = 0)
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
                        const double* y_re, const double* y_im, NrSchedule& out,
-                       int task_elems = 512);
+                       int task_elems = 512, bool column_store = true);
 
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);

@@ -67,8 +67,9 @@ def load_library(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    target = Path(path) if path else _LIB_PATH
-    if path is None:
+    override = os.environ.get("ACPF_LIB")  # an alternative build of the same C-ABI
+    target = Path(path) if path else (Path(override) if override else _LIB_PATH)
+    if path is None and not override:
         try:
             from . import _build
             if _build._stale() and Path(_build.NVCC).exists():
