@@ -104,14 +104,17 @@ __device__ __forceinline__ double2 mul_conj(double2 u, double2 a) {
 // NG consecutive scenario groups. A ring slot holds one stream element of all
 // NG groups (NG x 256 B, group h at +256h); CH elements per stage, NBUF
 // stages in the ring.
-template <int NG, int CH, int NBUF>
-struct Pipe {
+template <int NG_, int CH_, int NBUF_>
+struct PipeLdgsts {
+  static constexpr int NG = NG_, CH = CH_, NBUF = NBUF_;
   static constexpr int kSlot = NG * kBlkBytes;
   static constexpr int kRingN = CH * NBUF;
+  static constexpr bool kBulk = false;
   static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
   const uint32_t* stream;
   const double* src;  // this lane's copy source: its group's block region + chunk
   bool cp_ok;         // this lane's group is live (NG = 2: lanes 16-31 copy group 1)
+  int nlive;          // live groups of the unit
   uint32_t ring;      // smem [kRingN] slots
   uint32_t wring;     // smem [kRingN] u32 stream words
   int lane;
@@ -202,6 +205,127 @@ struct Pipe {
     cp_wait<0>();
     __syncwarp();
   }
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// Same pipeline with bulk copies (the TMA engine): each element of a stage is
+// one 256-byte cp.async.bulk issued by one lane, and a stage completes on its
+// own mbarrier (transaction count = the stage's bytes), so issuing a stage
+// costs a handful of instructions instead of one 16-byte LDGSTS per lane and
+// element.
+template <int NG_, int CH_, int NBUF_>
+struct PipeBulk {
+  static constexpr int NG = NG_, CH = CH_, NBUF = NBUF_;
+  static constexpr int kSlot = NG * kBlkBytes;
+  static constexpr int kRingN = CH * NBUF;
+  static constexpr bool kBulk = true;
+  static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
+  static_assert(CH * NG <= 32, "one copy per lane and stage");
+  const uint32_t* stream;
+  const double* src;  // this lane's group block region
+  bool cp_ok;         // this lane's group is live
+  int nlive;          // live groups of the unit
+  uint32_t ring;      // smem [kRingN] slots, then [kRingN] u32 words, then [NBUF] mbarriers
+  uint32_t wring;
+  int lane;
+  int s0, n, issued, ready_upto, q;
+  uint32_t wcur, wnext;
+  int wbase;
+
+  static constexpr size_t kSmem = (size_t)kRingN * (kSlot + 4) + (size_t)NBUF * 8;
+  __host__ __device__ static constexpr size_t smem_bytes() { return kSmem; }
+
+  __device__ __forceinline__ uint32_t bar(int stage) const {
+    return wring + kRingN * 4 + (uint32_t)(stage % NBUF) * 8;
+  }
+
+  __device__ __forceinline__ uint32_t load_window(int base) const {
+    const int k = base + lane;
+    return k < n ? stream[s0 + k] : 0u;
+  }
+
+  __device__ __forceinline__ void issue_stage() {
+    const int c = issued++;
+    const int e0 = c * CH;
+    if (e0 >= n) return;  // past the end: never waited on
+    if (e0 >= wbase + 32) {
+      wbase += 32;
+      wcur = wnext;
+      wnext = load_window(wbase + 32);
+    }
+    const int slot = (c % NBUF) * CH;
+    const int lim = min(CH, n - e0);
+    const int j = NG == 1 ? lane : (lane & 15);
+    const uint32_t mine = __shfl_sync(kFull, wcur, (e0 - wbase + j) & 31);
+    const uint32_t b = bar(c);
+    if (lane < lim) sts_u32(wring + (slot + lane) * 4, (mine >> 22) * (uint32_t)kSlot);
+    if (lane == 0) mbar_expect_tx(b, (uint32_t)(lim * nlive * kBlkBytes));
+    if (j < lim && (NG == 2 || lane < CH) && cp_ok)
+      bulk_g2s(ring + (slot + j) * kSlot + (NG == 1 ? 0 : (lane >> 4) * kBlkBytes),
+               src + (size_t)(mine & 0x3fffffu) * kBlk, kBlkBytes, b);
+  }
+
+  __device__ __forceinline__ void begin(const uint32_t* st, int start, int end) {
+    stream = st;
+    s0 = start;
+    n = end - start;
+    issued = 0;
+    ready_upto = 0;
+    q = 0;
+    wbase = 0;
+    if (lane < NBUF) mbar_init(bar(lane), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+    wcur = load_window(0);
+    wnext = load_window(32);
+#pragma unroll 1
+    for (int k = 0; k < NBUF - 2; ++k) issue_stage();
+  }
+
+  __device__ __forceinline__ void ensure(int e) {
+    while (e >= ready_upto) {
+      const int st = ready_upto / CH;
+      mbar_wait(bar(st), (uint32_t)(st / NBUF) & 1u);
+      __syncwarp();
+      issue_stage();
+      ready_upto += CH;
+    }
+  }
+
+  __device__ __forceinline__ uint32_t slot_base(int e) const {
+    return ring + ((uint32_t)e % (uint32_t)kRingN) * kSlot;
+  }
+
+  __device__ __forceinline__ uint32_t lofs(int e) const {
+    return lds_u32(wring + ((uint32_t)e % (uint32_t)kRingN) * 4);
+  }
+
+  __device__ __forceinline__ void finish() { __syncwarp(); }
 };
 
 // block-region entry `ent` of block element e, scenario sc (B = group block base + 2*sc).
@@ -400,16 +524,18 @@ __device__ __forceinline__ unsigned unit_live(const NrWorkspace& w, int64_t g0) 
   return live;
 }
 
-template <int NG, int CH, int NBUF>
-__device__ __forceinline__ void pipe_setup(Pipe<NG, CH, NBUF>& pp, const NrDeviceModel& m, const NrWorkspace& w,
-                                           int64_t g0, unsigned live, uint32_t ring, int lane) {
+// Point the pipe at the unit's arena (lane's copy source) and the CTA's ring.
+template <class P>
+__device__ __forceinline__ void pipe_setup(P& pp, const NrDeviceModel& m, const NrWorkspace& w, int64_t g0,
+                                           unsigned live, uint32_t ring, int lane) {
   const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
   const int half = lane >> 4, chunk = lane & 15;
-  const int h = NG == 1 ? 0 : half;
-  pp.src = w.arena + (size_t)(g0 + h) * gstride + chunk * 2;
+  const int h = P::NG == 1 ? 0 : half;
+  pp.src = w.arena + (size_t)(g0 + h) * gstride + (P::kBulk ? 0 : chunk * 2);
   pp.cp_ok = (live >> h) & 1u;
+  pp.nlive = __popc(live);
   pp.ring = ring;
-  pp.wring = ring + Pipe<NG, CH, NBUF>::kRingN * Pipe<NG, CH, NBUF>::kSlot;
+  pp.wring = ring + P::kRingN * P::kSlot;
   pp.lane = lane;
 }
 
@@ -417,9 +543,9 @@ __device__ __forceinline__ void pipe_setup(Pipe<NG, CH, NBUF>& pp, const NrDevic
 // scenario groups). Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every
 // block of scenario sc of each group of the unit; the NG groups share every
 // address computation (their copies sit 256 B apart in each ring slot).
-template <int NG, int CH, int NBUF>
+template <class P>
 __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units) {
-  using P = Pipe<NG, CH, NBUF>;
+  constexpr int NG = P::NG, CH = P::CH;
   constexpr int kSlot = P::kSlot;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
@@ -578,9 +704,9 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
 }
 
 // One back-substitution level: task = (run of back rows of the level, unit of NG groups).
-template <int NG, int CH, int NBUF>
+template <class P>
 __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units) {
-  using P = Pipe<NG, CH, NBUF>;
+  constexpr int NG = P::NG;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
@@ -716,50 +842,62 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
-// pipeline variants: (groups per warp, elements per stage, stages)
-using P1 = Pipe<1, 8, 8>;
-using P2s = Pipe<2, 4, 8>;
-using P2 = Pipe<2, 8, 8>;
+// pipeline variants
+using V0 = PipeLdgsts<1, 8, 8>;  // LDGSTS, 1 group per warp
+using V1 = PipeLdgsts<2, 4, 8>;  // LDGSTS, 2 groups per warp
+using V2 = PipeBulk<1, 8, 8>;    // bulk copies, 1 group per warp
+using V3 = PipeBulk<1, 4, 16>;   // bulk copies, finer stages
+using V4 = PipeBulk<2, 4, 8>;    // bulk copies, 2 groups per warp
+using V5 = PipeLdgsts<1, 4, 8>;  // LDGSTS, half-size ring (more resident warps)
+using V6 = PipeLdgsts<1, 4, 16>; // LDGSTS, finer stages, same ring
+using V7 = PipeLdgsts<1, 8, 4>;  // LDGSTS, half-size ring, 2 stages in flight
+using V8 = PipeLdgsts<1, 4, 4>;  // LDGSTS, quarter-size ring
+using V9 = PipeLdgsts<1, 2, 8>;  // LDGSTS, quarter-size ring, 2-element stages
+using V10 = PipeLdgsts<2, 4, 4>; // LDGSTS, 2 groups, half-size ring
 
-size_t variant_pipe_smem(int v) {
-  return v == 0 ? P1::smem_bytes() : (v == 1 ? P2s::smem_bytes() : P2::smem_bytes());
+template <class F>
+auto with_variant(int v, F&& f) {
+  switch (v) {
+    case 1: return f(V1{});
+    case 2: return f(V2{});
+    case 3: return f(V3{});
+    case 4: return f(V4{});
+    case 5: return f(V5{});
+    case 6: return f(V6{});
+    case 7: return f(V7{});
+    case 8: return f(V8{});
+    case 9: return f(V9{});
+    case 10: return f(V10{});
+    default: return f(V0{});
+  }
 }
-
-int variant_ng(int v) { return v == 0 ? 1 : 2; }
 
 }  // namespace
 
 size_t nr_smem_bytes(int variant, int cap) {
-  return variant_pipe_smem(variant) + (size_t)cap * variant_ng(variant) * kBlkBytes;
+  return with_variant(variant, [&](auto p) {
+    using P = decltype(p);
+    return P::smem_bytes() + (size_t)cap * P::kSlot;
+  });
 }
 
 size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
 
 namespace {
 
-template <int NG, int CH, int NBUF>
-cudaError_t launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
-                          int64_t groups, cudaStream_t stream) {
-  using P = Pipe<NG, CH, NBUF>;
-  static_assert(NG == 1 || NG == 2, "unit of 1 or 2 groups");
-  const int64_t units = (groups + NG - 1) / NG;
+template <class P>
+void launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t groups,
+                   cudaStream_t stream) {
+  const int64_t units = (groups + P::NG - 1) / P::NG;
   for (int l = 0; l < hs.n_levels; ++l) {
     const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
-    nr_factor_kernel<NG, CH, NBUF><<<(unsigned)(units * nt), 32,
-                                     P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(m, w, k0, units);
+    nr_factor_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(
+        m, w, k0, units);
   }
   for (int l = 0; l < hs.n_blevels; ++l) {
     const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
-    nr_back_kernel<NG, CH, NBUF><<<(unsigned)(units * nt), 32, P::smem_bytes(), stream>>>(m, w, k0, units);
+    nr_back_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes(), stream>>>(m, w, k0, units);
   }
-  return cudaSuccess;
-}
-
-template <int NG, int CH, int NBUF>
-cudaError_t set_factor_smem(const NrHostSchedule& hs) {
-  using P = Pipe<NG, CH, NBUF>;
-  return cudaFuncSetAttribute(nr_factor_kernel<NG, CH, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(P::smem_bytes() + (size_t)hs.max_l * P::kSlot));
 }
 
 }  // namespace
@@ -768,7 +906,11 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
                              int* launches) {
   const int v = hs.variant;
-  cudaError_t e = v == 0 ? set_factor_smem<1, 8, 8>(hs) : (v == 1 ? set_factor_smem<2, 4, 8>(hs) : set_factor_smem<2, 8, 8>(hs));
+  cudaError_t e = with_variant(v, [&](auto p) {
+    using P = decltype(p);
+    return cudaFuncSetAttribute(nr_factor_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(P::smem_bytes() + (size_t)hs.max_l * P::kSlot));
+  });
   if (e != cudaSuccess) return e;
   const int64_t groups = (io.batch + kGroup - 1) / kGroup;
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
@@ -789,12 +931,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
-    if (v == 0)
-      launch_levels<1, 8, 8>(m, hs, w, groups, stream);
-    else if (v == 1)
-      launch_levels<2, 4, 8>(m, hs, w, groups, stream);
-    else
-      launch_levels<2, 8, 8>(m, hs, w, groups, stream);
+    with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, stream); });
     nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
     nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);
     nl += hs.n_levels + hs.n_blevels + 2;
