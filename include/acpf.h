@@ -210,6 +210,48 @@ acpf_status acpf_zbus_scenarios(acpf_zbus_plan_t plan, uint64_t seed, int64_t st
                                 const double* wye_s, const double* delta_s, double* s_wye,
                                 double* s_delta, uint32_t flags, void* cuda_stream);
 
+/* ------------------------------------------------------------------------
+ * On-device certificates. Replace the host certificate
+ * helpers the reference's tests call per scenario.
+ * ------------------------------------------------------------------------ */
+
+/* Attach the branch table of the network to an NR plan (needed by
+ * acpf_nr_certify): per in-service branch its end buses and the four
+ * admittances yff, yft, ytf, ytt (interleaved complex, [n_br][4]) of the
+ * pi model, as branch_flows (transmission.py:453-481) forms them; bus_gs
+ * [n_bus] the bus shunt conductances. Copied to the device. */
+acpf_status acpf_nr_plan_set_branches(acpf_nr_plan_t plan, int32_t n_br, const int32_t* from_bus,
+                                      const int32_t* to_bus, const double* y4, const double* bus_gs);
+
+/* Per scenario of a solved batch (theta, vmag [batch][n_bus]; p_spec
+ * [batch][n_theta]; q_spec [batch][n_q]):
+ *   mismatch_inf  = ||F||inf at the state (mismatch, transmission.py:202-215;
+ *                   NaN if any mismatch is NaN),
+ *   slack_balance = sum over slack buses of P_calc
+ *                   - (-sum p_spec + branch loss + shunt loss)
+ *                   (test_transmission.py:398-416 for every scenario),
+ *   branch_loss   = sum over branches of Re(s_from + s_to).
+ * Any output pointer may be NULL. */
+acpf_status acpf_nr_certify(acpf_nr_plan_t plan, int64_t batch, const double* theta,
+                            const double* vmag, const double* p_spec, const double* q_spec,
+                            double* mismatch_inf, double* slack_balance, double* branch_loss,
+                            uint32_t flags, void* cuda_stream);
+
+/* Attach the reduced network to a Z-Bus plan (needed by
+ * acpf_zbus_kirchhoff): Y_NN in CSR (interleaved complex values, nnz =
+ * rowptr[n]) and inj = Y_NS v_slack [n] (interleaved complex). */
+acpf_status acpf_zbus_plan_set_network(acpf_zbus_plan_t plan, const int32_t* ynn_rowptr,
+                                       const int32_t* ynn_col, const double* ynn_val,
+                                       const double* inj);
+
+/* Kirchhoff residual per scenario (kirchhoff_residual, distribution.py:
+ * 624-630): max_k |(Y_NN v + Y_NS v_slack)_k - i_loads(v)_k| for v
+ * [batch][n] complex; +inf where a load voltage is at the voltage floor
+ * (the reference raises VoltageFloorError there). */
+acpf_status acpf_zbus_kirchhoff(acpf_zbus_plan_t plan, int64_t batch, const double* v,
+                                const double* s_wye, const double* s_delta, double* kcl,
+                                uint32_t flags, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,8 +8,10 @@ Same subcommands, flags and exit-code contract as the reference (cli.py:26-28,
 312-329): 0 ok, 1 input error, 2 numerical non-convergence / verification
 failure. ``--case`` is a file path or a fixture name. Scenarios are generated
 on the device (bitwise the reference generator). ``verify`` checks the GPU
-solution with host certificates (NR: ||F||inf at the returned state; Z-Bus:
-the reference CSV profile within 1e-3, as the reference does).
+solution with certificates computed on the device (NR: ||F||inf and the
+slack power balance at the returned state, acpf_nr_certify; Z-Bus: the
+reference CSV profile within 1e-3, as the reference does, plus the Kirchhoff
+residual, acpf_zbus_kirchhoff).
 """
 
 from __future__ import annotations
@@ -160,12 +162,20 @@ def cmd_verify(args) -> int:
     if kind == "tx":
         tol = args.tol if args.tol is not None else 1e-10
         res = tm.newton_solve(model, opts=tm.NewtonOptions(tol_mismatch=1e-10))
-        f = tm.mismatch(res.state, tm.base_scenario(model.net, model.part), model.y, model.part)
-        fn = float(np.abs(f).max()) if f.size else 0.0
+        sc = tm.base_scenario(model.net, model.part)
+        # certificates computed on the device (acpf_nr_certify)
+        plan = model.plan()
+        plan.set_branches(model.net)
+        cert = plan.certify(res.state.theta[None, :].copy(), res.state.vmag[None, :].copy(),
+                            np.ascontiguousarray(sc.p_spec[None, :]), np.ascontiguousarray(sc.q_spec[None, :]))
+        fn = float(cert["mismatch_inf"][0])
+        bal = float(cert["slack_balance"][0])
         print("quantity                     value")
         print(f"||F||inf at GPU solution     {fn:.3e}  (threshold {tol:.1e})")
+        print(f"slack power balance          {bal:.3e}  (threshold 1.0e-08)")
+        print(f"branch loss (p.u.)           {float(cert['branch_loss'][0]):.6f}")
         print(f"solver converged             {res.converged}")
-        return EXIT_OK if res.converged and fn <= tol else EXIT_NUMERICAL
+        return EXIT_OK if res.converged and fn <= tol and abs(bal) <= 1e-8 else EXIT_NUMERICAL
     ref = args.oracle or str(Path(path).with_suffix("")) + "_reference.csv"
     ref_name = Path(ref).name
     try:
@@ -179,6 +189,11 @@ def cmd_verify(args) -> int:
     except (FileNotFoundError, ValueError) as exc:
         raise CliInputError("reference", f"missing or bad reference fixture: {ref} ({exc})")
     res = dm.zbus_iterate(model)
+    plan = engine.zbus_plan_for(model, 0)
+    plan.set_network(model)
+    sc = dm.base_distribution_scenario(model)
+    kcl = float(plan.kirchhoff(res.v[None, :].copy(), np.ascontiguousarray(sc.wye_s[None, :]),
+                               np.ascontiguousarray(sc.delta_s[None, :]))[0])
     pos = {k: i for i, k in enumerate(model.reduced_ids())}
     missing = [i for i in ids if i not in pos]
     if missing:
@@ -188,6 +203,7 @@ def cmd_verify(args) -> int:
     print("quantity                     value")
     print(f"node-phases compared         {len(ids)}")
     print(f"max |dVmag| vs reference     {dev:.3e}  (threshold {thr:.1e})")
+    print(f"Kirchhoff residual (device)  {kcl:.3e}  (threshold 1.0e-08)")
     print(f"solver converged             {res.converged}")
     return EXIT_OK if res.converged and dev < thr else EXIT_NUMERICAL
 

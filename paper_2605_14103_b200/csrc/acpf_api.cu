@@ -101,6 +101,8 @@ struct acpf_nr_plan {
   void* stage_base = nullptr;
   int* host_active = nullptr;
   std::vector<int32_t> h_tpos, h_qidx;  // host copies for scenario generation
+  NrCertModel cert{};                   // acpf_nr_plan_set_branches (n_br < 0: not set)
+  DevArena cert_arena;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
@@ -109,6 +111,10 @@ struct acpf_nr_plan {
 struct acpf_zbus_plan {
   int device = 0;
   int n_wye = 0, n_delta = 0;
+  std::vector<int32_t> h_wye, h_dp, h_dq;  // reduced rows of the loads (certificates)
+  double floor = 0.0;
+  ZbCertModel cert{};                      // acpf_zbus_plan_set_network (rowptr null: not set)
+  DevArena cert_arena;
   cudaStream_t copy_stream = nullptr;  // host-path H2D/D2H overlap
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_kend[2] = {nullptr, nullptr},
               ev_d2h[2] = {nullptr, nullptr};
@@ -222,6 +228,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.off_spec = sc.off_spec;
   d.off_th = sc.off_th;
   d.off_vm = sc.off_vm;
+  p->cert.n_br = -1;
   p->hs.level_task_ptr = sc.level_task_ptr.data();
   p->hs.level_maxl = sc.level_maxl.data();
   p->hs.blevel_task_ptr = sc.blevel_task_ptr.data();
@@ -560,6 +567,10 @@ acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const 
   }
   p->device = device;
   DeviceGuard dg(device);
+  p->h_wye.assign(wye_idx, wye_idx + n_wye);
+  p->h_dp.assign(delta_p, delta_p + n_delta);
+  p->h_dq.assign(delta_q, delta_q + n_delta);
+  p->floor = voltage_floor;
   p->n_wye = n_wye;
   p->n_delta = n_delta;
   ZbDeviceModel& d = p->dm;
@@ -989,6 +1000,204 @@ acpf_status acpf_zbus_scenarios(acpf_zbus_plan_t p, uint64_t seed, int64_t start
     if (p->n_delta)
       ACPF_CUDA(cudaMemcpyAsync(s_delta, a.s_delta, (size_t)count * p->n_delta * 16, cudaMemcpyDeviceToHost, st));
   }
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  return ACPF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Certificates (kernels in cert_kernel.cu)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// Device views of the caller's arrays: the pointers themselves for
+// ACPF_DEVICE_PTRS, else device copies (inputs uploaded, outputs allocated).
+struct Staged {
+  DevArena a;
+  cudaError_t e = cudaSuccess;
+  bool host;
+  cudaStream_t st;
+  Staged(uint32_t flags, cudaStream_t s) : host(!(flags & ACPF_DEVICE_PTRS)), st(s) {}
+  template <class T>
+  T* in(const T* p, size_t count) {
+    if (!host || !p || e != cudaSuccess) return const_cast<T*>(p);
+    T* d = nullptr;
+    e = a.alloc((void**)&d, count * sizeof(T));
+    if (e == cudaSuccess && count) e = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    return d;
+  }
+  template <class T>
+  T* out(T* p, size_t count) {
+    if (!host || !p || e != cudaSuccess) return p;
+    T* d = nullptr;
+    e = a.alloc((void**)&d, count * sizeof(T));
+    return d;
+  }
+  template <class T>
+  void back(T* host_p, const T* dev_p, size_t count) {
+    if (host && host_p && e == cudaSuccess && count)
+      e = cudaMemcpyAsync(host_p, dev_p, count * sizeof(T), cudaMemcpyDeviceToHost, st);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+acpf_status acpf_nr_plan_set_branches(acpf_nr_plan_t p, int32_t n_br, const int32_t* from_bus,
+                                      const int32_t* to_bus, const double* y4, const double* bus_gs) {
+  if (!p || n_br < 0 || (n_br && (!from_bus || !to_bus || !y4)) || !bus_gs) {
+    set_error("acpf_nr_plan_set_branches: invalid argument");
+    return ACPF_EINVAL;
+  }
+  const int nb = p->dm.n_bus;
+  for (int b = 0; b < n_br; ++b)
+    if (from_bus[b] < 0 || from_bus[b] >= nb || to_bus[b] < 0 || to_bus[b] >= nb) {
+      set_error("acpf_nr_plan_set_branches: branch bus out of range");
+      return ACPF_EINVAL;
+    }
+  if (nr_cert_smem(nb) > 227 * 1024) {
+    set_error("acpf_nr_plan_set_branches: network too large for the certificate kernel");
+    return ACPF_ESTRUCT;
+  }
+  DeviceGuard dg(p->device);
+  p->cert_arena.release();
+  NrCertModel c{};
+  c.n_bus = nb;
+  c.n_theta = p->dm.n_theta;
+  c.n_q = p->dm.n_q;
+  c.n_br = n_br;
+  c.y_rowptr = p->dm.y_rowptr;
+  c.y_col = p->dm.y_col;
+  c.y_val = p->dm.y_val;
+  c.tpos = p->dm.tpos;
+  c.qidx = p->dm.qidx;
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = p->cert_arena.upload(dst, src, cnt);
+  };
+  up(const_cast<int32_t**>(&c.br_f), from_bus, (size_t)n_br);
+  up(const_cast<int32_t**>(&c.br_t), to_bus, (size_t)n_br);
+  up(const_cast<double2**>(&c.br_y), reinterpret_cast<const double2*>(y4), (size_t)n_br * 4);
+  up(const_cast<double**>(&c.gs), bus_gs, (size_t)nb);
+  ACPF_CUDA(e);
+  p->cert = c;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_certify(acpf_nr_plan_t p, int64_t batch, const double* theta, const double* vmag,
+                            const double* p_spec, const double* q_spec, double* mismatch_inf,
+                            double* slack_balance, double* branch_loss, uint32_t flags, void* cuda_stream) {
+  if (!p || batch < 0 || flags > 1u || (batch && (!theta || !vmag)) ||
+      (batch && p->dm.n_theta && !p_spec) || (batch && p->dm.n_q && !q_spec)) {
+    set_error("acpf_nr_certify: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (p->cert.n_br < 0) {
+    set_error("acpf_nr_certify: call acpf_nr_plan_set_branches first");
+    return ACPF_EINVAL;
+  }
+  if (batch == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t nb = p->dm.n_bus, nt = p->dm.n_theta, nq = p->dm.n_q, B = (size_t)batch;
+  Staged g(flags, st);
+  NrCertIO io{};
+  io.batch = batch;
+  io.theta = g.in(theta, B * nb);
+  io.vmag = g.in(vmag, B * nb);
+  io.p_spec = g.in(p_spec, B * nt);
+  io.q_spec = g.in(q_spec, B * nq);
+  io.mismatch_inf = g.out(mismatch_inf, B);
+  io.slack_balance = g.out(slack_balance, B);
+  io.branch_loss = g.out(branch_loss, B);
+  ACPF_CUDA(g.e);
+  ACPF_CUDA(launch_nr_cert(p->cert, io, st));
+  g.back(mismatch_inf, io.mismatch_inf, B);
+  g.back(slack_balance, io.slack_balance, B);
+  g.back(branch_loss, io.branch_loss, B);
+  ACPF_CUDA(g.e);
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_plan_set_network(acpf_zbus_plan_t p, const int32_t* ynn_rowptr, const int32_t* ynn_col,
+                                       const double* ynn_val, const double* inj) {
+  if (!p || !ynn_rowptr || !inj) {
+    set_error("acpf_zbus_plan_set_network: invalid argument");
+    return ACPF_EINVAL;
+  }
+  const int n = p->dm.n;
+  const int64_t nnz = ynn_rowptr[n];
+  if (ynn_rowptr[0] != 0 || nnz < 0 || (nnz && (!ynn_col || !ynn_val))) {
+    set_error("acpf_zbus_plan_set_network: bad CSR");
+    return ACPF_EINVAL;
+  }
+  for (int k = 0; k < n; ++k)
+    if (ynn_rowptr[k + 1] < ynn_rowptr[k]) {
+      set_error("acpf_zbus_plan_set_network: bad CSR row pointers");
+      return ACPF_EINVAL;
+    }
+  for (int64_t e = 0; e < nnz; ++e)
+    if (ynn_col[e] < 0 || ynn_col[e] >= n) {
+      set_error("acpf_zbus_plan_set_network: column out of range");
+      return ACPF_EINVAL;
+    }
+  if (zb_cert_smem(n) > 227 * 1024) {
+    set_error("acpf_zbus_plan_set_network: feeder too large for the certificate kernel");
+    return ACPF_ESTRUCT;
+  }
+  DeviceGuard dg(p->device);
+  p->cert_arena.release();
+  ZbCertModel c{};
+  c.n = n;
+  c.n_wye = p->n_wye;
+  c.n_delta = p->n_delta;
+  c.floor = p->floor;
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = p->cert_arena.upload(dst, src, cnt);
+  };
+  up(const_cast<int32_t**>(&c.rowptr), ynn_rowptr, (size_t)n + 1);
+  up(const_cast<int32_t**>(&c.col), ynn_col, (size_t)nnz);
+  up(const_cast<double2**>(&c.val), reinterpret_cast<const double2*>(ynn_val), (size_t)nnz);
+  up(const_cast<double2**>(&c.inj), reinterpret_cast<const double2*>(inj), (size_t)n);
+  up(const_cast<int32_t**>(&c.wye_row), p->h_wye.data(), p->h_wye.size());
+  up(const_cast<int32_t**>(&c.dp_row), p->h_dp.data(), p->h_dp.size());
+  up(const_cast<int32_t**>(&c.dq_row), p->h_dq.data(), p->h_dq.size());
+  ACPF_CUDA(e);
+  p->cert = c;
+  return ACPF_OK;
+}
+
+acpf_status acpf_zbus_kirchhoff(acpf_zbus_plan_t p, int64_t batch, const double* v, const double* s_wye,
+                                const double* s_delta, double* kcl, uint32_t flags, void* cuda_stream) {
+  if (!p || batch < 0 || flags > 1u || (batch && (!v || !kcl)) || (batch && p->n_wye && !s_wye) ||
+      (batch && p->n_delta && !s_delta)) {
+    set_error("acpf_zbus_kirchhoff: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (!p->cert.rowptr) {
+    set_error("acpf_zbus_kirchhoff: call acpf_zbus_plan_set_network first");
+    return ACPF_EINVAL;
+  }
+  if (batch == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t B = (size_t)batch, n = p->dm.n;
+  Staged g(flags, st);
+  ZbCertIO io{};
+  io.batch = batch;
+  io.v = g.in(reinterpret_cast<const double2*>(v), B * n);
+  io.s_wye = g.in(reinterpret_cast<const double2*>(s_wye), B * p->n_wye);
+  io.s_delta = g.in(reinterpret_cast<const double2*>(s_delta), B * p->n_delta);
+  io.kcl = g.out(kcl, B);
+  ACPF_CUDA(g.e);
+  ACPF_CUDA(launch_zb_kcl(p->cert, io, st));
+  g.back(kcl, io.kcl, B);
+  ACPF_CUDA(g.e);
   ACPF_CUDA(cudaStreamSynchronize(st));
   return ACPF_OK;
 }

@@ -166,4 +166,54 @@ cudaError_t launch_philox_multipliers(uint64_t seed, int64_t start, int64_t coun
 cudaError_t launch_nr_scenarios(const NrScenarioArgs& a, cudaStream_t st);
 cudaError_t launch_zb_scenarios(const ZbScenarioArgs& a, cudaStream_t st);
 
+// ---- certificates (cert_kernel.cu)
+struct NrCertModel {
+  int n_bus, n_theta, n_q, n_br;
+  const int32_t* y_rowptr;
+  const int32_t* y_col;
+  const double2* y_val;
+  const int32_t* tpos;   // [n_bus] p_spec index or -1 (slack)
+  const int32_t* qidx;   // [n_bus] q_spec index or -1
+  const int32_t* br_f;   // [n_br] from bus
+  const int32_t* br_t;   // [n_br] to bus
+  const double2* br_y;   // [n_br][4] yff, yft, ytf, ytt
+  const double* gs;      // [n_bus] shunt conductance
+};
+
+struct NrCertIO {
+  int64_t batch;
+  const double* theta;   // [batch][n_bus]
+  const double* vmag;
+  const double* p_spec;  // [batch][n_theta]
+  const double* q_spec;  // [batch][n_q]
+  double* mismatch_inf;  // [batch] (or null)
+  double* slack_balance;
+  double* branch_loss;
+};
+
+struct ZbCertModel {
+  int n, n_wye, n_delta;
+  const int32_t* rowptr;  // Y_NN CSR
+  const int32_t* col;
+  const double2* val;
+  const double2* inj;     // [n] Y_NS v_slack
+  const int32_t* wye_row;
+  const int32_t* dp_row;
+  const int32_t* dq_row;
+  double floor;
+};
+
+struct ZbCertIO {
+  int64_t batch;
+  const double2* v;        // [batch][n]
+  const double2* s_wye;    // [batch][n_wye]
+  const double2* s_delta;  // [batch][n_delta]
+  double* kcl;             // [batch]
+};
+
+size_t nr_cert_smem(int n_bus);
+size_t zb_cert_smem(int n);
+cudaError_t launch_nr_cert(const NrCertModel& m, const NrCertIO& io, cudaStream_t st);
+cudaError_t launch_zb_kcl(const ZbCertModel& m, const ZbCertIO& io, cudaStream_t st);
+
 }  // namespace acpf

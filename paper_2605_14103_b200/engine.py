@@ -32,7 +32,8 @@ EXPORTED = (
     "acpf_nr_solve", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
     "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
-    "acpf_zbus_scenarios",
+    "acpf_zbus_scenarios", "acpf_nr_plan_set_branches", "acpf_nr_certify",
+    "acpf_zbus_plan_set_network", "acpf_zbus_kirchhoff",
 )
 
 
@@ -98,6 +99,10 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_philox_multipliers": (I32, [C.c_uint64, I64, I64, I32, D, P, U32, P]),
         "acpf_nr_scenarios": (I32, [P, C.c_uint64, I64, I64, D, I32, P, P, P, P, P, P, P, U32, P]),
         "acpf_zbus_scenarios": (I32, [P, C.c_uint64, I64, I64, D, I32, P, P, P, P, P, U32, P]),
+        "acpf_nr_plan_set_branches": (I32, [P, I32, P, P, P, P]),
+        "acpf_nr_certify": (I32, [P, I64, P, P, P, P, P, P, P, U32, P]),
+        "acpf_zbus_plan_set_network": (I32, [P, P, P, P, P]),
+        "acpf_zbus_kirchhoff": (I32, [P, I64, P, P, P, P, U32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -185,6 +190,26 @@ def philox_multipliers(seed: int, start: int, count: int, n_elem: int, spread: f
 # ---------------------------------------------------------------------------
 # Newton plans
 # ---------------------------------------------------------------------------
+
+
+def branch_admittances(net):
+    """In-service branches of a TransmissionNetwork as (from, to, y4, bus_gs):
+    y4[k] = (yff, yft, ytf, ytt) of the pi model exactly as branch_flows
+    forms them (reference transmission.py:453-481)."""
+    idx = net.bus_index()
+    f, t, y4 = [], [], []
+    for br in net.branches:
+        if not br.status:
+            continue
+        ys = 1.0 / complex(br.r, br.x)
+        half_b = 0.5j * br.b_ch
+        ratio = br.tap * np.exp(1j * br.shift)
+        f.append(idx[br.from_bus])
+        t.append(idx[br.to_bus])
+        y4.append(((ys + half_b) / (br.tap * br.tap), -ys / np.conj(ratio), -ys / ratio, ys + half_b))
+    gs = np.ascontiguousarray([b.gs for b in net.buses], dtype=np.float64)
+    return (np.ascontiguousarray(f, dtype=np.int32), np.ascontiguousarray(t, dtype=np.int32),
+            np.ascontiguousarray(np.array(y4, dtype=np.complex128).reshape(-1, 4)), gs)
 
 
 class NrPlan:
@@ -275,6 +300,25 @@ class NrPlan:
                                       el.size, _ptr(el), *[_ptr(a) for a in arrs], _ptr(p), _ptr(q),
                                       flags, None))
         return p, q
+
+    def set_branches(self, net) -> None:
+        """Attach the branch table (acpf_nr_plan_set_branches) for certify()."""
+        f, t, y4, gs = branch_admittances(net)
+        _check(_lib.acpf_nr_plan_set_branches(self._h, f.size, _ptr(f), _ptr(t), _ptr(y4), _ptr(gs)))
+        self._branches = True
+
+    def certify(self, theta, vmag, p_spec, q_spec, stream=None) -> dict:
+        """Per-scenario certificates of solved states on the GPU
+        (acpf_nr_certify): mismatch_inf, slack_balance, branch_loss."""
+        dev = _is_device(theta)
+        b = int(theta.shape[0])
+        out = {k: _out_array((b,), np.float64, theta.device if dev else None)
+               for k in ("mismatch_inf", "slack_balance", "branch_loss")}
+        _check(_lib.acpf_nr_certify(
+            self._h, b, _ptr(theta), _ptr(vmag), _ptr(p_spec) if self.n_theta else None,
+            _ptr(q_spec) if self.n_q else None, _ptr(out["mismatch_inf"]), _ptr(out["slack_balance"]),
+            _ptr(out["branch_loss"]), ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS, _stream_ptr(stream)))
+        return out
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:
@@ -375,6 +419,30 @@ class ZbusPlan:
                                         _ptr(sw) if self.n_wye else None,
                                         _ptr(sd) if self.n_delta else None, flags, None))
         return sw, sd
+
+    def set_network(self, model) -> None:
+        """Attach Y_NN and Y_NS v_slack (acpf_zbus_plan_set_network) for kirchhoff()."""
+        y = model.y_nn.tocsr()
+        y.sort_indices()
+        rp = np.ascontiguousarray(y.indptr, dtype=np.int32)
+        col = np.ascontiguousarray(y.indices, dtype=np.int32)
+        val = np.ascontiguousarray(y.data, dtype=np.complex128)
+        inj = np.ascontiguousarray(model.y_ns @ model.v_slack, dtype=np.complex128)
+        _check(_lib.acpf_zbus_plan_set_network(self._h, _ptr(rp), _ptr(col) if col.size else None,
+                                               _ptr(val) if val.size else None, _ptr(inj)))
+        self._network = True
+
+    def kirchhoff(self, v, s_wye, s_delta, stream=None):
+        """max_k |Y_NN v + Y_NS v_s - i_loads(v)| per scenario (acpf_zbus_kirchhoff);
+        inf where a load voltage is at the floor."""
+        dev = _is_device(v)
+        b = int(v.shape[0])
+        out = _out_array((b,), np.float64, v.device if dev else None)
+        _check(_lib.acpf_zbus_kirchhoff(
+            self._h, b, _ptr(v), _ptr(s_wye) if self.n_wye else None,
+            _ptr(s_delta) if self.n_delta else None, _ptr(out),
+            ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS, _stream_ptr(stream)))
+        return out
 
     def close(self) -> None:
         if getattr(self, "_h", None) and _lib is not None:

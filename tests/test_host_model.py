@@ -126,3 +126,23 @@ def test_distribution_schema_errors():
     net = load_distribution("ieee13")
     again = pf.parse_distribution_json(pf.distribution_to_json(net))
     assert again.buses == net.buses and again.loads == net.loads
+
+
+def test_branch_admittances_reproduce_branch_flows():
+    # the table acpf_nr_plan_set_branches uploads gives the same flows as the
+    # host branch_flows (reference transmission.py:453-481) at a random state
+    from paper_2605_14103_b200 import engine
+    from paper_2605_14103_b200 import transmission as tm
+    net = load_transmission("case118")
+    rng = np.random.default_rng(7)
+    n = len(net.buses)
+    st = tm.PolarState(rng.normal(0, 0.1, n), 1.0 + rng.normal(0, 0.02, n))
+    f, t, y4, gs = engine.branch_admittances(net)
+    u = st.vmag * np.exp(1j * st.theta)
+    sf = u[f] * np.conj(y4[:, 0] * u[f] + y4[:, 1] * u[t])
+    s_t = u[t] * np.conj(y4[:, 2] * u[f] + y4[:, 3] * u[t])
+    hf, ht = tm.branch_flows(net, st)
+    live = np.array([bool(b.status) for b in net.branches])
+    np.testing.assert_allclose(sf, hf[live], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(s_t, ht[live], rtol=0, atol=1e-13)
+    assert gs.shape == (n,)
