@@ -405,52 +405,56 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
   const GroupBase gb = group_base(m, w, g, sc);
+  // the scalar region is read-only here (only block elements are written), so
+  // gathers go through the non-coherent path
+  const double* __restrict__ su = gb.s + m.off_u * kGroup;  // u_j: su[2j*8], su[(2j+1)*8]
+  const double* __restrict__ se = gb.s + m.off_e * kGroup;
+  double* __restrict__ blk = gb.b;
+  auto ld2 = [](const double* __restrict__ base, int j) {
+    return make_double2(__ldg(base + (size_t)(2 * j) * kGroup), __ldg(base + (size_t)(2 * j + 1) * kGroup));
+  };
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
   for (int i = i0 + r; i < i1; i += 4) {
-    const int p = m.bus_row[i];
+    const int p = __ldg(m.bus_row + i);
     if (p < 0) continue;  // slack: no equations
     double2 acc = make_double2(0.0, 0.0);
-    const int e1 = m.y_rowptr[i + 1];
-    for (int e = m.y_rowptr[i]; e < e1; ++e) {
-      const double2 y = m.y_val[e];
-      const int c = m.y_col[e];
-      const double ur = SL(gb.s, m.off_u + 2 * c), ui = SL(gb.s, m.off_u + 2 * c + 1);
-      acc.x += y.x * ur - y.y * ui;
-      acc.y += y.x * ui + y.y * ur;
+    const int e1 = __ldg(m.y_rowptr + i + 1);
+    for (int e = __ldg(m.y_rowptr + i); e < e1; ++e) {
+      const double2 y = __ldg(m.y_val + e);
+      const double2 uj = ld2(su, __ldg(m.y_col + e));
+      acc.x += y.x * uj.x - y.y * uj.y;
+      acc.y += y.x * uj.y + y.y * uj.x;
     }
-    const double2 u = make_double2(SL(gb.s, m.off_u + 2 * i), SL(gb.s, m.off_u + 2 * i + 1));
+    const double2 u = ld2(su, i);
     const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
-    const bool pq = m.qidx[i] >= 0;
-    const double fp = sv.x - SL(gb.s, m.off_spec + 2 * p);
+    const bool pq = __ldg(m.qidx + i) >= 0;
+    const double fp = sv.x - __ldg(gb.s + (m.off_spec + 2 * p) * kGroup);
     bad |= isnan(fp) ? 1 : (isinf(fp) ? 2 : 0);
     fmx = fmx < fabs(fp) ? fabs(fp) : fmx;
-    BL(gb.b, m.off_yx + p, 0) = -fp;
     double fq = 0.0;
     if (pq) {
-      fq = sv.y - SL(gb.s, m.off_spec + 2 * p + 1);
+      fq = sv.y - __ldg(gb.s + (m.off_spec + 2 * p + 1) * kGroup);
       bad |= isnan(fq) ? 1 : (isinf(fq) ? 2 : 0);
       fmx = fmx < fabs(fq) ? fabs(fq) : fmx;
     }
-    BL(gb.b, m.off_yx + p, 1) = -fq;
+    *reinterpret_cast<double2*>(&BL(blk, m.off_yx + p, 0)) = make_double2(-fp, -fq);
     // 2x2 Jacobian block of every Ybus entry (i, j) into its LU slot:
     //   dS_i/dth_j = -j u_i conj(y u_j)  (j != i);  dS_i/dth_i = j u_i conj(I_i - y u_i)
     //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
     //   [[H, N], [M, L]] = [[Re dS/dth, Re dS/dV], [Im dS/dth, Im dS/dV]]
     // with the PV padding rows/columns of the identity equation dV = 0.
-    const double2 ei = make_double2(SL(gb.s, m.off_e + 2 * i), SL(gb.s, m.off_e + 2 * i + 1));
-    const int a1 = m.asm_ptr[i + 1];
-    for (int a = m.asm_ptr[i]; a < a1; ++a) {
-      const int slot = m.asm_slot[a];
+    const double2 ei = ld2(se, i);
+    const int a0 = __ldg(m.asm_ptr + i), a1 = __ldg(m.asm_ptr + i + 1);
+    for (int a = a0; a < a1; ++a) {
+      const int slot = __ldg(m.asm_slot + a);
       if (slot < 0) continue;  // slack column
-      const double2 y = m.asm_y[a];
-      const int jb = m.asm_j[a];
-      const double2 ej = make_double2(SL(gb.s, m.off_e + 2 * jb), SL(gb.s, m.off_e + 2 * jb + 1));
-      const double2 wv = mul_conj(u, cmul(y, ej));
+      const double2 y = __ldg(m.asm_y + a);
+      const int jb = __ldg(m.asm_j + a);
+      const double2 wv = mul_conj(u, cmul(y, ld2(se, jb)));
       double2 dth, dv;
       if (jb != i) {
-        const double2 uj = make_double2(SL(gb.s, m.off_u + 2 * jb), SL(gb.s, m.off_u + 2 * jb + 1));
-        const double2 wt = mul_conj(u, cmul(y, uj));
+        const double2 wt = mul_conj(u, cmul(y, ld2(su, jb)));
         dth = make_double2(wt.y, -wt.x);
         dv = wv;
       } else {
@@ -459,12 +463,12 @@ __global__ void nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
         dth = make_double2(-wt.y, wt.x);
         dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
       }
-      const bool pqj = m.qidx[jb] >= 0;
-      // column-major [[H, N], [M, L]]: H (0,0)->0, M (1,0)->1, N (0,1)->2, L (1,1)->3
-      BL(gb.b, m.off_lu + slot, 0) = dth.x;
-      BL(gb.b, m.off_lu + slot, 1) = pq ? dth.y : 0.0;
-      BL(gb.b, m.off_lu + slot, 2) = pqj ? dv.x : 0.0;
-      BL(gb.b, m.off_lu + slot, 3) = (pq && pqj) ? dv.y : (jb == i ? 1.0 : 0.0);
+      const bool pqj = __ldg(m.qidx + jb) >= 0;
+      // column-major [[H, N], [M, L]]: H (0,0)->0, M (1,0)->1, N (0,1)->2, L (1,1)->3;
+      // one 16-byte store per block column (entries (0, j), (1, j) are adjacent)
+      double2* const col = reinterpret_cast<double2*>(&BL(blk, m.off_lu + slot, 0));
+      col[0] = make_double2(dth.x, pq ? dth.y : 0.0);
+      col[kGroup] = make_double2(pqj ? dv.x : 0.0, (pq && pqj) ? dv.y : (jb == i ? 1.0 : 0.0));
     }
   }
   const int64_t s = g * kGroup + sc;
