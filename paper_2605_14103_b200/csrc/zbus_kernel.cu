@@ -155,6 +155,9 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   // drift by up to one stage and a warp's epilogue overlaps the DMMA work of
   // the others. Empty-barrier parities live in bits 2..3 of phase_bits.
   if (tid == 0) {
+    // the stage buffers may have been generic-proxy scratch since the last
+    // pass (zb_injection_cta): order those accesses before the bulk writes
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     issue(0);
     if (n_stage > 1) issue(1);
   }
@@ -342,6 +345,81 @@ __device__ int zb_injection(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t
   return -1;
 }
 
+// Whole-CTA version of zb_injection for the columns with want[col] set (used
+// when its scratch fits the Z stage buffers, which are idle between passes):
+//   1. all threads gather v at the load rows of every wanted column into
+//      scratch (independent loads: one latency round instead of one per load),
+//   2. all threads compute the per-load currents (and the voltage-floor
+//      checks, first violation in the reference order via atomicMin),
+//   3. the column owner accumulates them into I_l in the reference order.
+// The currents are the same cdiv() values added in the same order as
+// zb_injection, so I_l is bitwise identical. fslot[col] gets the floor slot or -1.
+template <int NT>
+__device__ void zb_injection_cta(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t col0, const int* want,
+                                 bool from_v0, double* isf, double2* scratch, int* fslot) {
+  const int tid = threadIdx.x;
+  const int nl = m.n_l, nld = m.n_wye + m.n_delta;
+  double2* vl = scratch;                  // [NT][n_l]
+  double2* qb = scratch + (size_t)NT * nl;  // [NT][n_wye + n_delta]
+  if (tid < NT) fslot[tid] = 0x7fffffff;
+  for (int idx = tid; idx < NT * nl; idx += kThreads) {
+    const int col = idx / nl, lc = idx - col * nl;
+    if (!want[col]) continue;
+    const int row = m.l_row[lc];
+    vl[idx] = from_v0 ? m.v0[row] : io.v_out[(col0 + col) * m.n + row];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < NT * nld; idx += kThreads) {
+    const int col = idx / nld, k = idx - col * nld;
+    if (!want[col]) continue;
+    const int64_t scen = col0 + col;
+    const double2* v = vl + (size_t)col * nl;
+    double2 q;
+    int slot = 0x7fffffff;
+    if (k < m.n_wye) {
+      const double2 vp = v[m.wye_l[k]];
+      if (hypot(vp.x, vp.y) <= m.floor) slot = k;
+      q = cdiv(io.s_wye[scen * m.n_wye + k], vp);
+    } else {
+      const int d = k - m.n_wye;
+      const double2 vp = v[m.dp_l[d]], vq = v[m.dq_l[d]];
+      if (hypot(vp.x, vp.y) <= m.floor) slot = m.n_wye + d;
+      else if (hypot(vq.x, vq.y) <= m.floor) slot = m.n_wye + m.n_delta + d;
+      else if (hypot(vp.x - vq.x, vp.y - vq.y) <= m.floor) slot = m.n_wye + 2 * m.n_delta + d;
+      q = cdiv(io.s_delta[scen * m.n_delta + d], make_double2(vp.x - vq.x, vp.y - vq.y));
+    }
+    qb[idx] = q;
+    if (slot != 0x7fffffff) atomicMin(fslot + col, slot);
+  }
+  __syncthreads();
+  if (tid < NT && want[tid]) {
+    const int col = tid;
+    if (fslot[col] == 0x7fffffff) {
+      fslot[col] = -1;
+      for (int k = 0; k < m.kpad; ++k) {
+        isf[ifrag_index<NT>(k, col) + 0] = 0.0;
+        isf[ifrag_index<NT>(k, col) + 32] = 0.0;
+      }
+      const double2* q = qb + (size_t)col * nld;
+      for (int k = 0; k < m.n_wye; ++k) {  // wye: i[p] += -conj(s / v_p)
+        const int idx = ifrag_index<NT>(m.wye_l[k], col);
+        isf[idx] = isf[idx] + (-q[k].x);
+        isf[idx + 32] = isf[idx + 32] + q[k].y;
+      }
+      for (int k = 0; k < m.n_delta; ++k) {  // delta: i[p] -= i_line (all k) ...
+        const int idx = ifrag_index<NT>(m.dp_l[k], col);
+        isf[idx] = isf[idx] + (-q[m.n_wye + k].x);
+        isf[idx + 32] = isf[idx + 32] + q[m.n_wye + k].y;
+      }
+      for (int k = 0; k < m.n_delta; ++k) {  // ... then i[q] += i_line
+        const int idx = ifrag_index<NT>(m.dq_l[k], col);
+        isf[idx] = isf[idx] + q[m.n_wye + k].x;
+        isf[idx + 32] = isf[idx + 32] + (-q[m.n_wye + k].y);
+      }
+    }
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
     zbus_kernel(ZbDeviceModel m, ZbBatchIO io, double tol, int max_iter, int mag0_mode,
@@ -374,6 +452,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   uint32_t phase_bits = 0;
   ZbTileState st{colsum, red, run, cert};
+  // the CTA-wide injection needs [NT][n_l] voltages + [NT][loads] currents of
+  // scratch in the (then idle) Z stage buffers
+  const bool par_inj = (size_t)NT * (m.n_l + m.n_wye + m.n_delta) * 2 <= 2 * (size_t)stage_doubles;
 
   if (mag0_mode) {
     for (int k = tid; k < ksteps * NT * 8; k += kThreads) isf[k] = 0.0;
@@ -401,9 +482,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // ---- sweeps
     for (int k = 1; k <= max_iter; ++k) {
+      int* const inj_slot = reinterpret_cast<int*>(red);  // red is free between passes
+      if (par_inj) {
+        __syncthreads();  // run[] of the previous sweep visible to every thread
+        zb_injection_cta<NT>(m, io, col0, run, k == 1, isf, reinterpret_cast<double2*>(zs), inj_slot);
+      }
       if (tid < NT) {
         if (run[tid]) {
-          const int fs = zb_injection<NT>(m, io, scen, tid, k == 1, isf);
+          const int fs = par_inj ? inj_slot[tid] : zb_injection<NT>(m, io, scen, tid, k == 1, isf);
           if (fs >= 0) {
             run[tid] = 0;
             stat[tid] = ACPF_ZB_FLOOR;
@@ -442,11 +528,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncthreads();
     }
     // ---- certificate ||v - (Z i(v) + v0)||inf
+    if (par_inj) {
+      int* const inj_slot = reinterpret_cast<int*>(red);
+      if (tid < NT) cert[tid] = stat[tid] == ACPF_ZB_CONVERGED || stat[tid] == ACPF_ZB_MAX_ITER;
+      __syncthreads();
+      zb_injection_cta<NT>(m, io, col0, cert, false, isf, reinterpret_cast<double2*>(zs), inj_slot);
+    }
     if (tid < NT) {
+      const bool want = stat[tid] == ACPF_ZB_CONVERGED || stat[tid] == ACPF_ZB_MAX_ITER;
       cert[tid] = 0;
       colsum[tid] = 0.0;
-      if (stat[tid] == ACPF_ZB_CONVERGED || stat[tid] == ACPF_ZB_MAX_ITER) {
-        const int fs = zb_injection<NT>(m, io, scen, tid, false, isf);
+      if (want) {
+        const int fs = par_inj ? reinterpret_cast<int*>(red)[tid] : zb_injection<NT>(m, io, scen, tid, false, isf);
         if (fs >= 0) {
           resid[tid] = __longlong_as_double(0x7ff0000000000000LL);
         } else {
