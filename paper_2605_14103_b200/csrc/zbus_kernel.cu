@@ -33,7 +33,15 @@ namespace acpf {
 
 namespace {
 
-constexpr int kThreads = 256;   // 8 warps: 4 row-pairs x 2 column halves
+#ifndef ACPF_ZB_ROW_WARPS
+#define ACPF_ZB_ROW_WARPS 8
+#endif
+// warps = kRowWarps (row slices of a 64-row block, kRowGroups 8-row DMMA groups
+// each) x 2 column halves; 16 warps (4 per SM sub-partition) let one warp's
+// epilogue overlap the DMMA stream of the others
+constexpr int kRowWarps = ACPF_ZB_ROW_WARPS;
+constexpr int kRowGroups = 8 / kRowWarps;
+constexpr int kThreads = kRowWarps * 2 * 32;
 constexpr int kMaxKsPerStage = 16;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -110,7 +118,7 @@ __device__ __forceinline__ int ifrag_index(int k, int col) {
 
 struct ZbTileState {
   double* colsum;  // [NT]
-  double* red;     // [4][NT]
+  double* red;     // [kRowWarps][NT]
   int* run;        // [NT] 1 = running (writes allowed in an iterate pass)
   int* cert;       // [NT] 1 = needs the certificate pass
 };
@@ -122,7 +130,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
                         ZbTileState st) {
   constexpr int CGW = Smem<NT>::kCgWarp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rp = warp & 3, ch = warp >> 2;
+  const int rp = warp % kRowWarps, ch = warp / kRowWarps;
   const int ksteps = m.kpad >> 2;
   const int n_kc = (ksteps + kMaxKsPerStage - 1) / kMaxKsPerStage;
   const int n_stage = m.n_rb * n_kc;
@@ -162,7 +170,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     if (n_stage > 1) issue(1);
   }
 
-  double cr[2][CGW][2], ci[2][CGW][2];
+  double cr[kRowGroups][CGW][2], ci[kRowGroups][CGW][2];
   // per-lane running column partials over all row blocks (rows lane/4 of the
   // warp's two row groups); reduced across lanes/warps once per pass
   double acc[CGW][2];
@@ -173,7 +181,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     const int buf = sidx & 1;
     if (kc == 0) {
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < kRowGroups; ++a)
 #pragma unroll
         for (int b = 0; b < CGW; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
     }
@@ -183,10 +191,10 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     const int ks0 = kc * kMaxKsPerStage;
     const int nks = min(kMaxKsPerStage, ksteps - ks0);
     for (int ks = 0; ks < nks; ++ks) {
-      double ar[2], ai[2], br[CGW], bi[CGW];
+      double ar[kRowGroups], ai[kRowGroups], br[CGW], bi[CGW];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int rg = rp * 2 + a;
+      for (int a = 0; a < kRowGroups; ++a) {
+        const int rg = rp * kRowGroups + a;
         ar[a] = zb[((ks * 8 + rg) * 2 + 0) * 32 + lane];
         ai[a] = zb[((ks * 8 + rg) * 2 + 1) * 32 + lane];
       }
@@ -197,7 +205,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
         bi[b] = isf[(((ks0 + ks) * (NT / 8) + cg) * 2 + 1) * 32 + lane];
       }
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
+      for (int a = 0; a < kRowGroups; ++a) {
         const double nai = -ai[a];
 #pragma unroll
         for (int b = 0; b < CGW; ++b) {
@@ -219,8 +227,8 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     if (kc == n_kc - 1) {
       // ---- epilogue for row block rb (no CTA-wide synchronisation)
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int row = rb * kZbRows + (rp * 2 + a) * 8 + (lane >> 2);
+      for (int a = 0; a < kRowGroups; ++a) {
+        const int row = rb * kZbRows + (rp * kRowGroups + a) * 8 + (lane >> 2);
         const double2 v0 = m.v0[row];
         const bool in = row < m.n;
 #pragma unroll
@@ -262,7 +270,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
   }
   // ---- per-pass column reduction: 8 row lanes (fixed butterfly), then the
-  // 4 row-pair warps in fixed order
+  // kRowWarps row warps in fixed order
 #pragma unroll
   for (int b = 0; b < CGW; ++b)
 #pragma unroll
@@ -278,12 +286,10 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   __syncthreads();
   if (tid < NT) {
     const double* r = st.red;
-    if (MODE == kCert) {
-      st.colsum[tid] = nanmax(nanmax(nanmax(st.colsum[tid], r[tid]), r[NT + tid]),
-                              nanmax(r[2 * NT + tid], r[3 * NT + tid]));
-    } else {
-      st.colsum[tid] = st.colsum[tid] + (((r[tid] + r[NT + tid]) + r[2 * NT + tid]) + r[3 * NT + tid]);
-    }
+    double x = r[tid];
+#pragma unroll
+    for (int w = 1; w < kRowWarps; ++w) x = (MODE == kCert) ? nanmax(x, r[w * NT + tid]) : x + r[w * NT + tid];
+    st.colsum[tid] = (MODE == kCert) ? nanmax(st.colsum[tid], x) : st.colsum[tid] + x;
   }
   __syncthreads();
 }
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* isf = zs + 2 * stage_doubles;
   double* colsum = isf + (size_t)ksteps * NT * 8;
   double* red = colsum + NT;
-  double* mag = red + 4 * NT;
+  double* mag = red + kRowWarps * NT;
   double* delta = mag + NT;
   double* resid = delta + NT;
   int* run = reinterpret_cast<int*>(resid + NT);
@@ -573,7 +579,7 @@ template <int NT>
 size_t zbus_smem_bytes(int kpad) {
   const int ksteps = kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
-  size_t d = 2 * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + 4 * NT + 3 * NT;
+  size_t d = 2 * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kRowWarps * NT + 3 * NT;
   size_t bytes = d * 8 + (5 * NT + 2) * 4 + 32 + 16;
   return bytes;
 }
