@@ -101,6 +101,9 @@ struct acpf_nr_plan {
   void* stage_base = nullptr;
   int* host_active = nullptr;
   std::vector<int32_t> h_tpos, h_qidx;  // host copies for scenario generation
+  cudaStream_t copy_stream = nullptr;   // host-path H2D/D2H overlap
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_kend[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
   NrCertModel cert{};                   // acpf_nr_plan_set_branches (n_br < 0: not set)
   DevArena cert_arena;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -386,6 +389,103 @@ static acpf_status ensure_stage(DevArena& arena, size_t& have, void*& base, size
   return ACPF_OK;
 }
 
+// Host-pointer solve pipelined over two staging sets: the H2D of chunk c+1
+// and the D2H of chunk c-1 run on a copy stream while chunk c solves.
+static acpf_status nr_solve_host(acpf_nr_plan* p, int64_t batch, int64_t chunk, const double* p_spec,
+                                 const double* q_spec, double tol, int32_t max_newton, double* theta_out,
+                                 double* vmag_out, uint8_t* converged, int32_t* iterations,
+                                 double* final_mismatch_inf, int32_t* status, cudaStream_t st) {
+  const NrDeviceModel& d = p->dm;
+  if (!p->copy_stream) ACPF_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    if (!p->ev_h2d[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
+    if (!p->ev_kend[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_kend[k], cudaEventDisableTiming));
+    if (!p->ev_d2h[k]) ACPF_CUDA(cudaEventCreateWithFlags(&p->ev_d2h[k], cudaEventDisableTiming));
+  }
+  cudaStream_t cs = p->copy_stream;
+  const size_t set_b = (size_t)chunk * ((size_t)(d.n_theta + d.n_q) * 8 + (size_t)d.n_bus * 16 + 8 + 4 + 4 + 1) + 256;
+  acpf_status rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, 2 * set_b);
+  if (rc != ACPF_OK) return rc;
+  struct Set {
+    double *ps, *qs, *th, *vm, *fn;
+    int32_t *it, *stt;
+    uint8_t* cv;
+  } sets[2];
+  for (int k = 0; k < 2; ++k) {
+    char* b = (char*)p->stage_base + k * set_b;
+    auto take = [&](size_t bytes) {
+      char* r = b;
+      b += (bytes + 15) & ~(size_t)15;
+      return r;
+    };
+    sets[k].ps = (double*)take((size_t)chunk * d.n_theta * 8);
+    sets[k].qs = (double*)take((size_t)chunk * d.n_q * 8);
+    sets[k].th = (double*)take((size_t)chunk * d.n_bus * 8);
+    sets[k].vm = (double*)take((size_t)chunk * d.n_bus * 8);
+    sets[k].fn = (double*)take((size_t)chunk * 8);
+    sets[k].it = (int32_t*)take((size_t)chunk * 4);
+    sets[k].stt = (int32_t*)take((size_t)chunk * 4);
+    sets[k].cv = (uint8_t*)take((size_t)chunk);
+  }
+  const int64_t n_chunks = (batch + chunk - 1) / chunk;
+  auto h2d = [&](int64_t c) -> acpf_status {
+    const Set& S = sets[c & 1];
+    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    if (d.n_theta)
+      ACPF_CUDA(cudaMemcpyAsync(S.ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, cs));
+    if (d.n_q) ACPF_CUDA(cudaMemcpyAsync(S.qs, q_spec + s0 * d.n_q, nb * d.n_q * 8, cudaMemcpyHostToDevice, cs));
+    ACPF_CUDA(cudaEventRecord(p->ev_h2d[c & 1], cs));
+    return ACPF_OK;
+  };
+  ACPF_CUDA(cudaStreamWaitEvent(cs, p->ev1, 0));  // a previous call's work on st is done with the sets
+  if ((rc = h2d(0)) != ACPF_OK) return rc;
+  float total_ms = 0.0f;
+  int launches = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const Set& S = sets[c & 1];
+    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    ACPF_CUDA(cudaStreamWaitEvent(st, p->ev_h2d[c & 1], 0));
+    if (c >= 2) ACPF_CUDA(cudaStreamWaitEvent(st, p->ev_d2h[c & 1], 0));  // outputs of chunk c-2 read
+    if (c + 1 < n_chunks && (rc = h2d(c + 1)) != ACPF_OK) return rc;  // queued behind D2H(c-1) on cs
+    NrBatchIO io{};
+    io.batch = nb;
+    io.p_spec = S.ps;
+    io.q_spec = S.qs;
+    io.theta_out = S.th;
+    io.vmag_out = S.vm;
+    io.fnorm = S.fn;
+    io.iterations = S.it;
+    io.status = S.stt;
+    io.converged = S.cv;
+    ACPF_CUDA(cudaEventRecord(p->ev0, st));
+    int nl = 0;
+    NrWorkspace wsb = p->ws;
+    wsb.groups = (nb + kGroup - 1) / kGroup;
+    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, st, &nl));
+    ACPF_CUDA(cudaEventRecord(p->ev1, st));
+    ACPF_CUDA(cudaEventRecord(p->ev_kend[c & 1], st));
+    launches += nl;
+    ACPF_CUDA(cudaStreamWaitEvent(cs, p->ev_kend[c & 1], 0));
+    ACPF_CUDA(cudaMemcpyAsync(theta_out + s0 * d.n_bus, S.th, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, cs));
+    ACPF_CUDA(cudaMemcpyAsync(vmag_out + s0 * d.n_bus, S.vm, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, cs));
+    if (final_mismatch_inf)
+      ACPF_CUDA(cudaMemcpyAsync(final_mismatch_inf + s0, S.fn, nb * 8, cudaMemcpyDeviceToHost, cs));
+    if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + s0, S.it, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (status) ACPF_CUDA(cudaMemcpyAsync(status + s0, S.stt, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, S.cv, nb, cudaMemcpyDeviceToHost, cs));
+    ACPF_CUDA(cudaEventRecord(p->ev_d2h[c & 1], cs));
+    ACPF_CUDA(cudaEventSynchronize(p->ev1));
+    float ms = 0.0f;
+    ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    total_ms += ms;
+  }
+  ACPF_CUDA(cudaStreamSynchronize(cs));
+  ACPF_CUDA(cudaStreamSynchronize(st));
+  p->last_ms = total_ms;
+  p->last_launches = launches;
+  return ACPF_OK;
+}
+
 acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
                           const double* q_spec, double tol_mismatch, int32_t max_newton,
                           double* theta_out, double* vmag_out, uint8_t* converged,
@@ -413,11 +513,17 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     chunk = groups * kGroup;
   }
   chunk = std::min<int64_t>(chunk, batch);
+  // host buffers: at least two chunks so transfers overlap the solves
+  if (!dev_ptrs && env_int("ACPF_NR_CHUNK", 0) <= 0 && batch >= 2 * 8192)
+    chunk = std::min<int64_t>(chunk, (batch + 1) / 2);
   chunk = ((chunk + kGroup - 1) / kGroup) * kGroup;
   const int64_t groups = chunk / kGroup;
   acpf_status rc = nr_ensure_workspace(p, groups);
   if (rc != ACPF_OK) return rc;
 
+  if (!dev_ptrs && env_int("ACPF_NR_PIPELINE", 1) != 0)
+    return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
+                         converged, iterations, final_mismatch_inf, status, st);
   // per-scenario byte sizes
   const size_t in_b = (size_t)(d.n_theta + d.n_q) * 8;
   const size_t out_b = (size_t)d.n_bus * 16 + 1 + 4 + 8 + 4;
@@ -514,6 +620,12 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
     DeviceGuard dg(p->device);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    for (int k = 0; k < 2; ++k) {
+      if (p->ev_h2d[k]) cudaEventDestroy(p->ev_h2d[k]);
+      if (p->ev_kend[k]) cudaEventDestroy(p->ev_kend[k]);
+      if (p->ev_d2h[k]) cudaEventDestroy(p->ev_d2h[k]);
+    }
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     if (p->host_active) cudaFreeHost(p->host_active);
     p->work.release();
     p->stage.release();
