@@ -252,6 +252,20 @@ acpf_status acpf_zbus_kirchhoff(acpf_zbus_plan_t plan, int64_t batch, const doub
                                 const double* s_wye, const double* s_delta, double* kcl,
                                 uint32_t flags, void* cuda_stream);
 
+/* ------------------------------------------------------------------------
+ * Network reduction on the device (reference reduce_zbus,
+ * distribution.py:431-517): factor Y_NN (CSR, interleaved complex values)
+ * with partial pivoting and solve for the load columns and v0:
+ *   zl_out [n][n_l] = (Y_NN^-1)[:, l_index]   (interleaved complex, row-major)
+ *   v0_out [n]      = Y_NN^-1 rhs0,  rhs0 = -(Y_NS v_slack)
+ * ACPF_ESTRUCT when Y_NN is numerically singular by the reference's test
+ * (non-finite factor or min |U_ii| <= n eps max |Y_NN|). The outputs feed
+ * acpf_zbus_plan_create.
+ * ------------------------------------------------------------------------ */
+acpf_status acpf_zbus_reduce(int32_t device, int32_t n, const int32_t* ynn_rowptr, const int32_t* ynn_col,
+                             const double* ynn_val, const double* rhs0, int32_t n_l, const int32_t* l_index,
+                             double* zl_out, double* v0_out);
+
 #ifdef __cplusplus
 }
 #endif

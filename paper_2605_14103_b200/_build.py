@@ -18,6 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
          "-I", str(ROOT / "include"), "-Xptxas", "-v"]
+LIBS = ["-lcusolver"]
 
 
 def sources() -> list:
@@ -36,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", str(tmp), *map(str, sources())]
+    cmd = [NVCC, *ARCH, *FLAGS, "-o", str(tmp), *map(str, sources()), *LIBS]
     res = subprocess.run(cmd, cwd=str(PKG), capture_output=True, text=True)
     log = PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)

@@ -1314,4 +1314,31 @@ acpf_status acpf_zbus_kirchhoff(acpf_zbus_plan_t p, int64_t batch, const double*
   return ACPF_OK;
 }
 
+acpf_status acpf_zbus_reduce(int32_t device, int32_t n, const int32_t* ynn_rowptr, const int32_t* ynn_col,
+                             const double* ynn_val, const double* rhs0, int32_t n_l, const int32_t* l_index,
+                             double* zl_out, double* v0_out) {
+  if (n <= 0 || !ynn_rowptr || !rhs0 || n_l < 0 || (n_l && (!l_index || !zl_out)) || !v0_out ||
+      ynn_rowptr[0] != 0 || (ynn_rowptr[n] > 0 && (!ynn_col || !ynn_val))) {
+    set_error("acpf_zbus_reduce: invalid argument");
+    return ACPF_EINVAL;
+  }
+  for (int k = 0; k < n; ++k)
+    if (ynn_rowptr[k + 1] < ynn_rowptr[k]) {
+      set_error("acpf_zbus_reduce: bad CSR row pointers");
+      return ACPF_EINVAL;
+    }
+  for (int64_t e = 0; e < ynn_rowptr[n]; ++e)
+    if (ynn_col[e] < 0 || ynn_col[e] >= n) {
+      set_error("acpf_zbus_reduce: column out of range");
+      return ACPF_EINVAL;
+    }
+  for (int k = 0; k < n_l; ++k)
+    if (l_index[k] < 0 || l_index[k] >= n) {
+      set_error("acpf_zbus_reduce: l_index out of range");
+      return ACPF_EINVAL;
+    }
+  DeviceGuard dg(device);
+  return zbus_reduce_device(device, n, ynn_rowptr, ynn_col, ynn_val, rhs0, n_l, l_index, zl_out, v0_out, nullptr);
+}
+
 }  // extern "C"

@@ -211,6 +211,11 @@ struct ZbCertIO {
   double* kcl;             // [batch]
 };
 
+acpf_status zbus_reduce_device(int device, int n, const int32_t* rowptr, const int32_t* col, const double* val,
+                               const double* rhs0, int n_l, const int32_t* l_index, double* zl_out,
+                               double* v0_out, double* min_pivot_out);
+void set_error(const std::string& msg);
+
 size_t nr_cert_smem(int n_bus);
 size_t zb_cert_smem(int n);
 cudaError_t launch_nr_cert(const NrCertModel& m, const NrCertIO& io, cudaStream_t st);

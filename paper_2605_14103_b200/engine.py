@@ -33,7 +33,7 @@ EXPORTED = (
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
     "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
     "acpf_zbus_scenarios", "acpf_nr_plan_set_branches", "acpf_nr_certify",
-    "acpf_zbus_plan_set_network", "acpf_zbus_kirchhoff",
+    "acpf_zbus_plan_set_network", "acpf_zbus_kirchhoff", "acpf_zbus_reduce",
 )
 
 
@@ -103,6 +103,7 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_nr_certify": (I32, [P, I64, P, P, P, P, P, P, P, U32, P]),
         "acpf_zbus_plan_set_network": (I32, [P, P, P, P, P]),
         "acpf_zbus_kirchhoff": (I32, [P, I64, P, P, P, P, U32, P]),
+        "acpf_zbus_reduce": (I32, [I32, I32, P, P, P, P, I32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -450,6 +451,28 @@ class ZbusPlan:
             self._h = None
 
     __del__ = close
+
+
+def zbus_reduce(y_nn, rhs0, l_index, device: int = 0):
+    """Y_NN^-1 [E_l | rhs0] on the GPU (acpf_zbus_reduce): (Z[:, l], v0).
+    Raises EngineError with the reference's singular-Ybus text when Y_NN is
+    numerically singular (status ACPF_ESTRUCT)."""
+    require_device(device)
+    lib = load_library()
+    y = y_nn.tocsr()
+    y.sort_indices()
+    n = y.shape[0]
+    rp = np.ascontiguousarray(y.indptr, dtype=np.int32)
+    col = np.ascontiguousarray(y.indices, dtype=np.int32)
+    val = np.ascontiguousarray(y.data, dtype=np.complex128)
+    r0 = np.ascontiguousarray(rhs0, dtype=np.complex128)
+    li = np.ascontiguousarray(l_index, dtype=np.int32)
+    zl = np.empty((n, li.size), dtype=np.complex128)
+    v0 = np.empty(n, dtype=np.complex128)
+    _check(lib.acpf_zbus_reduce(device, n, _ptr(rp), _ptr(col) if col.size else None,
+                                _ptr(val) if val.size else None, _ptr(r0), li.size,
+                                _ptr(li) if li.size else None, _ptr(zl) if li.size else None, _ptr(v0)))
+    return zl, v0
 
 
 def zbus_plan_for(model, device: int | None = None) -> ZbusPlan:
