@@ -187,3 +187,53 @@ def test_zbus_device_scenarios_bitwise(tag, zb_models, golden):
     sw, sd = engine.zbus_plan_for(model).scenarios(base, int(g["seed"]), 0, count)
     np.testing.assert_array_equal(sw, g["s_wye"][:count])
     np.testing.assert_array_equal(sd, g["s_delta"][:count])
+
+
+# ---------------------------------------------------------------------------
+# edge cases: empty, single, ragged batches; chunked and pipelined host paths
+# ---------------------------------------------------------------------------
+
+
+def test_nr_empty_and_ragged_batches(tx_models, golden):
+    g = golden("nr_case118")
+    model = tx_models["case118"]
+    plan = model.plan()
+    p, q = np.ascontiguousarray(g["p_spec"]), np.ascontiguousarray(g["q_spec"])
+    full = plan.solve(p, q, 1e-8, 20)
+    empty = plan.solve(np.zeros((0, p.shape[1])), np.zeros((0, q.shape[1])), 1e-8, 20)
+    assert empty["theta"].shape == (0, model.net.n)
+    for b in (1, 7, 9, 17, 65):  # not multiples of the 8-scenario group
+        out = plan.solve(np.ascontiguousarray(p[:b]), np.ascontiguousarray(q[:b]), 1e-8, 20)
+        np.testing.assert_array_equal(out["theta"], full["theta"][:b])
+        np.testing.assert_array_equal(out["vmag"], full["vmag"][:b])
+        np.testing.assert_array_equal(out["iterations"], g["iterations"][:b])
+
+
+def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch):
+    # ragged chunks (ACPF_NR_CHUNK) through the pipelined host path and the
+    # device-pointer path give the same bits as one chunk
+    torch = pytest.importorskip("torch")
+    model = pf.build_transmission_model(load_transmission("case118"))
+    base = pf.transmission_base(model.net, model.part)
+    p, q = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=1000, seed=1010))
+    ref = model.plan().solve(p, q, 1e-8, 20)
+    monkeypatch.setenv("ACPF_NR_CHUNK", "136")
+    model2 = pf.build_transmission_model(load_transmission("case118"))
+    chunked = model2.plan().solve(p, q, 1e-8, 20)
+    np.testing.assert_array_equal(chunked["theta"], ref["theta"])
+    np.testing.assert_array_equal(chunked["iterations"], ref["iterations"])
+    dev = model2.plan().solve(torch.from_numpy(p).cuda(), torch.from_numpy(q).cuda(), 1e-8, 20)
+    np.testing.assert_array_equal(dev["vmag"].cpu().numpy(), ref["vmag"])
+
+
+def test_zbus_empty_and_ragged_batches(zb_models, golden):
+    g = golden("zb_ieee13")
+    model = zb_models["ieee13"]
+    sw, sd = np.ascontiguousarray(g["s_wye"][:200]), np.ascontiguousarray(g["s_delta"][:200])
+    full = engine.zbus_solve_arrays(model, sw, sd, 1e-9, 100)
+    empty = engine.zbus_solve_arrays(model, sw[:0], sd[:0], 1e-9, 100)
+    assert empty["v"].shape == (0, model.n)
+    for b in (1, 31, 33, 63, 65, 129):  # around the 32/64-scenario tiles
+        out = engine.zbus_solve_arrays(model, sw[:b], sd[:b], 1e-9, 100)
+        np.testing.assert_array_equal(out["v"], full["v"][:b])
+        np.testing.assert_array_equal(out["iterations"], g["iterations"][:b])
