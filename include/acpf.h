@@ -266,6 +266,34 @@ acpf_status acpf_zbus_reduce(int32_t device, int32_t n, const int32_t* ynn_rowpt
                              const double* ynn_val, const double* rhs0, int32_t n_l, const int32_t* l_index,
                              double* zl_out, double* v0_out);
 
+/* ------------------------------------------------------------------------
+ * The reference's own Newton step on the GPU (an ablation of
+ * the exact sparse-LU step): matrix-free J v (_jvp_operator,
+ * transmission.py:218-236) inside left-preconditioned restarted GMRES
+ * (sparse.py:219-338) with the fast-decoupled preconditioner
+ * (transmission.py:259-298).
+ * ------------------------------------------------------------------------ */
+
+/* FD data of the network: bprime_inv = (B' + eps I)^-1 [n_theta][n_theta]
+ * and bdprime_inv = (B'' + eps I)^-1 [n_q][n_q] (row-major; B' = -Im Y over
+ * the theta block, B'' = -Im Y over the q block, network.py:519-543), and
+ * G = -Re Y[q, theta] in CSR (n_q rows, columns index the theta block). */
+acpf_status acpf_nr_plan_set_fd(acpf_nr_plan_t plan, const double* bprime_inv, const double* bdprime_inv,
+                                const int32_t* g_rowptr, const int32_t* g_col, const double* g_val);
+
+/* Batched GMRES-Newton (reference _newton_loop semantics, statuses 0-3 as
+ * acpf_nr_solve). precond: 1 = FD, 0 = none. Extra outputs (each may be
+ * NULL): gmres_steps [batch][max_newton] GMRES iterations of each Newton step
+ * (NewtonResult.per_iteration_gmres, entries past `iterations` are 0);
+ * gmres_diag [batch]: 0 none, 1 breakdown, 2 stagnation (transmission.py:
+ * 371-376) at Newton step gmres_diag_k with relres gmres_diag_relres. */
+acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t plan, int64_t batch, const double* p_spec, const double* q_spec,
+                                double tol_mismatch, int32_t max_newton, double gmres_tol, int32_t restart,
+                                int32_t max_outer, int32_t precond, double* theta_out, double* vmag_out,
+                                uint8_t* converged, int32_t* iterations, double* final_mismatch_inf,
+                                int32_t* status, int32_t* gmres_steps, int32_t* gmres_diag, int32_t* gmres_diag_k,
+                                double* gmres_diag_relres, uint32_t flags, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,7 @@
 // chunking when the batch would not fit the device workspace, staging host
 // buffers through device memory when ACPF_HOST_PTRS is given.
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -106,6 +107,9 @@ struct acpf_nr_plan {
               ev_d2h[2] = {nullptr, nullptr};
   NrCertModel cert{};                   // acpf_nr_plan_set_branches (n_br < 0: not set)
   DevArena cert_arena;
+  GmModel gm{};                         // acpf_nr_plan_set_fd (binv1 null: not set)
+  DevArena gm_arena;
+  void* cublas = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
@@ -626,6 +630,7 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
       if (p->ev_d2h[k]) cudaEventDestroy(p->ev_d2h[k]);
     }
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+    if (p->cublas) cublasDestroy((cublasHandle_t)p->cublas);
     if (p->host_active) cudaFreeHost(p->host_active);
     p->work.release();
     p->stage.release();
@@ -1339,6 +1344,226 @@ acpf_status acpf_zbus_reduce(int32_t device, int32_t n, const int32_t* ynn_rowpt
     }
   DeviceGuard dg(device);
   return zbus_reduce_device(device, n, ynn_rowptr, ynn_col, ynn_val, rhs0, n_l, l_index, zl_out, v0_out, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// GMRES-FD Newton ablation (kernels in gmres_kernel.cu)
+// ---------------------------------------------------------------------------
+
+acpf_status acpf_nr_plan_set_fd(acpf_nr_plan_t p, const double* bprime_inv, const double* bdprime_inv,
+                                const int32_t* g_rowptr, const int32_t* g_col, const double* g_val) {
+  if (!p || (p->dm.n_theta && !bprime_inv) || (p->dm.n_q && (!bdprime_inv || !g_rowptr))) {
+    set_error("acpf_nr_plan_set_fd: invalid argument");
+    return ACPF_EINVAL;
+  }
+  const int nt = p->dm.n_theta, nq = p->dm.n_q, nb = p->dm.n_bus;
+  const int64_t gnnz = nq ? g_rowptr[nq] : 0;
+  for (int64_t e = 0; e < gnnz; ++e)
+    if (g_col[e] < 0 || g_col[e] >= nt) {
+      set_error("acpf_nr_plan_set_fd: G column out of range");
+      return ACPF_EINVAL;
+    }
+  std::vector<int32_t> tb(nt), qb(nq);
+  for (int b = 0; b < nb; ++b) {
+    if (p->h_tpos[b] >= 0) tb[p->h_tpos[b]] = b;
+    if (p->h_qidx[b] >= 0) qb[p->h_qidx[b]] = b;
+  }
+  DeviceGuard dg(p->device);
+  p->gm_arena.release();
+  GmModel g{};
+  g.n_bus = nb;
+  g.n_theta = nt;
+  g.n_q = nq;
+  g.nj = nt + nq;
+  g.y_rowptr = p->dm.y_rowptr;
+  g.y_col = p->dm.y_col;
+  g.y_val = p->dm.y_val;
+  g.tpos = p->dm.tpos;
+  g.qidx = p->dm.qidx;
+  g.theta_init = p->dm.theta_init;
+  g.vmag_init = p->dm.vmag_init;
+  const std::vector<int32_t> zero_rp(nq + 1, 0);
+  cudaError_t e = cudaSuccess;
+  auto up = [&](auto** dst, const auto* src, size_t cnt) {
+    if (e == cudaSuccess) e = p->gm_arena.upload(dst, src, cnt);
+  };
+  up(const_cast<int32_t**>(&g.theta_block), tb.data(), tb.size());
+  up(const_cast<int32_t**>(&g.q_block), qb.data(), qb.size());
+  up(const_cast<double**>(&g.binv1), bprime_inv, (size_t)nt * nt);
+  up(const_cast<double**>(&g.binv2), bdprime_inv, (size_t)nq * nq);
+  up(const_cast<int32_t**>(&g.g_rowptr), nq ? g_rowptr : zero_rp.data(), (size_t)nq + 1);
+  up(const_cast<int32_t**>(&g.g_col), g_col, (size_t)gnnz);
+  up(const_cast<double**>(&g.g_val), g_val, (size_t)gnnz);
+  ACPF_CUDA(e);
+  if (!p->cublas) {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
+      set_error("acpf_nr_plan_set_fd: cublasCreate failed");
+      return ACPF_ECUDA;
+    }
+    p->cublas = h;
+  }
+  p->gm = g;
+  return ACPF_OK;
+}
+
+acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t p, int64_t batch, const double* p_spec, const double* q_spec,
+                                double tol_mismatch, int32_t max_newton, double gmres_tol, int32_t restart,
+                                int32_t max_outer, int32_t precond, double* theta_out, double* vmag_out,
+                                uint8_t* converged, int32_t* iterations, double* final_mismatch_inf,
+                                int32_t* status, int32_t* gmres_steps, int32_t* gmres_diag, int32_t* gmres_diag_k,
+                                double* gmres_diag_relres, uint32_t flags, void* cuda_stream) {
+  if (!p || batch < 0 || !theta_out || !vmag_out || max_newton < 1 || !(tol_mismatch > 0) ||
+      !(gmres_tol > 0) || restart < 1 || max_outer < 1 || (precond != 0 && precond != 1) || flags > 1u ||
+      (p->dm.n_theta && !p_spec) || (p->dm.n_q && !q_spec)) {
+    set_error("acpf_nr_solve_gmres: invalid argument");
+    return ACPF_EINVAL;
+  }
+  if (!p->gm.theta_block && p->dm.n_theta) {
+    set_error("acpf_nr_solve_gmres: call acpf_nr_plan_set_fd first");
+    return ACPF_EINVAL;
+  }
+  if (batch == 0) return ACPF_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cublasSetStream((cublasHandle_t)p->cublas, st);
+  const GmModel& m = p->gm;
+  const int mm = std::min<int>(restart, std::max(1, m.nj));  // m = min(restart, n) (sparse.py:262)
+  const int bc = (int)std::min<int64_t>(batch, std::max<int64_t>(32, env_int("ACPF_GMRES_CHUNK", 4096)));
+  // workspace for one chunk
+  const size_t nd = gmres_work_doubles(m, bc, mm);
+  const size_t ni = (size_t)bc * (16 + (max_newton + 1)) + 8;
+  DevArena wa;
+  double* dbase = nullptr;
+  int* ibase = nullptr;
+  ACPF_CUDA(wa.alloc((void**)&dbase, nd * sizeof(double)));
+  ACPF_CUDA(wa.alloc((void**)&ibase, ni * sizeof(int)));
+  ACPF_CUDA(cudaMemsetAsync(ibase, 0, ni * sizeof(int), st));
+  GmWork w{};
+  w.bc = bc;
+  {
+    double* d = dbase;
+    const size_t B = bc, nb = m.n_bus, nj = m.nj;
+    auto take = [&](size_t n) {
+      double* r = d;
+      d += n;
+      return r;
+    };
+    w.th = take(B * nb);
+    w.vm = take(B * nb);
+    w.u = (double2*)take(2 * B * nb);
+    w.ph = (double2*)take(2 * B * nb);
+    w.ic = (double2*)take(2 * B * nb);
+    w.du = (double2*)take(2 * B * nb);
+    w.b = take(B * nj);
+    w.x = take(B * nj);
+    w.wv = take(B * nj);
+    w.t1 = take(B * nj);
+    w.t2 = take(B * nj);
+    w.vb = take(B * nj * (mm + 1));
+    w.h = take(B * (size_t)(mm + 1) * mm);
+    w.cs = take(B * mm);
+    w.sn = take(B * mm);
+    w.g = take(B * (mm + 1));
+    w.y = take(B * (mm + 1));
+    w.part = take(B * ((nj + 63) / 64));
+    w.beta0 = take(B);
+    w.beta = take(B);
+    w.relres = take(B);
+    w.scal = take(B);
+    w.fout = take(B);
+    w.gdiag_rel = take(B);
+    w.fmax_bits = (unsigned long long*)take(B);
+    int* q = ibase;
+    auto takei = [&](size_t n) {
+      int* r = q;
+      q += n;
+      return r;
+    };
+    w.flags = takei(B);
+    w.nactive = takei(B);
+    w.status = takei(B);
+    w.iters = takei(B);
+    w.gstate = takei(B);
+    w.cyc = takei(B);
+    w.kk = takei(B);
+    w.brk = takei(B);
+    w.gsum = takei(B);
+    w.gtotal = takei(B);
+    w.gdiag = takei(B);
+    w.gdiag_k = takei(B);
+    w.gsteps = takei(B * (max_newton + 1));
+    w.count = takei(1);
+  }
+  int* host_count = nullptr;
+  ACPF_CUDA(cudaMallocHost((void**)&host_count, sizeof(int)));
+  w.host_count = host_count;
+  const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
+  const size_t nt = m.n_theta, nq = m.n_q, nbus = m.n_bus;
+  // device staging for host pointers (one chunk)
+  double *sp = nullptr, *sq = nullptr, *sth = nullptr, *svm = nullptr, *sfn = nullptr, *sdr = nullptr;
+  int32_t *sit = nullptr, *sst = nullptr, *sgs = nullptr, *sgd = nullptr, *sgk = nullptr;
+  uint8_t* scv = nullptr;
+  if (!dev_ptrs) {
+    ACPF_CUDA(wa.alloc((void**)&sp, (size_t)bc * nt * 8 + 8));
+    ACPF_CUDA(wa.alloc((void**)&sq, (size_t)bc * nq * 8 + 8));
+    ACPF_CUDA(wa.alloc((void**)&sth, (size_t)bc * nbus * 8));
+    ACPF_CUDA(wa.alloc((void**)&svm, (size_t)bc * nbus * 8));
+    ACPF_CUDA(wa.alloc((void**)&sfn, (size_t)bc * 8));
+    ACPF_CUDA(wa.alloc((void**)&sdr, (size_t)bc * 8));
+    ACPF_CUDA(wa.alloc((void**)&sit, (size_t)bc * 4));
+    ACPF_CUDA(wa.alloc((void**)&sst, (size_t)bc * 4));
+    ACPF_CUDA(wa.alloc((void**)&sgs, (size_t)bc * max_newton * 4));
+    ACPF_CUDA(wa.alloc((void**)&sgd, (size_t)bc * 4));
+    ACPF_CUDA(wa.alloc((void**)&sgk, (size_t)bc * 4));
+    ACPF_CUDA(wa.alloc((void**)&scv, (size_t)bc));
+  }
+  ACPF_CUDA(cudaEventRecord(p->ev0, st));
+  cudaError_t err = cudaSuccess;
+  for (int64_t s0 = 0; s0 < batch && err == cudaSuccess; s0 += bc) {
+    const int64_t nb = std::min<int64_t>(bc, batch - s0);
+    if (dev_ptrs) {
+      w.p_spec = p_spec ? p_spec + s0 * nt : nullptr;
+      w.q_spec = q_spec ? q_spec + s0 * nq : nullptr;
+    } else {
+      if (nt) err = cudaMemcpyAsync(sp, p_spec + s0 * nt, nb * nt * 8, cudaMemcpyHostToDevice, st);
+      if (nq && err == cudaSuccess) err = cudaMemcpyAsync(sq, q_spec + s0 * nq, nb * nq * 8, cudaMemcpyHostToDevice, st);
+      w.p_spec = sp;
+      w.q_spec = sq;
+    }
+    if (err == cudaSuccess)
+      err = gmres_newton(m, w, p->cublas, nb, tol_mismatch, max_newton, gmres_tol, mm, max_outer, precond == 1, st);
+    auto o = [&](auto* user, auto* stage, int64_t per) { return dev_ptrs ? (user ? user + s0 * per : nullptr) : (user ? stage : nullptr); };
+    if (err == cudaSuccess)
+      err = gmres_output(m, w, nb, max_newton, o(theta_out, sth, (int64_t)nbus), o(vmag_out, svm, (int64_t)nbus),
+                         o(converged, scv, 1), o(iterations, sit, 1), o(final_mismatch_inf, sfn, 1),
+                         o(status, sst, 1), o(gmres_steps, sgs, max_newton), o(gmres_diag, sgd, 1),
+                         o(gmres_diag_k, sgk, 1), o(gmres_diag_relres, sdr, 1), st);
+    if (!dev_ptrs && err == cudaSuccess) {
+      auto back = [&](auto* user, const auto* stage, size_t bytes) {
+        if (user && err == cudaSuccess) err = cudaMemcpyAsync(user, stage, bytes, cudaMemcpyDeviceToHost, st);
+      };
+      back(theta_out + s0 * nbus, sth, nb * nbus * 8);
+      back(vmag_out + s0 * nbus, svm, nb * nbus * 8);
+      back(converged ? converged + s0 : nullptr, scv, nb);
+      back(iterations ? iterations + s0 : nullptr, sit, nb * 4);
+      back(final_mismatch_inf ? final_mismatch_inf + s0 : nullptr, sfn, nb * 8);
+      back(status ? status + s0 : nullptr, sst, nb * 4);
+      back(gmres_steps ? gmres_steps + s0 * max_newton : nullptr, sgs, nb * max_newton * 4);
+      back(gmres_diag ? gmres_diag + s0 : nullptr, sgd, nb * 4);
+      back(gmres_diag_k ? gmres_diag_k + s0 : nullptr, sgk, nb * 4);
+      back(gmres_diag_relres ? gmres_diag_relres + s0 : nullptr, sdr, nb * 8);
+    }
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  }
+  cudaEventRecord(p->ev1, st);
+  cudaEventSynchronize(p->ev1);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, p->ev0, p->ev1);
+  p->last_ms = ms;
+  cudaFreeHost(host_count);
+  ACPF_CUDA(err);
+  return ACPF_OK;
 }
 
 }  // extern "C"

@@ -216,6 +216,49 @@ acpf_status zbus_reduce_device(int device, int n, const int32_t* rowptr, const i
                                double* v0_out, double* min_pivot_out);
 void set_error(const std::string& msg);
 
+// ---- GMRES-FD Newton ablation (gmres_kernel.cu)
+struct GmModel {
+  int n_bus, n_theta, n_q, nj;
+  const int32_t* y_rowptr;
+  const int32_t* y_col;
+  const double2* y_val;
+  const int32_t* tpos;
+  const int32_t* qidx;
+  const int32_t* theta_block;  // [n_theta] bus of each theta unknown
+  const int32_t* q_block;      // [n_q]
+  const double* theta_init;
+  const double* vmag_init;
+  const double* binv1;  // [n_theta][n_theta] (B' + eps I)^-1, row-major
+  const double* binv2;  // [n_q][n_q]
+  const int32_t* g_rowptr;  // G = -Re Y[q, theta] (CSR, n_q rows)
+  const int32_t* g_col;
+  const double* g_val;
+};
+
+struct GmWork {
+  int bc;  // scenarios per chunk (vectors are [rows][bc])
+  double *th, *vm;
+  double2 *u, *ph, *ic, *du;
+  double *b, *x, *wv, *t1, *t2, *vb, *h, *cs, *sn, *g, *y, *part;
+  double *beta0, *beta, *relres, *scal, *fout;
+  const double* p_spec;  // [bc][n_theta] (scenario-major, as the caller's)
+  const double* q_spec;
+  unsigned long long* fmax_bits;
+  int *flags, *nactive, *status, *iters, *gstate, *cyc, *kk, *brk, *gsum, *gtotal, *gdiag, *count;
+  int* gsteps;     // [max_newton + 1][bc] GMRES iterations per Newton step
+  int* gdiag_k;    // Newton step of the first GMRES diagnostic
+  double* gdiag_rel;
+  int* host_count;
+};
+
+size_t gmres_work_doubles(const GmModel& m, int bc, int restart);
+cudaError_t gmres_newton(const GmModel& m, GmWork& w, void* cublas, int64_t nb, double tol, int max_newton,
+                         double gtol, int restart, int max_outer, bool fd, cudaStream_t st);
+cudaError_t gmres_output(const GmModel& m, const GmWork& w, int64_t nb, int max_newton, double* theta_out,
+                         double* vmag_out, uint8_t* converged, int32_t* iterations, double* fnorm,
+                         int32_t* status, int32_t* gmres_steps, int32_t* gmres_diag, int32_t* gmres_diag_k,
+                         double* gmres_diag_relres, cudaStream_t st);
+
 size_t nr_cert_smem(int n_bus);
 size_t zb_cert_smem(int n);
 cudaError_t launch_nr_cert(const NrCertModel& m, const NrCertIO& io, cudaStream_t st);

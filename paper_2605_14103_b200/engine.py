@@ -34,6 +34,7 @@ EXPORTED = (
     "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
     "acpf_zbus_scenarios", "acpf_nr_plan_set_branches", "acpf_nr_certify",
     "acpf_zbus_plan_set_network", "acpf_zbus_kirchhoff", "acpf_zbus_reduce",
+    "acpf_nr_plan_set_fd", "acpf_nr_solve_gmres",
 )
 
 
@@ -104,6 +105,9 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_zbus_plan_set_network": (I32, [P, P, P, P, P]),
         "acpf_zbus_kirchhoff": (I32, [P, I64, P, P, P, P, U32, P]),
         "acpf_zbus_reduce": (I32, [I32, I32, P, P, P, P, I32, P, P, P]),
+        "acpf_nr_plan_set_fd": (I32, [P, P, P, P, P, P]),
+        "acpf_nr_solve_gmres": (I32, [P, I64, P, P, D, I32, D, I32, I32, I32, P, P, P, P, P, P, P, P, P,
+                                      P, U32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -301,6 +305,69 @@ class NrPlan:
                                       el.size, _ptr(el), *[_ptr(a) for a in arrs], _ptr(p), _ptr(q),
                                       flags, None))
         return p, q
+
+    def set_fd(self, y_csr, theta_block, q_block, epsilon: float = 1e-6) -> None:
+        """Attach the fast-decoupled preconditioner data (acpf_nr_plan_set_fd):
+        explicit inverses of B' + eps I and B'' + eps I (factorised with the
+        reference's singularity test, sparse.py:159-183) and G = -Re Y[q, th]."""
+        import scipy.linalg
+        import scipy.sparse
+        y = y_csr.tocsr()
+        tb = np.asarray(theta_block, dtype=np.int64)
+        qb = np.asarray(q_block, dtype=np.int64)
+
+        def inverse(block):
+            dense = -(y[block][:, block].imag).toarray()
+            n = dense.shape[0]
+            if n == 0:
+                return np.zeros((0, 0))
+            dense = dense + epsilon * np.eye(n)
+            lu, piv = scipy.linalg.lu_factor(dense, check_finite=False)
+            scale = max(np.abs(dense).max(), np.finfo(np.float64).tiny)
+            if not np.all(np.isfinite(lu)) or np.abs(np.diag(lu)).min() <= n * np.finfo(np.float64).eps * scale:
+                raise EngineError(f"block of dim {n} numerically singular (epsilon={epsilon!r})")
+            return np.ascontiguousarray(scipy.linalg.lu_solve((lu, piv), np.eye(n), check_finite=False))
+
+        b1, b2 = inverse(tb), inverse(qb)
+        g = scipy.sparse.csr_matrix(-(y[qb][:, tb].real))
+        g.eliminate_zeros()
+        g.sort_indices()
+        rp = np.ascontiguousarray(g.indptr, dtype=np.int32)
+        col = np.ascontiguousarray(g.indices, dtype=np.int32)
+        val = np.ascontiguousarray(g.data, dtype=np.float64)
+        _check(_lib.acpf_nr_plan_set_fd(self._h, _ptr(b1) if b1.size else None, _ptr(b2) if b2.size else None,
+                                        _ptr(rp), _ptr(col) if col.size else None,
+                                        _ptr(val) if val.size else None))
+        self._fd_eps = epsilon
+
+    def solve_gmres(self, p_spec, q_spec, tol: float, max_newton: int, precond: str = "fd",
+                    gmres_tol: float = 1e-8, restart: int = 60, max_outer: int = 10, stream=None) -> dict:
+        """The reference's Newton step (matrix-free GMRES, FD or no
+        preconditioner) for a stacked batch (acpf_nr_solve_gmres)."""
+        dev = _is_device(p_spec)
+        b = int(p_spec.shape[0])
+        out = self.alloc_outputs(b, like=p_spec if dev else None)
+        if dev:
+            import torch
+            kw = dict(device=p_spec.device)
+            out["gmres_steps"] = torch.zeros((b, max_newton), dtype=torch.int32, **kw)
+            out["gmres_diag"] = torch.zeros(b, dtype=torch.int32, **kw)
+            out["gmres_diag_k"] = torch.zeros(b, dtype=torch.int32, **kw)
+            out["gmres_diag_relres"] = torch.zeros(b, dtype=torch.float64, **kw)
+        else:
+            out["gmres_steps"] = np.zeros((b, max_newton), dtype=np.int32)
+            out["gmres_diag"] = np.zeros(b, dtype=np.int32)
+            out["gmres_diag_k"] = np.zeros(b, dtype=np.int32)
+            out["gmres_diag_relres"] = np.zeros(b)
+        flags = ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS
+        _check(_lib.acpf_nr_solve_gmres(
+            self._h, b, _ptr(p_spec), _ptr(q_spec), float(tol), int(max_newton), float(gmres_tol),
+            int(restart), int(max_outer), 1 if precond == "fd" else 0, _ptr(out["theta"]),
+            _ptr(out["vmag"]), _ptr(out["converged"]), _ptr(out["iterations"]),
+            _ptr(out["final_mismatch_inf"]), _ptr(out["status"]), _ptr(out["gmres_steps"]),
+            _ptr(out["gmres_diag"]), _ptr(out["gmres_diag_k"]), _ptr(out["gmres_diag_relres"]), flags,
+            _stream_ptr(stream)))
+        return out
 
     def set_branches(self, net) -> None:
         """Attach the branch table (acpf_nr_plan_set_branches) for certify()."""

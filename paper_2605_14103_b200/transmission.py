@@ -66,9 +66,10 @@ class GmresOptions:
 
 @dataclass
 class NewtonOptions:
-    """Reference transmission.py:100-117. ``epsilon``/``gmres``/``precond``
-    parameterise the reference's iterative step solve and are validated but
-    do not change the exact-LU step."""
+    """Reference transmission.py:100-117 plus ``step``: "lu" (default) solves
+    each Newton step with the engine's exact sparse LU; "gmres" runs the
+    reference's own step on the GPU (matrix-free GMRES with ``precond`` "fd"
+    or "none", ``gmres`` and ``epsilon`` as in the reference; SURVEY 8(f) #4)."""
 
     tol_mismatch: float = 1e-8
     max_newton: int = 20
@@ -76,6 +77,7 @@ class NewtonOptions:
     gmres: GmresOptions = field(default_factory=GmresOptions)
     flat_start: bool = True
     precond: str = "fd"
+    step: str = "lu"
 
     def __post_init__(self):
         if not self.tol_mismatch > 0:
@@ -84,6 +86,8 @@ class NewtonOptions:
             raise ValueError("max_newton must be >= 1")
         if self.precond not in ("fd", "none"):
             raise ValueError(f"unknown preconditioner {self.precond!r}")
+        if self.step not in ("lu", "gmres"):
+            raise ValueError(f"unknown step solver {self.step!r}")
 
 
 @dataclass(frozen=True)
@@ -211,22 +215,33 @@ def _check_options(opts: NewtonOptions | None, start) -> NewtonOptions:
 
 
 def results_from_arrays(out: dict, index=None) -> list:
-    """Per-scenario NewtonResult records from the stacked engine outputs."""
+    """Per-scenario NewtonResult records from the stacked engine outputs
+    (with the GMRES step's per-iteration counts and diagnostics when present,
+    transmission.py:366-376)."""
     res = []
     rng = range(out["theta"].shape[0]) if index is None else index
+    gm = "gmres_steps" in out
     for k in rng:
         st = int(out["status"][k])
         it = int(out["iterations"][k])
+        per = ()
+        diag = None
+        if gm:
+            per = tuple(int(c) for c in out["gmres_steps"][k][:it])
+            kind, kk = int(out["gmres_diag"][k]), int(out["gmres_diag_k"][k])
+            if kind == 1:
+                diag = f"GMRES breakdown at Newton iteration {kk}"
+            elif kind == 2:
+                diag = (f"GMRES stagnated at Newton iteration {kk} "
+                        f"(relres {float(out['gmres_diag_relres'][k]):.2e})")
         if st in _STATUS_TEXT:
             diag = _STATUS_TEXT[st]
         elif st == 4:
             diag = f"zero pivot in the static-pivot LU at Newton iteration {it}"
-        else:
-            diag = None
         res.append(NewtonResult(
             state=PolarState(out["theta"][k].copy(), out["vmag"][k].copy()),
             converged=bool(out["converged"][k]), iterations=it,
-            final_mismatch_inf=float(out["final_mismatch_inf"][k]), per_iteration_gmres=(),
+            final_mismatch_inf=float(out["final_mismatch_inf"][k]), per_iteration_gmres=per,
             diagnostic=diag))
     return res
 
@@ -244,7 +259,14 @@ def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = Non
     if not scenarios:
         return []
     p, q = stack_transmission_scenarios(model, scenarios)
-    out = model.plan(0 if device is None else device).solve(p, q, opts.tol_mismatch, opts.max_newton)
+    plan = model.plan(0 if device is None else device)
+    if opts.step == "gmres":
+        if getattr(plan, "_fd_eps", None) != opts.epsilon:
+            plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, opts.epsilon)
+        out = plan.solve_gmres(p, q, opts.tol_mismatch, opts.max_newton, opts.precond, opts.gmres.tol,
+                               opts.gmres.restart, opts.gmres.max_outer)
+    else:
+        out = plan.solve(p, q, opts.tol_mismatch, opts.max_newton)
     return results_from_arrays(out)
 
 
