@@ -81,15 +81,21 @@ def _load(args):
     return path, kind, model, base
 
 
-def _solve_device(kind, model, base, seed, count, spread, tol):
-    """Generate and solve `count` seeded scenarios on the device; host results."""
+def _solve_device(kind, model, base, seed, count, spread, tol, step="lu", precond="fd"):
+    """Generate and solve `count` seeded scenarios on the device; host results.
+    ``step`` "gmres" runs the reference's GMRES step (``precond`` fd|none)."""
     import torch
     dev = torch.device("cuda", 0)
     if kind == "tx":
         plan = model.plan(0)
         p, q = plan.scenarios(base, seed, 0, count, spread, device=dev)
+        if step == "gmres":
+            plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, 1e-6)
         t0 = time.perf_counter()
-        out = plan.solve(p, q, tol if tol is not None else 1e-8, 20)
+        if step == "gmres":
+            out = plan.solve_gmres(p, q, tol if tol is not None else 1e-8, 20, precond=precond)
+        else:
+            out = plan.solve(p, q, tol if tol is not None else 1e-8, 20)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     else:
@@ -104,7 +110,8 @@ def _solve_device(kind, model, base, seed, count, spread, tol):
 
 def cmd_solve(args) -> int:
     path, kind, model, base = _load(args)
-    out, wall = _solve_device(kind, model, base, args.seed, args.batch, args.spread, args.tol)
+    out, wall = _solve_device(kind, model, base, args.seed, args.batch, args.spread, args.tol, args.step,
+                              args.precond)
     results = (tm.results_from_arrays(out) if kind == "tx" else engine.zbus_results(model, out))
     per = wall / len(results)
     report = bm.BatchReport(
@@ -144,9 +151,10 @@ def cmd_bench(args) -> int:
     if top not in sizes:
         sizes.append(top)
     lines = ["case,kind,batch_size,workers,n_converged,total_wall_time,throughput"]
-    _solve_device(kind, model, base, args.seed, 1, args.spread, args.tol)  # warm-up
+    _solve_device(kind, model, base, args.seed, 1, args.spread, args.tol, args.step, args.precond)  # warm-up
     for size in sizes:
-        out, wall = _solve_device(kind, model, base, args.seed, size, args.spread, args.tol)
+        out, wall = _solve_device(kind, model, base, args.seed, size, args.spread, args.tol, args.step,
+                                  args.precond)
         lines.append(f"{Path(path).name},{kind},{size},1,{int(out['converged'].sum())},{wall!r},"
                      f"{size / wall!r}")
     payload = "\n".join(lines) + "\n"
@@ -223,6 +231,10 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--out", default=None)
         p.add_argument("--format", choices=("json", "csv"), default="json")
         p.add_argument("--oracle", default=None)
+        p.add_argument("--precond", choices=("fd", "none"), default="fd",
+                       help="GMRES preconditioner for --step gmres (reference cli.py:322-327)")
+        p.add_argument("--step", choices=("lu", "gmres"), default="lu",
+                       help="Newton step: exact sparse LU (default) or the reference's GMRES")
         p.add_argument("-v", "--verbose", action="count", default=0)
         p.set_defaults(fn=fn)
     return ap
