@@ -109,7 +109,6 @@ struct PipeLdgsts {
   static constexpr int NG = NG_, CH = CH_, NBUF = NBUF_;
   static constexpr int kSlot = NG * kBlkBytes;
   static constexpr int kRingN = CH * NBUF;
-  static constexpr bool kBulk = false;
   static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
   const uint32_t* stream;
   const double* src;  // this lane's copy source: its group's block region + chunk
@@ -205,127 +204,6 @@ struct PipeLdgsts {
     cp_wait<0>();
     __syncwarp();
   }
-};
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-
-// Same pipeline with bulk copies (the TMA engine): each element of a stage is
-// one 256-byte cp.async.bulk issued by one lane, and a stage completes on its
-// own mbarrier (transaction count = the stage's bytes), so issuing a stage
-// costs a handful of instructions instead of one 16-byte LDGSTS per lane and
-// element.
-template <int NG_, int CH_, int NBUF_>
-struct PipeBulk {
-  static constexpr int NG = NG_, CH = CH_, NBUF = NBUF_;
-  static constexpr int kSlot = NG * kBlkBytes;
-  static constexpr int kRingN = CH * NBUF;
-  static constexpr bool kBulk = true;
-  static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
-  static_assert(CH * NG <= 32, "one copy per lane and stage");
-  const uint32_t* stream;
-  const double* src;  // this lane's group block region
-  bool cp_ok;         // this lane's group is live
-  int nlive;          // live groups of the unit
-  uint32_t ring;      // smem [kRingN] slots, then [kRingN] u32 words, then [NBUF] mbarriers
-  uint32_t wring;
-  int lane;
-  int s0, n, issued, ready_upto, q;
-  uint32_t wcur, wnext;
-  int wbase;
-
-  static constexpr size_t kSmem = (size_t)kRingN * (kSlot + 4) + (size_t)NBUF * 8;
-  __host__ __device__ static constexpr size_t smem_bytes() { return kSmem; }
-
-  __device__ __forceinline__ uint32_t bar(int stage) const {
-    return wring + kRingN * 4 + (uint32_t)(stage % NBUF) * 8;
-  }
-
-  __device__ __forceinline__ uint32_t load_window(int base) const {
-    const int k = base + lane;
-    return k < n ? stream[s0 + k] : 0u;
-  }
-
-  __device__ __forceinline__ void issue_stage() {
-    const int c = issued++;
-    const int e0 = c * CH;
-    if (e0 >= n) return;  // past the end: never waited on
-    if (e0 >= wbase + 32) {
-      wbase += 32;
-      wcur = wnext;
-      wnext = load_window(wbase + 32);
-    }
-    const int slot = (c % NBUF) * CH;
-    const int lim = min(CH, n - e0);
-    const int j = NG == 1 ? lane : (lane & 15);
-    const uint32_t mine = __shfl_sync(kFull, wcur, (e0 - wbase + j) & 31);
-    const uint32_t b = bar(c);
-    if (lane < lim) sts_u32(wring + (slot + lane) * 4, (mine >> 22) * (uint32_t)kSlot);
-    if (lane == 0) mbar_expect_tx(b, (uint32_t)(lim * nlive * kBlkBytes));
-    if (j < lim && (NG == 2 || lane < CH) && cp_ok)
-      bulk_g2s(ring + (slot + j) * kSlot + (NG == 1 ? 0 : (lane >> 4) * kBlkBytes),
-               src + (size_t)(mine & 0x3fffffu) * kBlk, kBlkBytes, b);
-  }
-
-  __device__ __forceinline__ void begin(const uint32_t* st, int start, int end) {
-    stream = st;
-    s0 = start;
-    n = end - start;
-    issued = 0;
-    ready_upto = 0;
-    q = 0;
-    wbase = 0;
-    if (lane < NBUF) mbar_init(bar(lane), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    __syncwarp();
-    wcur = load_window(0);
-    wnext = load_window(32);
-#pragma unroll 1
-    for (int k = 0; k < NBUF - 2; ++k) issue_stage();
-  }
-
-  __device__ __forceinline__ void ensure(int e) {
-    while (e >= ready_upto) {
-      const int st = ready_upto / CH;
-      mbar_wait(bar(st), (uint32_t)(st / NBUF) & 1u);
-      __syncwarp();
-      issue_stage();
-      ready_upto += CH;
-    }
-  }
-
-  __device__ __forceinline__ uint32_t slot_base(int e) const {
-    return ring + ((uint32_t)e % (uint32_t)kRingN) * kSlot;
-  }
-
-  __device__ __forceinline__ uint32_t lofs(int e) const {
-    return lds_u32(wring + ((uint32_t)e % (uint32_t)kRingN) * 4);
-  }
-
-  __device__ __forceinline__ void finish() { __syncwarp(); }
 };
 
 // block-region entry `ent` of block element e, scenario sc (B = group block base + 2*sc).
@@ -535,7 +413,7 @@ __device__ __forceinline__ void pipe_setup(P& pp, const NrDeviceModel& m, const 
   const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
   const int half = lane >> 4, chunk = lane & 15;
   const int h = P::NG == 1 ? 0 : half;
-  pp.src = w.arena + (size_t)(g0 + h) * gstride + (P::kBulk ? 0 : chunk * 2);
+  pp.src = w.arena + (size_t)(g0 + h) * gstride + chunk * 2;
   pp.cp_ok = (live >> h) & 1u;
   pp.nlive = __popc(live);
   pp.ring = ring;
@@ -846,33 +724,19 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
-// pipeline variants
-using V0 = PipeLdgsts<1, 8, 8>;  // LDGSTS, 1 group per warp
-using V1 = PipeLdgsts<2, 4, 8>;  // LDGSTS, 2 groups per warp
-using V2 = PipeBulk<1, 8, 8>;    // bulk copies, 1 group per warp
-using V3 = PipeBulk<1, 4, 16>;   // bulk copies, finer stages
-using V4 = PipeBulk<2, 4, 8>;    // bulk copies, 2 groups per warp
-using V5 = PipeLdgsts<1, 4, 8>;  // LDGSTS, half-size ring (more resident warps)
-using V6 = PipeLdgsts<1, 4, 16>; // LDGSTS, finer stages, same ring
-using V7 = PipeLdgsts<1, 8, 4>;  // LDGSTS, half-size ring, 2 stages in flight
-using V8 = PipeLdgsts<1, 4, 4>;  // LDGSTS, quarter-size ring
-using V9 = PipeLdgsts<1, 2, 8>;  // LDGSTS, quarter-size ring, 2-element stages
-using V10 = PipeLdgsts<2, 4, 4>; // LDGSTS, 2 groups, half-size ring
+// pipeline variants (ACPF_NR_VARIANT; measured one-step times on gb2224 x 65536
+// in DESIGN.md): ring of 8 x 8 elements (6 stages in flight, ~11 warps/SM),
+// 8 x 4 (2 in flight, 8 KB, ~19 warps/SM, the default) and 4 x 4
+using V0 = PipeLdgsts<1, 8, 8>;
+using V1 = PipeLdgsts<1, 8, 4>;
+using V2 = PipeLdgsts<1, 4, 4>;
 
 template <class F>
 auto with_variant(int v, F&& f) {
   switch (v) {
-    case 1: return f(V1{});
+    case 0: return f(V0{});
     case 2: return f(V2{});
-    case 3: return f(V3{});
-    case 4: return f(V4{});
-    case 5: return f(V5{});
-    case 6: return f(V6{});
-    case 7: return f(V7{});
-    case 8: return f(V8{});
-    case 9: return f(V9{});
-    case 10: return f(V10{});
-    default: return f(V0{});
+    default: return f(V1{});
   }
 }
 
