@@ -1,0 +1,105 @@
+"""Scale-level golden summaries from the REAL reference (build container only).
+
+    PYTHONDONTWRITEBYTECODE=1 python tools/make_golden_scale.py [--ref /root/reference/pkg/src]
+
+Solves 256 seeded GBnetwork scenarios (seed 10010, the acceptance seed) with
+the reference's `newton_solve` and 512 seeded EULV scenarios (seed 10011) with
+`zbus_iterate`, through the reference's public API, on a process pool. The
+scenario inputs are not stored (they are the reference generator's rows
+0..count-1, reproduced bitwise by the engine); stored are the per-scenario
+flags, iteration counts, GMRES totals, residuals, fixed-order state summaries
+and the full state of every 32nd scenario. tests/test_gpu_scale.py checks the
+CUDA path against them.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import sys
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "tests" / "golden"
+FIX = ROOT / "fixtures"
+REF = "/root/reference/pkg/src"
+NR_COUNT, ZB_COUNT, KEEP_EVERY = 256, 512, 32
+
+_state = {}
+
+
+def _text(name: str) -> str:
+    p = FIX / name
+    if p.exists():
+        return p.read_text()
+    with gzip.open(str(p) + ".gz", "rt") as fh:
+        return fh.read()
+
+
+def _init(ref: str):
+    sys.path.insert(0, ref)
+    import acpflow as ac
+    _state["ac"] = ac
+    net = ac.parse_matpower_case(_text("gb2224.m"))
+    model = ac.build_transmission_model(net)
+    base = ac.transmission_base(net, model.part)
+    mult = ac.generate_load_multipliers(ac.ScenarioSpec(count=NR_COUNT, seed=10010, spread=0.2),
+                                        base.n_elements)
+    _state["nr"] = (model, base, mult)
+    dnet = ac.parse_distribution_json(_text("eulv.json"))
+    dmodel = ac.build_zbus_model(dnet)
+    dbase = ac.distribution_base(dmodel)
+    dmult = ac.generate_load_multipliers(
+        ac.ScenarioSpec(count=ZB_COUNT, seed=10011, spread=0.2, target="distribution"), dbase.n_elements)
+    _state["zb"] = (dmodel, dbase, dmult)
+
+
+def _nr(i: int):
+    ac = _state["ac"]
+    model, base, mult = _state["nr"]
+    r = ac.newton_solve(model, ac.apply_multipliers(base, mult[i]))
+    return (r.converged, r.iterations, r.total_gmres_iterations, r.final_mismatch_inf, r.state.theta,
+            r.state.vmag)
+
+
+def _zb(i: int):
+    ac = _state["ac"]
+    model, base, mult = _state["zb"]
+    r = ac.zbus_iterate(model, ac.apply_multipliers(base, mult[i]))
+    return r.converged, r.iterations, r.final_delta, r.residual_inf, r.v
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default=REF)
+    ap.add_argument("--workers", type=int, default=8)
+    args = ap.parse_args()
+    with ProcessPoolExecutor(args.workers, initializer=_init, initargs=(args.ref,)) as ex:
+        nr = list(ex.map(_nr, range(NR_COUNT), chunksize=4))
+        zb = list(ex.map(_zb, range(ZB_COUNT), chunksize=8))
+    keep = np.arange(0, NR_COUNT, KEEP_EVERY)
+    th = np.array([r[4] for r in nr])
+    vm = np.array([r[5] for r in nr])
+    np.savez_compressed(
+        OUT / "scale_nr_gb2224.npz", seed=10010, count=NR_COUNT,
+        converged=np.array([r[0] for r in nr]), iterations=np.array([r[1] for r in nr]),
+        gmres_total=np.array([r[2] for r in nr]), fnorm=np.array([r[3] for r in nr]),
+        theta_sum=th.sum(1), vmag_sum=vm.sum(1), vmag_min=vm.min(1), vmag_max=vm.max(1),
+        keep=keep, theta=th[keep], vmag=vm[keep])
+    keepz = np.arange(0, ZB_COUNT, KEEP_EVERY)
+    v = np.array([r[4] for r in zb])
+    np.savez_compressed(
+        OUT / "scale_zb_eulv.npz", seed=10011, count=ZB_COUNT,
+        converged=np.array([r[0] for r in zb]), iterations=np.array([r[1] for r in zb]),
+        final_delta=np.array([r[2] for r in zb]), residual=np.array([r[3] for r in zb]),
+        vabs_sum=np.abs(v).sum(1), vabs_min=np.abs(v).min(1), keep=keepz, v=v[keepz])
+    print("NR iterations", np.unique([r[1] for r in nr], return_counts=True))
+    print("ZB iterations", np.unique([r[1] for r in zb], return_counts=True))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
