@@ -47,7 +47,8 @@ constexpr int kRowGroups = 8 / kRowWarps;
 #endif
 constexpr int kColWarps = ACPF_ZB_COL_WARPS;
 constexpr int kThreads = kRowWarps * kColWarps * 32;
-constexpr int kMaxKsPerStage = 16;
+constexpr int kMaxKsPerStage = 16;  // k-steps (of 4) per Z stage
+constexpr int kZbBuf = 2;            // Z stage buffers (TMA ring; 4 x half-K stages measured 2% slower)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -152,8 +153,8 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     const double* src;
     uint32_t bytes;
     stage_src(sidx, src, bytes);
-    double* dst = zs + (sidx & 1) * stage_doubles;
-    uint64_t* bar = bars + (sidx & 1);
+    double* dst = zs + (sidx % kZbBuf) * stage_doubles;
+    uint64_t* bar = bars + (sidx % kZbBuf);
     mbar_expect_tx(bar, bytes);
     for (uint32_t off = 0; off < bytes; off += 32768u) {
       const uint32_t chunk = min(32768u, bytes - off);
@@ -162,17 +163,17 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
   };
 
-  // bars[0..1]: stage full (TMA tx count); bars[2..3]: stage empty (one
-  // arrive per warp once its DMMAs on the stage are issued and complete).
-  // Thread 0 refills a buffer only after all warps released it, so warps may
-  // drift by up to one stage and a warp's epilogue overlaps the DMMA work of
-  // the others. Empty-barrier parities live in bits 2..3 of phase_bits.
+  // bars[0..kZbBuf): stage full (TMA tx count); bars[kZbBuf..2 kZbBuf): stage
+  // empty (one arrive per warp once its DMMAs on the stage are issued and
+  // complete). Thread 0 refills a buffer only after all warps released it, so
+  // warps may drift by up to kZbBuf-1 stages and a warp's epilogue overlaps
+  // the DMMA work of the others. Empty-barrier parities live in bits
+  // kZbBuf.. of phase_bits.
   if (tid == 0) {
     // the stage buffers may have been generic-proxy scratch since the last
     // pass (zb_injection_cta): order those accesses before the bulk writes
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    issue(0);
-    if (n_stage > 1) issue(1);
+    for (int k = 0; k < kZbBuf && k < n_stage; ++k) issue(k);
   }
 
   double cr[kRowGroups][CGW][2], ci[kRowGroups][CGW][2];
@@ -183,7 +184,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   for (int b = 0; b < CGW; ++b) acc[b][0] = acc[b][1] = 0.0;
   for (int sidx = 0; sidx < n_stage; ++sidx) {
     const int rb = sidx / n_kc, kc = sidx % n_kc;
-    const int buf = sidx & 1;
+    const int buf = sidx % kZbBuf;
     if (kc == 0) {
 #pragma unroll
       for (int a = 0; a < kRowGroups; ++a)
@@ -223,11 +224,11 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
     // release the stage buffer (all lanes' shared reads of zb are done)
     __syncwarp();
-    if (lane == 0) mbar_arrive(bars + 2 + buf);
-    if (tid == 0 && sidx + 2 < n_stage) {
-      mbar_wait(bars + 2 + buf, (phase_bits >> (2 + buf)) & 1u);
-      phase_bits ^= (1u << (2 + buf));
-      issue(sidx + 2);
+    if (lane == 0) mbar_arrive(bars + kZbBuf + buf);
+    if (tid == 0 && sidx + kZbBuf < n_stage) {
+      mbar_wait(bars + kZbBuf + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
+      phase_bits ^= (1u << (kZbBuf + buf));
+      issue(sidx + kZbBuf);
     }
     if (kc == n_kc - 1) {
       // ---- epilogue for row block rb (no CTA-wide synchronisation)
@@ -266,12 +267,12 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
   }
   // the empty-barrier phases of the stages whose refill was not needed
-  // (the last two) still advance: keep thread 0's parity bits in sync
+  // (the last kZbBuf) still advance: keep thread 0's parity bits in sync
   if (tid == 0) {
-    for (int sidx = (n_stage > 2 ? n_stage - 2 : 0); sidx < n_stage; ++sidx) {
-      const int buf = sidx & 1;
-      mbar_wait(bars + 2 + buf, (phase_bits >> (2 + buf)) & 1u);
-      phase_bits ^= (1u << (2 + buf));
+    for (int sidx = (n_stage > kZbBuf ? n_stage - kZbBuf : 0); sidx < n_stage; ++sidx) {
+      const int buf = sidx % kZbBuf;
+      mbar_wait(bars + kZbBuf + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
+      phase_bits ^= (1u << (kZbBuf + buf));
     }
   }
   // ---- per-pass column reduction: 8 row lanes (fixed butterfly), then the
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ksteps = m.kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
   double* zs = reinterpret_cast<double*>(smem_raw);
-  double* isf = zs + 2 * stage_doubles;
+  double* isf = zs + kZbBuf * stage_doubles;
   double* colsum = isf + (size_t)ksteps * NT * 8;
   double* red = colsum + NT;
   double* mag = red + kRowWarps * NT;
@@ -454,10 +455,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(bars + 0, 1);
-    mbar_init(bars + 1, 1);
-    mbar_init(bars + 2, kThreads / 32);
-    mbar_init(bars + 3, kThreads / 32);
+    for (int b = 0; b < kZbBuf; ++b) {
+      mbar_init(bars + b, 1);                      // stage full (TMA transaction count)
+      mbar_init(bars + kZbBuf + b, kThreads / 32);  // stage empty (one arrive per warp)
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ZbTileState st{colsum, red, run, cert};
   // the CTA-wide injection needs [NT][n_l] voltages + [NT][loads] currents of
   // scratch in the (then idle) Z stage buffers
-  const bool par_inj = (size_t)NT * (m.n_l + m.n_wye + m.n_delta) * 2 <= 2 * (size_t)stage_doubles;
+  const bool par_inj = (size_t)NT * (m.n_l + m.n_wye + m.n_delta) * 2 <= kZbBuf * (size_t)stage_doubles;
 
   if (mag0_mode) {
     for (int k = tid; k < ksteps * NT * 8; k += kThreads) isf[k] = 0.0;
@@ -584,8 +585,8 @@ template <int NT>
 size_t zbus_smem_bytes(int kpad) {
   const int ksteps = kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
-  size_t d = 2 * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kRowWarps * NT + 3 * NT;
-  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 32 + 16;
+  size_t d = kZbBuf * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kRowWarps * NT + 3 * NT;
+  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 16 * kZbBuf + 16;
   return bytes;
 }
 
