@@ -246,8 +246,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     // factor pipeline variant: the requested one if its shared memory (ring +
     // the longest L part of a row) fits one SM, else the next smaller one
     constexpr size_t kSmemMax = 227 * 1024;
-    int v = (int)env_int("ACPF_NR_VARIANT", 1);
-    v = v < 0 ? 0 : (v > 2 ? 2 : v);
+    int v = (int)env_int("ACPF_NR_VARIANT", 3);
+    v = v < 0 ? 0 : (v > 3 ? 3 : v);
     if (nr_smem_bytes(v, sc.max_l) > kSmemMax) v = 0;
     if (nr_smem_bytes(v, sc.max_l) > kSmemMax) {
       set_error("acpf_nr_plan_create: an L row of " + std::to_string(sc.max_l) +

@@ -52,7 +52,7 @@ struct NrHostSchedule {
   const int32_t* level_maxl;       // [n_levels]
   const int32_t* blevel_task_ptr;  // [n_blevels+1]
   int n_levels, n_blevels, max_l;
-  int variant;  // factor/back pipeline shape (nr_kernel.cu: 0 = 8x8 ring, 1 = 8x4 (default), 2 = 4x4)
+  int variant;  // factor/back pipeline shape (nr_kernel.cu: 0 = 8x8 ring, 1 = 8x4, 2 = 4x4, 3 = mixed (default))
 };
 
 struct NrWorkspace {

@@ -732,7 +732,7 @@ using V1 = PipeLdgsts<1, 8, 4>;
 using V2 = PipeLdgsts<1, 4, 4>;
 
 template <class F>
-auto with_variant(int v, F&& f) {
+auto with_variant(int v, F&& f) {  // 3 (mixed) sizes like 1
   switch (v) {
     case 0: return f(V0{});
     case 2: return f(V2{});
@@ -754,13 +754,25 @@ size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
 namespace {
 
 template <class P>
+void launch_factor_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t units,
+                         int l, cudaStream_t stream) {
+  const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
+  nr_factor_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(
+      m, w, k0, units);
+}
+
+// mixed: levels with several tasks per group take the 4x4 ring (more
+// resident warps), single-task levels (the chain) the 8x4 ring (deeper
+// per-warp pipeline where the L-row buffer limits residency)
+template <class P>
 void launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t groups,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, bool mixed = false) {
   const int64_t units = (groups + P::NG - 1) / P::NG;
   for (int l = 0; l < hs.n_levels; ++l) {
-    const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
-    nr_factor_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(
-        m, w, k0, units);
+    if (mixed && hs.level_task_ptr[l + 1] - hs.level_task_ptr[l] > 1)
+      launch_factor_level<V2>(m, hs, w, units, l, stream);
+    else
+      launch_factor_level<P>(m, hs, w, units, l, stream);
   }
   for (int l = 0; l < hs.n_blevels; ++l) {
     const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
@@ -774,7 +786,12 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
                              int* launches) {
   const int v = hs.variant;
-  cudaError_t e = with_variant(v, [&](auto p) {
+  if (v == 3) {  // mixed: the 4x4 factor kernel is launched too
+    cudaError_t e2 = cudaFuncSetAttribute(nr_factor_kernel<V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(V2::smem_bytes() + (size_t)hs.max_l * V2::kSlot));
+    if (e2 != cudaSuccess) return e2;
+  }
+  cudaError_t e = with_variant(v == 3 ? 1 : v, [&](auto p) {
     using P = decltype(p);
     return cudaFuncSetAttribute(nr_factor_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(P::smem_bytes() + (size_t)hs.max_l * P::kSlot));
@@ -799,7 +816,10 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
-    with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, stream); });
+    if (v == 3)
+      launch_levels<V1>(m, hs, w, groups, stream, true);
+    else
+      with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, stream); });
     nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
     nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);
     nl += hs.n_levels + hs.n_blevels + 2;
