@@ -48,7 +48,10 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlk = 4 * kGroup;      // doubles per block element (32)
 constexpr int kBlkBytes = kBlk * 8;   // 256
 constexpr int kHalf = kBlkBytes / 2;  // bytes of one block column of the group (128)
-constexpr int kBusChunk = 64;
+#ifndef ACPF_NR_BUS_CHUNK
+#define ACPF_NR_BUS_CHUNK 16  // 64: mismatch 9.6 ms, 16: 8.3 ms, 8: 8.0 ms, 4: 10.7 ms (gb2224 x 65536)
+#endif
+constexpr int kBusChunk = ACPF_NR_BUS_CHUNK;  // buses per warp in the per-bus kernels
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
