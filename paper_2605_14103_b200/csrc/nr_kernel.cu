@@ -33,10 +33,11 @@
 // Inside a factor/back task every operand not produced by the task itself
 // (earlier U blocks, pivot-block inverses, y/x, assembled J blocks) is a
 // precomputed element index in a gather stream; the warp runs a cp.async
-// (LDGSTS) multistage pipeline over it (8 elements per stage, 6 stages in
-// flight) into a shared-memory ring. No element of a task can be produced by
-// another task of the same level, so the pipeline needs no hazard checks.
-// The row's own L blocks stay in shared memory (later rows only read U).
+// (LDGSTS) multistage pipeline over it into a small shared-memory ring
+// (PipeLdgsts; 4- or 8-element stages, 2 stages in flight, so ~20 warps stay
+// resident per SM). No element of a task can be produced by another task of
+// the same level, so the pipeline needs no hazard checks. The row's own L
+// blocks stay in shared memory (later rows only read U).
 
 #include "acpf_internal.cuh"
 
