@@ -630,7 +630,14 @@ void zbus_pack_fragments(const double* zl, int n, int n_l, int n_rb, int kpad, d
 cudaError_t launch_zbus(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter,
                         bool mag0_mode, double* mag0_out, int* launches, cudaStream_t stream) {
   if (launches) *launches = 1;
-  if (m.kpad <= 64) return launch_nt<64>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
+  // 64-scenario tiles unless that leaves SMs idle (small batches) or the load
+  // columns need the 32-wide tile's smaller I_l; per-column reduction orders
+  // do not depend on the tile width, so both give the same bits
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool small = !mag0_mode && (io.batch + 63) / 64 < sms;
+  if (m.kpad <= 64 && !small) return launch_nt<64>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
   return launch_nt<32>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
 }
 
