@@ -51,7 +51,8 @@ typedef int32_t acpf_status;
 #define ACPF_EINVAL (-1)  /* bad argument / inconsistent sizes            */
 #define ACPF_ECUDA (-2)   /* CUDA runtime error (message has details)     */
 #define ACPF_ENOMEM (-3)  /* device or host allocation failed             */
-#define ACPF_ESTRUCT (-4) /* structurally singular Jacobian pattern       */
+#define ACPF_ESTRUCT (-4) /* structural problem: singular pattern/matrix, */
+                          /* or a network beyond the kernels' limits     */
 
 #define ACPF_HOST_PTRS 0u
 #define ACPF_DEVICE_PTRS 1u
@@ -84,12 +85,13 @@ typedef struct acpf_nr_plan_info {
   int32_t n_bus;        /* buses                                        */
   int32_t n_theta;      /* |PV| + |PQ|  (angle unknowns)                */
   int32_t n_q;          /* |PQ|         (magnitude unknowns)            */
-  int32_t n_j;          /* n_theta + n_q                                */
+  int32_t n_j;          /* block rows (= n_theta, one 2x2 block per     */
+                        /* non-slack bus; PV buses padded)              */
   int32_t nnz_y;        /* Ybus nonzeros                                */
-  int32_t nnz_j;        /* Jacobian nonzeros                            */
-  int64_t nnz_lu;       /* static-pivot L+U slots (incl. fill)          */
-  int64_t n_pairs;      /* multiply-adds of one refactorisation         */
-  int32_t group;        /* scenarios interleaved per warp (32)          */
+  int32_t nnz_j;        /* Jacobian 2x2 blocks (Ybus pattern, no slack) */
+  int64_t nnz_lu;       /* static-pivot L+U 2x2 blocks (incl. fill)     */
+  int64_t n_pairs;      /* 2x2-block Crout updates of one refactorisation */
+  int32_t group;        /* scenarios interleaved per warp (8)           */
   int32_t etree_height; /* informational                                */
   int64_t workspace_bytes_per_group;
 } acpf_nr_plan_info;
@@ -103,9 +105,12 @@ typedef struct acpf_nr_plan_info {
  *                 (network.py:499-516)
  *   theta_init, vmag_init   flat start incl. pinned slack/PV values
  *                 (transmission.py:169-177), len n_bus.
- *   perm          fill-reducing ordering of the n_theta+n_q unknowns
- *                 (perm[k] = packed unknown eliminated k-th) or NULL for the
- *                 built-in minimum-degree ordering.                        */
+ *   perm          fill-reducing ordering of the n_theta block rows (one
+ *                 2x2 block per non-slack bus): perm[k] = index into
+ *                 theta_block of the bus eliminated k-th; NULL for the
+ *                 built-in minimum-degree ordering. Rows are then
+ *                 level-sorted (a topological order of the elimination tree,
+ *                 same fill).                                              */
 acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_rowptr,
                                 const int32_t* y_col, const double* y_re, const double* y_im,
                                 int32_t n_theta, const int32_t* theta_block, int32_t n_q,
