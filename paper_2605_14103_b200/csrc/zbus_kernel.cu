@@ -142,19 +142,25 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   const int n_stage = m.n_rb * n_kc;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
 
-  auto stage_src = [&](int sidx, const double*& src, uint32_t& bytes) {
+  // Each stage is two row halves (rows 0-31 / 32-63 of the row block), each
+  // a contiguous fragment block streamed by its own bulk copy onto its own
+  // full barrier and released through its own empty barrier by the 16 warps
+  // that read it; a leader thread per half refills it. The two halves of the
+  // CTA thus only share I_l (constant during a pass) and drift independently.
+  constexpr int kHalfRW = kRowWarps / 2;        // row warps per half
+  const int half = rp / kHalfRW;
+  const bool leader = (rp % kHalfRW) == 0 && ch == 0 && lane == 0;
+  const int half_doubles = stage_doubles / 2;
+  uint64_t* const fullb = bars + half * kZbBuf;                // [kZbBuf] of this half
+  uint64_t* const emptyb = bars + 2 * kZbBuf + half * kZbBuf;  // [kZbBuf] of this half
+  auto issue = [&](int sidx) {
     const int rb = sidx / n_kc, kc = sidx % n_kc;
     const int ks0 = kc * kMaxKsPerStage;
     const int nks = min(kMaxKsPerStage, ksteps - ks0);
-    src = m.zfrag + ((size_t)rb * ksteps + ks0) * 512;
-    bytes = (uint32_t)nks * 512 * 8;
-  };
-  auto issue = [&](int sidx) {
-    const double* src;
-    uint32_t bytes;
-    stage_src(sidx, src, bytes);
-    double* dst = zs + (sidx % kZbBuf) * stage_doubles;
-    uint64_t* bar = bars + (sidx % kZbBuf);
+    const double* src = m.zfrag + (((size_t)rb * 2 + half) * ksteps + ks0) * 256;
+    const uint32_t bytes = (uint32_t)nks * 256 * 8;
+    double* dst = zs + (sidx % kZbBuf) * stage_doubles + half * half_doubles;
+    uint64_t* bar = fullb + (sidx % kZbBuf);
     mbar_expect_tx(bar, bytes);
     for (uint32_t off = 0; off < bytes; off += 32768u) {
       const uint32_t chunk = min(32768u, bytes - off);
@@ -163,13 +169,11 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
   };
 
-  // bars[0..kZbBuf): stage full (TMA tx count); bars[kZbBuf..2 kZbBuf): stage
-  // empty (one arrive per warp once its DMMAs on the stage are issued and
-  // complete). Thread 0 refills a buffer only after all warps released it, so
-  // warps may drift by up to kZbBuf-1 stages and a warp's epilogue overlaps
-  // the DMMA work of the others. Empty-barrier parities live in bits
-  // kZbBuf.. of phase_bits.
-  if (tid == 0) {
+  // full barriers: TMA transaction count; empty barriers: one arrive per warp
+  // of the half once its DMMAs on the stage are issued and complete. Parities:
+  // full in bits 0..kZbBuf-1, empty (leaders only) in bits kZbBuf.. of
+  // phase_bits.
+  if (leader) {
     // the stage buffers may have been generic-proxy scratch since the last
     // pass (zb_injection_cta): order those accesses before the bulk writes
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -191,18 +195,18 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
 #pragma unroll
         for (int b = 0; b < CGW; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
     }
-    mbar_wait(bars + buf, (phase_bits >> buf) & 1u);
+    mbar_wait(fullb + buf, (phase_bits >> buf) & 1u);
     phase_bits ^= (1u << buf);
-    const double* zb = zs + buf * stage_doubles;
+    const double* zb = zs + buf * stage_doubles + half * half_doubles;
     const int ks0 = kc * kMaxKsPerStage;
     const int nks = min(kMaxKsPerStage, ksteps - ks0);
     for (int ks = 0; ks < nks; ++ks) {
       double ar[kRowGroups], ai[kRowGroups], br[CGW], bi[CGW];
 #pragma unroll
       for (int a = 0; a < kRowGroups; ++a) {
-        const int rg = rp * kRowGroups + a;
-        ar[a] = zb[((ks * 8 + rg) * 2 + 0) * 32 + lane];
-        ai[a] = zb[((ks * 8 + rg) * 2 + 1) * 32 + lane];
+        const int rg = (rp % kHalfRW) * kRowGroups + a;  // row group within the half
+        ar[a] = zb[((ks * 4 + rg) * 2 + 0) * 32 + lane];
+        ai[a] = zb[((ks * 4 + rg) * 2 + 1) * 32 + lane];
       }
 #pragma unroll
       for (int b = 0; b < CGW; ++b) {
@@ -224,9 +228,9 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
     }
     // release the stage buffer (all lanes' shared reads of zb are done)
     __syncwarp();
-    if (lane == 0) mbar_arrive(bars + kZbBuf + buf);
-    if (tid == 0 && sidx + kZbBuf < n_stage) {
-      mbar_wait(bars + kZbBuf + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
+    if (lane == 0) mbar_arrive(emptyb + buf);
+    if (leader && sidx + kZbBuf < n_stage) {
+      mbar_wait(emptyb + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
       phase_bits ^= (1u << (kZbBuf + buf));
       issue(sidx + kZbBuf);
     }
@@ -268,10 +272,10 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   }
   // the empty-barrier phases of the stages whose refill was not needed
   // (the last kZbBuf) still advance: keep thread 0's parity bits in sync
-  if (tid == 0) {
+  if (leader) {
     for (int sidx = (n_stage > kZbBuf ? n_stage - kZbBuf : 0); sidx < n_stage; ++sidx) {
       const int buf = sidx % kZbBuf;
-      mbar_wait(bars + kZbBuf + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
+      mbar_wait(emptyb + buf, (phase_bits >> (kZbBuf + buf)) & 1u);
       phase_bits ^= (1u << (kZbBuf + buf));
     }
   }
@@ -455,9 +459,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int b = 0; b < kZbBuf; ++b) {
-      mbar_init(bars + b, 1);                      // stage full (TMA transaction count)
-      mbar_init(bars + kZbBuf + b, kThreads / 32);  // stage empty (one arrive per warp)
+    for (int b = 0; b < 2 * kZbBuf; ++b) {
+      mbar_init(bars + b, 1);                              // half-stage full (TMA transaction count)
+      mbar_init(bars + 2 * kZbBuf + b, kThreads / 64);     // half-stage empty (one arrive per warp of the half)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -586,7 +590,7 @@ size_t zbus_smem_bytes(int kpad) {
   const int ksteps = kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
   size_t d = kZbBuf * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kRowWarps * NT + 3 * NT;
-  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 16 * kZbBuf + 16;
+  size_t bytes = d * 8 + (5 * NT + 2) * 4 + 32 * kZbBuf + 16;
   return bytes;
 }
 
@@ -611,17 +615,19 @@ cudaError_t launch_nt(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, i
 size_t zbus_frag_doubles(int n_rb, int kpad) { return (size_t)n_rb * (kpad >> 2) * 512; }
 
 // Host: pack Z[:, l] ([n][n_l] interleaved complex) into DMMA A-fragment
-// order: [row block][kstep][row group 0..7][re|im][lane], lane t holds
-// Z[rb*64 + rg*8 + t/4][ks*4 + t%4] (zero padded).
+// order: [row block][row half][kstep][row group 0..3][re|im][lane], lane t
+// holds Z[rb*64 + (4*half + rg)*8 + t/4][ks*4 + t%4] (zero padded); each row
+// half of a stage is one contiguous bulk copy.
 void zbus_pack_fragments(const double* zl, int n, int n_l, int n_rb, int kpad, double* out) {
   const int ksteps = kpad >> 2;
   size_t o = 0;
   for (int rb = 0; rb < n_rb; ++rb)
+    for (int half = 0; half < 2; ++half)
     for (int ks = 0; ks < ksteps; ++ks)
-      for (int rg = 0; rg < 8; ++rg)
+      for (int rg = 0; rg < 4; ++rg)
         for (int comp = 0; comp < 2; ++comp)
           for (int t = 0; t < 32; ++t) {
-            const int row = rb * kZbRows + rg * 8 + (t >> 2);
+            const int row = rb * kZbRows + (4 * half + rg) * 8 + (t >> 2);
             const int k = ks * 4 + (t & 3);
             out[o++] = (row < n && k < n_l) ? zl[((size_t)row * n_l + k) * 2 + comp] : 0.0;
           }
