@@ -38,3 +38,22 @@ def test_solve_and_verify_on_gpu(tmp_path):
     csv = tmp_path / "b.csv"
     assert cli.main(["bench", "--case", "ieee13", "--batch", "64", "--out", str(csv)]) == 0
     assert csv.read_text().splitlines()[0].startswith("case,kind,batch_size")
+
+
+@pytest.mark.gpu
+def test_solve_with_gmres_step_on_gpu(tmp_path):
+    # --step gmres --precond fd|none: the reference's own Newton step on the GPU
+    for pre in ("fd", "none"):
+        out = tmp_path / f"g_{pre}.json"
+        assert cli.main(["solve", "--case", "case14", "--batch", "8", "--seed", "1010", "--step", "gmres",
+                         "--precond", pre, "--out", str(out)]) == 0
+        doc = json.loads(out.read_text())
+        assert doc["report"]["aggregate"]["n_converged"] == 8
+
+
+def test_step_option_validated():
+    from paper_2605_14103_b200 import transmission as tm
+    with pytest.raises(ValueError):
+        tm.NewtonOptions(step="cg")
+    with pytest.raises(SystemExit):
+        cli.build_parser().parse_args(["solve", "--case", "case14", "--step", "cg"])
