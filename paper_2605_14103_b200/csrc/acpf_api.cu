@@ -228,7 +228,6 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   d.n_block = sc.n_block;
   d.n_scalar = sc.n_scalar;
   d.off_lu = sc.off_lu;
-  d.off_invd = sc.off_invd;
   d.off_yx = sc.off_yx;
   d.off_u = sc.off_u;
   d.off_e = sc.off_e;

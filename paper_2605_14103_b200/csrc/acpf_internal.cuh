@@ -43,7 +43,7 @@ struct NrDeviceModel {
   const uint32_t* stream;     // [n_stream]
   int64_t nnz_lu;
   int64_t n_block, n_scalar;  // arena elements per group (block / scalar region)
-  int64_t off_lu, off_invd, off_yx;                   // block region
+  int64_t off_lu, off_yx;                   // block region
   int64_t off_u, off_e, off_spec, off_th, off_vm;     // scalar region
 };
 

@@ -24,14 +24,18 @@
 //                -> min V <= 0 -> k == max_newton (transmission.py:347-359)
 //   nr_factor    one launch per elimination level: every (block row of the
 //                level, group) pair is an independent warp task computing the
-//                row by block Crout updates + fused forward substitution
+//                row by block Crout updates + fused forward substitution, in
+//                the unit-upper form A = L^ U^ (L^ = L D, U^ = D^-1 U with
+//                D = diag(U_pp)): the pivot inverse stays in registers for the
+//                row's own U^ blocks and y_p, so no later row or the back
+//                substitution ever gathers a pivot inverse
 //   nr_back      one launch per back-substitution level
 //   nr_update    x += dx (transmission.py:378)
 // This replaces the reference's FD-preconditioned GMRES step
 // (transmission.py:361-369) by an exact sparse LU solve (static 2x2 pivots).
 //
 // Inside a factor/back task every operand not produced by the task itself
-// (earlier U blocks, pivot-block inverses, y/x, assembled J blocks) is a
+// (earlier U^ blocks, y/x, assembled J blocks) is a
 // precomputed element index in a gather stream; the warp runs a cp.async
 // (LDGSTS) multistage pipeline over it into a small shared-memory ring
 // (PipeLdgsts; 4- or 8-element stages, 2 stages in flight, so ~20 warps stay
@@ -479,6 +483,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
       for (int h = 0; h < NG; ++h) yacc[h] = lds_f64(sb + h * kBlkBytes);
     }
     ++pp.q;
+    double ir0[NG], ir1[NG];  // row i of inv(U_pp), set at the diagonal slot
     for (;; ++t) {
       if (t - tw == 32) {
         tw += 32;
@@ -537,38 +542,40 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
 #pragma unroll
       for (int h = 0; h < NG; ++h) a[h] = (a[h] + a3[h]) + (a2[h] + a4[h]);
       if (info & kSlotL) {
-        pp.ensure(pp.q + 1);
-        const uint32_t ib = pp.slot_base(pp.q) + offU, yb = pp.slot_base(pp.q + 1) + 16 * sc;
+        // unit-upper form A = L^ U^ (L^ = L D, U^ = D^-1 U, D = diag(U_tt)):
+        // L^_pt is the updated block itself; y_p -= L^_pt y_t
+        pp.ensure(pp.q);
+        const uint32_t yb = pp.slot_base(pp.q) + 16 * sc;
         const uint32_t lb = lbuf + (t - t0) * kSlot + offL + 8 * bj;
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
-          // L_pt = A' inv(U_tt); y_p -= L_pt y_t
-          const double o = __shfl_xor_sync(kFull, a[h], 8);  // entry (i, 1-j)
-          const double ai0 = bj ? o : a[h], ai1 = bj ? a[h] : o;
-          const double2 iv = lds_f64x2(ib + h * kBlkBytes);  // inv[0][j], inv[1][j]
-          const double l = ai0 * iv.x + ai1 * iv.y;
+          const double l = a[h];
           sts_f64(lb + h * kBlkBytes, l);
-          const double lo = __shfl_xor_sync(kFull, l, 8);
+          const double lo = __shfl_xor_sync(kFull, l, 8);  // entry (i, 1-j)
           const double li0 = bj ? lo : l, li1 = bj ? l : lo;
           const double2 yt = lds_f64x2(yb + h * kBlkBytes);
           yacc[h] = fma(-li1, yt.y, fma(-li0, yt.x, yacc[h]));
         }
-        pp.q += 2;
+        pp.q += 1;
       } else {
         const int64_t st = m.off_lu + __shfl_sync(kFull, wstore, t - tw);
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
-          double* const gb = gb0 + h * gstride;
           if (info & kSlotDiag) {
+            // inv(U_pp), kept in registers for the row's U^ blocks and y_p
             const double a00 = __shfl_sync(kFull, a[h], sc), a01 = __shfl_sync(kFull, a[h], 8 + sc);
             const double a10 = __shfl_sync(kFull, a[h], 16 + sc), a11 = __shfl_sync(kFull, a[h], 24 + sc);
             const double det = a00 * a11 - a01 * a10;
             zero |= (det == 0.0 ? 1u : 0u) << h;
             const double rd = 1.0 / det;
-            const double inv = r == 0 ? a11 * rd : (r == 1 ? -a01 * rd : (r == 2 ? -a10 * rd : a00 * rd));
-            if ((live >> h) & 1u) BL(gb, m.off_invd + p, ce) = inv;
+            ir0[h] = bi ? -a10 * rd : a11 * rd;  // inv[i][0]
+            ir1[h] = bi ? a00 * rd : -a01 * rd;  // inv[i][1]
+          } else {
+            // U^_pt = inv(U_pp) A'_pt: column j of A' from the other row's lane
+            const double o = __shfl_xor_sync(kFull, a[h], 16);  // entry (1-i, j)
+            const double c0 = bi ? o : a[h], c1 = bi ? a[h] : o;
+            if ((live >> h) & 1u) BL(gb0 + h * gstride, st, ce) = ir0[h] * c0 + ir1[h] * c1;
           }
-          if ((live >> h) & 1u) BL(gb, st, ce) = a[h];
         }
       }
       if (info & kSlotRowEnd) {
@@ -576,10 +583,11 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         break;
       }
     }
-    if (bj == 0) {
 #pragma unroll
-      for (int h = 0; h < NG; ++h)
-        if ((live >> h) & 1u) BL(gb0 + h * gstride, m.off_yx + p, bi) = yacc[h];
+    for (int h = 0; h < NG; ++h) {  // y_p = inv(U_pp) (b_p - sum_t L^_pt y_t)
+      const double o = __shfl_xor_sync(kFull, yacc[h], 16);  // the other row
+      const double y = ir0[h] * (bi ? o : yacc[h]) + ir1[h] * (bi ? yacc[h] : o);
+      if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = y;
     }
     __syncwarp();  // lbuf of this row complete before the next row of the task reuses it
   }
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
   int rw = r0;
   uint32_t wrow = r0 + lane < r1 ? m.brow[r0 + lane] : 0u;
   uint32_t nrow = r0 + 32 + lane < r1 ? m.brow[r0 + 32 + lane] : 0u;
-  const uint32_t offY = 16 * sc + 8 * bi, offI = 16 * sc + 8 * bi;  // y[i]; inv[i][0] (+kHalf: inv[i][1])
+  const uint32_t offY = 16 * sc + 8 * bi;  // y[i]
   const uint32_t offUp = kHalf * bj + 16 * sc + 8 * bi, offX = 16 * sc + 8 * bj;
   for (int rr = r0; rr < r1; ++rr) {
     if (rr - rw == 32) {
@@ -625,19 +633,17 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
     const uint32_t b = __shfl_sync(kFull, wrow, rr - rw);
     const int p = (int)(b & 0xfffffu);
     const int cnt = (int)(b >> 20);
-    pp.ensure(pp.q + 1);
-    double yi[NG], inv0[NG], inv1[NG], part[NG], part2[NG];
+    pp.ensure(pp.q);
+    double yi[NG], part[NG], part2[NG];
     {
-      const uint32_t yb = pp.slot_base(pp.q) + offY, ib = pp.slot_base(pp.q + 1) + offI;
+      const uint32_t yb = pp.slot_base(pp.q) + offY;
 #pragma unroll
       for (int h = 0; h < NG; ++h) {
         yi[h] = lds_f64(yb + h * kBlkBytes);
-        inv0[h] = lds_f64(ib + h * kBlkBytes);
-        inv1[h] = lds_f64(ib + h * kBlkBytes + kHalf);
-        part[h] = part2[h] = 0.0;  // sum_c U_pc[i][j] x_c[j]
+        part[h] = part2[h] = 0.0;  // sum_c U^_pc[i][j] x_c[j]
       }
     }
-    pp.q += 2;
+    pp.q += 1;
     for (int q = 0; q < cnt;) {
       pp.ensure(pp.q + 1);
       const int nb = min(cnt - q, (pp.ready_upto - pp.q) >> 1);
@@ -666,10 +672,7 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
     for (int h = 0; h < NG; ++h) {
       const double pt = part[h] + part2[h];
       const double po = __shfl_xor_sync(kFull, pt, 8);
-      const double acc = yi[h] - (bj ? po + pt : pt + po);  // (y_p - sum)[i]
-      const double ao = __shfl_xor_sync(kFull, acc, 16);    // the other row
-      const double acc0 = bi ? ao : acc, acc1 = bi ? acc : ao;
-      const double x = inv0[h] * acc0 + inv1[h] * acc1;     // x_p[i]
+      const double x = yi[h] - (bj ? po + pt : pt + po);  // x_p[i] = (y_p - sum_c U^_pc x_c)[i]
       if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = x;
     }
   }

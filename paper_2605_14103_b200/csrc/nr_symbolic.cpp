@@ -272,8 +272,7 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   if (s.n_q != 0) throw std::logic_error("block schedule expects a bus-level symbolic analysis");
   // ---- arena layout
   o.off_lu = 0;
-  o.off_invd = s.nnz_lu;
-  o.off_yx = o.off_invd + nr;
+  o.off_yx = s.nnz_lu;
   o.n_block = o.off_yx + nr;
   int64_t e = 0;
   o.off_u = e;     e += 2 * (int64_t)nb;
@@ -362,8 +361,8 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   }
 
   // ---- factor stream: per block row b_p, then per slot: assembled block
-  // (unless fill), the Crout updates' U blocks (with the L position), and for
-  // an L slot the pivot-block inverse and y of its column
+  // (unless fill), the Crout updates' U^ blocks (with the L position), and for
+  // an L slot y of its column (unit-upper form A = L^ U^, nr_kernel.cu)
   o.stream.clear();
   auto gw = [&](int64_t gidx, int lpos) {
     o.stream.push_back((uint32_t)gidx | ((uint32_t)lpos << 22));
@@ -389,14 +388,11 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
       if (!fill) gw(o.off_lu + st[t], 0);
       for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
         gw(o.off_lu + st[s.pair_u[q]], (int)(s.pair_l[q] - r0));
-      if (t < s.diag[p]) {
-        gw(o.off_invd + s.col[t], 0);
-        gw(o.off_yx + s.col[t], 0);
-      }
+      if (t < s.diag[p]) gw(o.off_yx + s.col[t], 0);  // y_t (unit-upper form: no pivot inverse)
     }
     o.row_sptr[p + 1] = (int32_t)o.stream.size();
   }
-  // ---- back stream: rows by back level; per row y_p, inv(U_pp), then (U_pc, x_c)
+  // ---- back stream: rows by back level; per row y_p, then (U^_pc, x_c)
   std::vector<int32_t> border(nr);
   for (int p = 0; p < nr; ++p) border[p] = p;
   std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
@@ -413,7 +409,6 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     o.brow[r] = (uint32_t)p | ((uint32_t)cnt << 20);
     o.blevel_ptr[blev[p] + 1] = r + 1;
     gw(o.off_yx + p, 0);
-    gw(o.off_invd + p, 0);
     for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
       gw(o.off_lu + st[t], 0);
       gw(o.off_yx + s.col[t], 0);

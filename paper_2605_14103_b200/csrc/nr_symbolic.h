@@ -33,10 +33,10 @@ struct NrSymbolic {
 // (NrSymbolic) is run on that bus graph; its rows/slots are block rows/slots.
 //
 // Arena per scenario group: a block region of 4*kGroup-double elements
-// (LU blocks, pivot-block inverses, y/x 2-vectors padded to 4) followed by a
+// (L^/U^ blocks, y/x 2-vectors padded to 4) followed by a
 // scalar region of kGroup-double elements (per-bus phasors, state, specs).
 struct NrSchedule {
-  int64_t off_lu = 0, off_invd = 0, off_yx = 0, n_block = 0;          // block region
+  int64_t off_lu = 0, off_yx = 0, n_block = 0;                        // block region
   int64_t off_u = 0, off_e = 0, off_spec = 0, off_th = 0, off_vm = 0, n_scalar = 0;
   int max_l = 0;     // longest L part (blocks) of any row
   int n_levels = 0;  // factor levels (etree height)
