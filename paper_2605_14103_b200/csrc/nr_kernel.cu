@@ -458,6 +458,8 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   const uint32_t offL = kHalf * bi + 16 * sc;  // L[i][0], L[i][1] (row i)
   const uint32_t offU = kHalf * bj + 16 * sc;  // U[0][j], U[1][j] (column j)
   const int ce = 2 * bj + bi;                     // this lane's column-major entry
+  // this lane's entry of LU element 0 of group 0 (stores index it by slot)
+  double* const luw = &BL(gb0, m.off_lu, ce);
   const uint32_t lrow = lbuf + offL;
   const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
   P pp;
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         }
         pp.q += 1;
       } else {
-        const int64_t st = m.off_lu + __shfl_sync(kFull, wstore, t - tw);
+        const size_t st = (size_t)(uint32_t)__shfl_sync(kFull, wstore, t - tw) * kBlk;
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
           if (info & kSlotDiag) {
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
             // U^_pt = inv(U_pp) A'_pt: column j of A' from the other row's lane
             const double o = __shfl_xor_sync(kFull, a[h], 16);  // entry (1-i, j)
             const double c0 = bi ? o : a[h], c1 = bi ? a[h] : o;
-            if ((live >> h) & 1u) BL(gb0 + h * gstride, st, ce) = ir0[h] * c0 + ir1[h] * c1;
+            if ((live >> h) & 1u) luw[h * gstride + st] = ir0[h] * c0 + ir1[h] * c1;
           }
         }
       }
