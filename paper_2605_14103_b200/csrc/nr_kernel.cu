@@ -30,7 +30,7 @@
 //                row's own U^ blocks and y_p, so no later row or the back
 //                substitution ever gathers a pivot inverse
 //   nr_back      one launch per back-substitution level
-//   nr_update    x += dx (transmission.py:378)
+//   (next step) nr_phasor applies x += dx (transmission.py:378) first
 // This replaces the reference's FD-preconditioned GMRES step
 // (transmission.py:361-369) by an exact sparse LU solve (static 2x2 pivots).
 //
@@ -261,7 +261,11 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   if (sc == 0) w.gactive[g] = 1;
 }
 
-__global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
+// Applies the previous step's correction x += dx (transmission.py:378) to the
+// scenarios still active (`apply`, every step but the first; scenarios whose
+// factorisation hit a zero pivot were deactivated by nr_zero_pivot_kernel),
+// then u = V e^{j theta}, E = e^{j theta} and the V <= 0 flag.
+__global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w, int apply) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
@@ -269,9 +273,21 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
   const GroupBase gb = group_base(m, w, g, sc);
+  const bool upd = apply && w.active[g * kGroup + sc];
   bool neg = false;
   for (int i = i0 + r; i < i1; i += 4) {
-    const double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
+    double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
+    if (upd) {
+      const int p = m.bus_row[i];
+      if (p >= 0) {
+        t = t + BL(gb.b, m.off_yx + p, 0);
+        SL(gb.s, m.off_th + i) = t;
+        if (m.qidx[i] >= 0) {
+          v = v + BL(gb.b, m.off_yx + p, 1);
+          SL(gb.s, m.off_vm + i) = v;
+        }
+      }
+    }
     double sn, cs;
     sincos(t, &sn, &cs);
     SL(gb.s, m.off_e + 2 * i) = cs;
@@ -681,36 +697,17 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
   pp.finish();
 }
 
-__global__ void nr_update_kernel(NrDeviceModel m, NrWorkspace w, int k) {
-  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
-  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
-  const int64_t g = item / nch;
-  if (g >= w.groups || !w.gactive[g]) return;
-  const int64_t s = g * kGroup + sc;
-  if (!w.active[s]) return;
-  if (w.flags[s] & 8) {  // zero pivot in this step's factorisation: stop here
-    if (item % nch == 0 && r == 0) {
-      w.status[s] = ACPF_NR_ZERO_PIVOT;
-      w.iters[s] = k;
-    }
-    return;
-  }
-  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
-  const GroupBase gb = group_base(m, w, g, sc);
-  for (int i = i0 + r; i < i1; i += 4) {
-    const int p = m.bus_row[i];
-    if (p < 0) continue;
-    SL(gb.s, m.off_th + i) = SL(gb.s, m.off_th + i) + BL(gb.b, m.off_yx + p, 0);
-    if (m.qidx[i] >= 0) SL(gb.s, m.off_vm + i) = SL(gb.s, m.off_vm + i) + BL(gb.b, m.off_yx + p, 1);
-  }
-}
-
-// scenarios whose factorisation hit an exact zero pivot stop (state not updated)
-__global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch) {
+// scenarios whose factorisation hit an exact zero pivot stop here (state not
+// updated): status, iteration count, and out of the active set before the
+// next step's phasor applies the corrections
+__global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch, int k) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch || !w.active[s]) return;
-  if (w.flags[s] & 8) w.active[s] = 0;
+  if (w.flags[s] & 8) {
+    w.status[s] = ACPF_NR_ZERO_PIVOT;
+    w.iters[s] = k;
+    w.active[s] = 0;
+  }
 }
 
 __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
@@ -817,7 +814,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   nr_init_kernel<<<blocks(groups), 32 * wpb, 0, stream>>>(m, w, io);
   ++nl;
   for (int k = 0; k <= max_newton; ++k) {
-    nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w);
+    nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k > 0);
     nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w);
     e = cudaMemsetAsync(w.n_active, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
@@ -832,9 +829,8 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
       launch_levels<V1>(m, hs, w, groups, stream, true);
     else
       with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, stream); });
-    nr_update_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k);
-    nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch);
-    nl += hs.n_levels + hs.n_blevels + 2;
+    nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch, k);
+    nl += hs.n_levels + hs.n_blevels + 1;
   }
   nr_output_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, io);
   ++nl;
