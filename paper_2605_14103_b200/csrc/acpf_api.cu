@@ -101,6 +101,7 @@ struct acpf_nr_plan {
   size_t stage_bytes = 0;
   void* stage_base = nullptr;
   int* host_active = nullptr;
+  NrGraphCache graphs;                  // captured Newton-step sequences
   std::vector<int32_t> h_tpos, h_qidx;  // host copies for scenario generation
   cudaStream_t copy_stream = nullptr;   // host-path H2D/D2H overlap
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_kend[2] = {nullptr, nullptr},
@@ -335,6 +336,12 @@ acpf_status acpf_nr_plan_structure(acpf_nr_plan_t p, int32_t* perm_out, int64_t*
   return ACPF_OK;
 }
 
+// the plan's graph cache unless ACPF_NR_GRAPHS=0 (direct launches)
+static NrGraphCache* nr_graphs(acpf_nr_plan* p) {
+  static const bool on = env_int("ACPF_NR_GRAPHS", 1) != 0;
+  return on ? &p->graphs : nullptr;
+}
+
 static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
   if (p->ws_groups >= groups) return ACPF_OK;
   p->work.release();
@@ -359,6 +366,7 @@ static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
   w.active = (uint8_t*)get(S);
   w.gactive = (int*)get((size_t)groups * 4);
   w.n_active = (int*)get(4);
+  w.kstep = (int*)get(4);
   if (!ok) {
     p->work.release();
     cudaGetLastError();
@@ -464,7 +472,7 @@ static acpf_status nr_solve_host(acpf_nr_plan* p, int64_t batch, int64_t chunk, 
     int nl = 0;
     NrWorkspace wsb = p->ws;
     wsb.groups = (nb + kGroup - 1) / kGroup;
-    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, st, &nl));
+    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, st, &nl, nr_graphs(p)));
     ACPF_CUDA(cudaEventRecord(p->ev1, st));
     ACPF_CUDA(cudaEventRecord(p->ev_kend[c & 1], st));
     launches += nl;
@@ -583,7 +591,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     int nl = 0;
     NrWorkspace wsb = p->ws;  // capacity may exceed this chunk: index by the chunk's groups
     wsb.groups = (nb + kGroup - 1) / kGroup;
-    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol_mismatch, max_newton, st, &nl));
+    ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol_mismatch, max_newton, st, &nl, nr_graphs(p)));
     ACPF_CUDA(cudaEventRecord(p->ev1, st));
     launches += nl;
     if (!dev_ptrs) {
@@ -630,6 +638,8 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
     }
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     if (p->cublas) cublasDestroy((cublasHandle_t)p->cublas);
+    p->graphs.release();
+    if (p->graphs.capture) cudaStreamDestroy(p->graphs.capture);
     if (p->host_active) cudaFreeHost(p->host_active);
     p->work.release();
     p->stage.release();

@@ -68,6 +68,20 @@ struct NrWorkspace {
   int* gactive;     // [groups]
   int* n_active;    // device counter
   int* host_active; // pinned host mirror
+  int* kstep;       // device Newton step counter (kernels read it; graphs stay step-independent)
+};
+
+// Captured per-step launch sequences (CUDA graphs), cached by the plan and
+// re-captured when the chunk size, tolerances or workspace change.
+struct NrGraphCache {
+  cudaStream_t capture = nullptr;  // private stream used only for capture
+  cudaGraphExec_t head = nullptr;  // phasor, mismatch, check, D2H of the active count
+  cudaGraphExec_t body = nullptr;  // factor levels, back levels, zero-pivot, step++
+  int64_t groups = -1, batch = -1;
+  double tol = 0.0;
+  int max_newton = -1;
+  const double* arena = nullptr;
+  void release();
 };
 
 struct NrBatchIO {
@@ -87,7 +101,7 @@ size_t nr_smem_bytes(int variant, int cap);
 size_t nr_group_state_bytes();
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
-                             int* launches);
+                             int* launches, NrGraphCache* graphs = nullptr);
 
 // ---------------------------------------------------------------------------
 // Z-Bus plan

@@ -252,6 +252,7 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
     }
   }
   if (r) return;
+  if (g == 0 && sc == 0) *w.kstep = 0;
   w.active[s] = valid;
   w.status[s] = 0;
   w.iters[s] = 0;
@@ -265,7 +266,7 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
 // scenarios still active (`apply`, every step but the first; scenarios whose
 // factorisation hit a zero pivot were deactivated by nr_zero_pivot_kernel),
 // then u = V e^{j theta}, E = e^{j theta} and the V <= 0 flag.
-__global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w, int apply) {
+__global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
@@ -273,7 +274,7 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w, int apply) {
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
   const GroupBase gb = group_base(m, w, g, sc);
-  const bool upd = apply && w.active[g * kGroup + sc];
+  const bool upd = *w.kstep > 0 && w.active[g * kGroup + sc];
   bool neg = false;
   for (int i = i0 + r; i < i1; i += 4) {
     double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
@@ -382,8 +383,9 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
   if (bad) atomicOr(&w.flags[s], bad);
 }
 
-__global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int k, int max_newton, double tol) {
+__global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int max_newton, double tol) {
   const int lane = threadIdx.x & 31;
+  const int k = *w.kstep;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= w.groups) return;
   const int64_t s = g * kGroup + (lane & 7);
@@ -700,15 +702,17 @@ __global__ void __launch_bounds__(32) nr_back_kernel(NrDeviceModel m, NrWorkspac
 // scenarios whose factorisation hit an exact zero pivot stop here (state not
 // updated): status, iteration count, and out of the active set before the
 // next step's phasor applies the corrections
-__global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch, int k) {
+__global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch || !w.active[s]) return;
   if (w.flags[s] & 8) {
     w.status[s] = ACPF_NR_ZERO_PIVOT;
-    w.iters[s] = k;
+    w.iters[s] = *w.kstep;
     w.active[s] = 0;
   }
 }
+
+__global__ void nr_step_advance_kernel(NrWorkspace w) { *w.kstep += 1; }
 
 __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
@@ -791,9 +795,17 @@ void launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWor
 
 }  // namespace
 
+void NrGraphCache::release() {
+  if (head) cudaGraphExecDestroy(head);
+  if (body) cudaGraphExecDestroy(body);
+  head = body = nullptr;
+  groups = batch = -1;
+  arena = nullptr;
+}
+
 cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
-                             int* launches) {
+                             int* launches, NrGraphCache* graphs) {
   const int v = hs.variant;
   if (v == 3) {  // mixed: the 4x4 factor kernel is launched too
     cudaError_t e2 = cudaFuncSetAttribute(nr_factor_kernel<V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -810,27 +822,70 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int wpb = 4;
   auto blocks = [&](int64_t items) { return (unsigned)((items + wpb - 1) / wpb); };
+  // one Newton step = head (phasor with the previous correction, mismatch,
+  // exit checks, D2H of the active count) | host test | body (one factor
+  // launch per elimination level, one back launch per back level, zero-pivot
+  // bookkeeping, step counter). Kernels read the step from w.kstep, so each
+  // part is step-independent and is replayed as a CUDA graph.
+  auto head = [&](cudaStream_t st) -> cudaError_t {
+    nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
+    nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
+    cudaError_t r = cudaMemsetAsync(w.n_active, 0, sizeof(int), st);
+    if (r != cudaSuccess) return r;
+    nr_check_kernel<<<blocks(groups), 32 * wpb, 0, st>>>(w, io.batch, max_newton, tol);
+    return cudaMemcpyAsync(w.host_active, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
+  };
+  auto body = [&](cudaStream_t st) -> cudaError_t {
+    if (v == 3)
+      launch_levels<V1>(m, hs, w, groups, st, true);
+    else
+      with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, st); });
+    nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, st>>>(w, io.batch);
+    nr_step_advance_kernel<<<1, 1, 0, st>>>(w);
+    return cudaGetLastError();
+  };
+  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 2;
+  bool use_graphs = graphs != nullptr;
+  if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
+                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
+    graphs->release();
+    if (!graphs->capture && cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) != cudaSuccess)
+      use_graphs = false;
+    auto capture = [&](auto&& seq, cudaGraphExec_t* out) -> bool {
+      cudaGraph_t gr = nullptr;
+      if (cudaStreamBeginCapture(graphs->capture, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+      const cudaError_t r = seq(graphs->capture);
+      const cudaError_t r2 = cudaStreamEndCapture(graphs->capture, &gr);
+      bool ok = r == cudaSuccess && r2 == cudaSuccess && gr &&
+                cudaGraphInstantiate(out, gr, 0) == cudaSuccess;
+      if (gr) cudaGraphDestroy(gr);
+      return ok;
+    };
+    if (use_graphs && capture(head, &graphs->head) && capture(body, &graphs->body)) {
+      graphs->groups = groups;
+      graphs->batch = io.batch;
+      graphs->tol = tol;
+      graphs->max_newton = max_newton;
+      graphs->arena = w.arena;
+    } else {
+      graphs->release();
+      cudaGetLastError();
+      use_graphs = false;
+    }
+  }
   int nl = 0;
   nr_init_kernel<<<blocks(groups), 32 * wpb, 0, stream>>>(m, w, io);
   ++nl;
   for (int k = 0; k <= max_newton; ++k) {
-    nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, k > 0);
-    nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w);
-    e = cudaMemsetAsync(w.n_active, 0, sizeof(int), stream);
+    e = use_graphs ? cudaGraphLaunch(graphs->head, stream) : head(stream);
     if (e != cudaSuccess) return e;
-    nr_check_kernel<<<blocks(groups), 32 * wpb, 0, stream>>>(w, io.batch, k, max_newton, tol);
-    nl += 3;
-    e = cudaMemcpyAsync(w.host_active, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) return e;
+    nl += n_head;
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
-    if (v == 3)
-      launch_levels<V1>(m, hs, w, groups, stream, true);
-    else
-      with_variant(v, [&](auto p) { launch_levels<decltype(p)>(m, hs, w, groups, stream); });
-    nr_zero_pivot_kernel<<<(unsigned)((io.batch + 255) / 256), 256, 0, stream>>>(w, io.batch, k);
-    nl += hs.n_levels + hs.n_blevels + 1;
+    e = use_graphs ? cudaGraphLaunch(graphs->body, stream) : body(stream);
+    if (e != cudaSuccess) return e;
+    nl += n_body;
   }
   nr_output_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, io);
   ++nl;
