@@ -1504,9 +1504,14 @@ acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t p, int64_t batch, const double* p
     w.gsteps = takei(B * (max_newton + 1));
     w.count = takei(1);
   }
-  int* host_count = nullptr;
-  ACPF_CUDA(cudaMallocHost((void**)&host_count, sizeof(int)));
-  w.host_count = host_count;
+  struct PinnedInt {  // released on every return path
+    int* p = nullptr;
+    ~PinnedInt() {
+      if (p) cudaFreeHost(p);
+    }
+  } host_count;
+  ACPF_CUDA(cudaMallocHost((void**)&host_count.p, sizeof(int)));
+  w.host_count = host_count.p;
   const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
   const size_t nt = m.n_theta, nq = m.n_q, nbus = m.n_bus;
   // device staging for host pointers (one chunk)
@@ -1570,7 +1575,6 @@ acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t p, int64_t batch, const double* p
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, p->ev0, p->ev1);
   p->last_ms = ms;
-  cudaFreeHost(host_count);
   ACPF_CUDA(err);
   return ACPF_OK;
 }
