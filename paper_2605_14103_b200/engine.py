@@ -562,7 +562,7 @@ def zbus_solve_arrays(model, s_wye, s_delta, tol, max_iter, device=None) -> dict
 
 def zbus_floor_message(model, v: np.ndarray, slot: int) -> str:
     """Reconstruct the reference VoltageFloorError text (distribution.py:45-50)."""
-    from .distribution import _floor_label
+    from .distribution import floor_site_label
     nw, nd = model.wye_idx.size, model.delta_p.size
     if slot < nw:
         kind, k, mag = "wye", slot, abs(v[model.wye_idx[slot]])
@@ -575,7 +575,7 @@ def zbus_floor_message(model, v: np.ndarray, slot: int) -> str:
     else:
         k = slot - nw - 2 * nd
         kind, mag = "pq", abs(v[model.delta_p[k]] - v[model.delta_q[k]])
-    label = _floor_label(model, kind, k)
+    label = floor_site_label(model, kind, k)
     return f"voltage magnitude {float(mag):.3e} below floor at node-phase {label}"
 
 
