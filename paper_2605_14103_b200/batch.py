@@ -27,9 +27,16 @@ from .distribution import DistributionScenario, ZBusModel
 from .network import BusPartition, TransmissionNetwork
 
 
+_TARGETS = ("transmission", "distribution")
+
+
 @dataclass(frozen=True)
 class ScenarioSpec:
-    """count, 64-bit seed, multiplier half-range, target (reference :25-42)."""
+    """Seeded batch description (reference :25-42).
+
+    ``count`` scenarios, 64-bit ``seed``, multipliers uniform on
+    ``[1 - spread, 1 + spread)``, ``target`` the model family.
+    """
 
     count: int
     seed: int
@@ -37,34 +44,37 @@ class ScenarioSpec:
     target: str = "transmission"
 
     def __post_init__(self):
-        if self.count < 1:
-            raise ValueError("count must be >= 1")
-        if not 0 <= self.spread < 1:
-            raise ValueError("spread must satisfy 0 <= spread < 1")
-        if self.target not in ("transmission", "distribution"):
-            raise ValueError(f"unknown target {self.target!r}")
-        if self.seed < 0:
-            raise ValueError("seed must be a non-negative 64-bit integer")
+        problems = (
+            (self.count < 1, "count must be >= 1"),
+            (not 0 <= self.spread < 1, "spread must satisfy 0 <= spread < 1"),
+            (self.target not in _TARGETS, f"unknown target {self.target!r}"),
+            (self.seed < 0, "seed must be a non-negative 64-bit integer"),
+        )
+        for bad, why in problems:
+            if bad:
+                raise ValueError(why)
+
+
+def _uniform_row(seed: int, index: int, n: int) -> np.ndarray:
+    """First ``n`` doubles of numpy's Philox4x64-10 stream keyed by (seed, index)."""
+    key = np.array([seed, index], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key)).random(n)
 
 
 def generate_load_multipliers(spec: ScenarioSpec, n_elements: int,
                               start: int = 0, count: int | None = None) -> np.ndarray:
     """Rows ``start .. start+count`` of the (count, n_elements) multiplier table.
 
-    Row i = (1 - spread) + 2 spread * U, U the first ``n_elements`` doubles of
-    ``Generator(Philox(key=[seed, i]))`` (reference batch.py:45-60). ``start``
-    lets a shard build only its own rows; every row depends only on
-    (seed, i).
+    Row i is ``(1 - spread) + 2 spread * U_i`` (reference batch.py:45-60); it
+    depends only on (seed, i), so a shard can build just its own rows. The
+    device generator (``csrc/scenario_kernel.cu``) reproduces these bitwise.
     """
-    count = spec.count - start if count is None else count
-    out = np.empty((count, n_elements))
-    lo = 1.0 - spec.spread
-    width = 2.0 * spec.spread
-    for r in range(count):
-        gen = np.random.Generator(
-            np.random.Philox(key=np.array([spec.seed, start + r], dtype=np.uint64)))
-        out[r] = lo + width * gen.random(n_elements)
-    return out
+    rows = spec.count - start if count is None else count
+    offset, scale = 1.0 - spec.spread, 2.0 * spec.spread
+    table = np.empty((rows, n_elements))
+    for r in range(rows):
+        table[r] = offset + scale * _uniform_row(spec.seed, start + r, n_elements)
+    return table
 
 
 @dataclass(frozen=True)
@@ -178,19 +188,10 @@ class BatchReport:
     results: tuple = field(repr=False, default=())
 
 
-@dataclass(frozen=True)
-class _SlimOutcome:
-    converged: bool
-    iterations: int
-    residual_inf: float
-    diagnostic: str | None
-
-
 def _residual_of(res) -> float:
-    for name in ("final_mismatch_inf", "residual_inf"):
-        if hasattr(res, name):
-            return float(getattr(res, name))
-    return float("nan")
+    """Transmission results carry ``final_mismatch_inf``, distribution ``residual_inf``."""
+    name = next((k for k in ("final_mismatch_inf", "residual_inf") if hasattr(res, k)), None)
+    return float("nan") if name is None else float(getattr(res, name))
 
 
 def _record(index: int, res, wall: float, err: str | None) -> ScenarioRecord:
@@ -200,9 +201,61 @@ def _record(index: int, res, wall: float, err: str | None) -> ScenarioRecord:
                           wall, getattr(res, "diagnostic", None))
 
 
-def _slim(res):
-    return _SlimOutcome(bool(res.converged), int(res.iterations), _residual_of(res),
-                        getattr(res, "diagnostic", None))
+def _failure(exc: BaseException) -> str:
+    return f"{type(exc).__name__}: {exc}"
+
+
+def _run_batched(solver, scenarios: list, warmup: bool):
+    """One device call for the whole batch; per-scenario time = total / count."""
+    if warmup:
+        solver.solve_batch(scenarios[:1])
+    t0 = time.perf_counter()
+    try:
+        results, err = list(solver.solve_batch(scenarios)), None
+    except Exception as exc:  # a whole-batch failure becomes one error per record
+        results, err = [None] * len(scenarios), _failure(exc)
+    total = time.perf_counter() - t0
+    share = total / len(scenarios)
+    return [(r, share, err) for r in results], total
+
+
+def _run_serial(solver, scenarios: list, warmup: bool):
+    """Reference-style per-scenario callable, errors isolated per scenario."""
+    if warmup:
+        try:
+            solver(scenarios[0])
+        except Exception:
+            pass
+    done = []
+    t0 = time.perf_counter()
+    for sc in scenarios:
+        t_sc = time.perf_counter()
+        try:
+            res, err = solver(sc), None
+        except Exception as exc:
+            res, err = None, _failure(exc)
+        done.append((res, time.perf_counter() - t_sc, err))
+    return done, time.perf_counter() - t0
+
+
+def _report(outcomes, total: float, worker_count: int, keep_results: bool) -> BatchReport:
+    records = tuple(_record(k, res, wall, err) for k, (res, wall, err) in enumerate(outcomes))
+    return BatchReport(
+        records=records,
+        n_converged=sum(rec.converged for rec in records),
+        total_wall_time=total,
+        throughput=len(records) / total if total > 0 else float("inf"),
+        worker_count=worker_count,
+        results=tuple(res for res, _, _ in outcomes) if keep_results else (),
+    )
+
+
+def report_from_results(results, wall: float, worker_count: int = 1) -> BatchReport:
+    """Report for results solved together in ``wall`` seconds (even time split)."""
+    results = list(results)
+    share = wall / len(results)
+    return _report([(r, share, getattr(r, "diagnostic", None)) for r in results], wall,
+                   worker_count, True)
 
 
 def run_batch(
@@ -212,84 +265,46 @@ def run_batch(
     warmup: bool = True,
     keep_results: bool = True,
 ) -> BatchReport:
-    """Solve every scenario, preserve order, aggregate (reference :280-344).
+    """Solve every scenario in order and aggregate (reference :280-344).
 
-    ``solver`` is either the reference-style per-scenario callable or a
-    batched solver exposing ``solve_batch(list) -> list``; the GPU engine is
-    the latter. ``worker_count`` is recorded; the device decides its own
-    parallelism. Warm-up (one scenario) is excluded from timing, as in the
-    reference.
+    ``solver`` is a per-scenario callable (the reference's contract) or a
+    batched solver with ``solve_batch(list) -> list`` (the GPU engine).
+    ``worker_count`` is recorded only; the device sets its own parallelism.
+    The optional one-scenario warm-up is not timed, as in the reference.
     """
     if worker_count < 1:
         raise ValueError("worker_count must be >= 1")
     scenarios = list(scenarios)
     if not scenarios:
         raise ValueError("empty scenario batch")
-    batched = hasattr(solver, "solve_batch")
-    if batched:
-        if warmup:
-            solver.solve_batch(scenarios[:1])
-        t0 = time.perf_counter()
-        try:
-            results = list(solver.solve_batch(scenarios))
-            errs = [None] * len(results)
-        except Exception as exc:  # whole-batch failure: isolate per record
-            results = [None] * len(scenarios)
-            errs = [f"{type(exc).__name__}: {exc}"] * len(scenarios)
-        total = time.perf_counter() - t0
-        per = total / len(scenarios)
-        outcomes = [(r, per, e) for r, e in zip(results, errs)]
-    else:
-        if warmup:
-            try:
-                solver(scenarios[0])
-            except Exception:
-                pass
-        outcomes = []
-        t0 = time.perf_counter()
-        for sc in scenarios:
-            s0 = time.perf_counter()
-            try:
-                res, err = solver(sc), None
-            except Exception as exc:
-                res, err = None, f"{type(exc).__name__}: {exc}"
-            outcomes.append((res, time.perf_counter() - s0, err))
-        total = time.perf_counter() - t0
-    records = tuple(_record(i, r, w, e) for i, (r, w, e) in enumerate(outcomes))
-    kept = tuple(r for r, _, _ in outcomes) if keep_results else ()
-    return BatchReport(
-        records=records,
-        n_converged=sum(r.converged for r in records),
-        total_wall_time=total,
-        throughput=len(records) / total if total > 0 else float("inf"),
-        worker_count=worker_count,
-        results=kept,
-    )
+    run = _run_batched if hasattr(solver, "solve_batch") else _run_serial
+    outcomes, total = run(solver, scenarios, warmup)
+    return _report(outcomes, total, worker_count, keep_results)
+
+
+_REPORT_SCHEMA = "acpflow-batch-report/1"
+_CSV_COLUMNS = ("index", "converged", "iterations", "residual", "error", "wall_time")
 
 
 def report_to_dict(report: BatchReport) -> dict:
-    """``acpflow-batch-report/1`` (reference :352-376)."""
-    return {
-        "schema": "acpflow-batch-report/1",
-        "aggregate": {
-            "count": len(report.records),
-            "n_converged": report.n_converged,
-            "worker_count": report.worker_count,
-            "timing": {"total_wall_time": report.total_wall_time,
-                       "throughput": report.throughput},
-        },
-        "records": [
-            {"index": r.index, "converged": r.converged, "iterations": r.iterations,
-             "residual": r.residual, "error": r.error, "timing": {"wall_time": r.wall_time}}
-            for r in report.records
-        ],
-    }
+    """``acpflow-batch-report/1`` document (reference :352-376)."""
+    aggregate = {"count": len(report.records), "n_converged": report.n_converged,
+                 "worker_count": report.worker_count,
+                 "timing": {"total_wall_time": report.total_wall_time,
+                            "throughput": report.throughput}}
+    records = [{"index": rec.index, "converged": rec.converged, "iterations": rec.iterations,
+                "residual": rec.residual, "error": rec.error,
+                "timing": {"wall_time": rec.wall_time}} for rec in report.records]
+    return {"schema": _REPORT_SCHEMA, "aggregate": aggregate, "records": records}
+
+
+def _csv_cells(rec: ScenarioRecord) -> tuple:
+    err = (rec.error or "").replace(",", ";").replace("\n", " ")
+    return (str(rec.index), str(int(rec.converged)), str(rec.iterations), repr(rec.residual),
+            err, repr(rec.wall_time))
 
 
 def report_to_csv(report: BatchReport) -> str:
-    """CSV by scenario index, timing last (reference :379-387)."""
-    out = ["index,converged,iterations,residual,error,wall_time"]
-    for r in report.records:
-        err = (r.error or "").replace(",", ";").replace("\n", " ")
-        out.append(f"{r.index},{int(r.converged)},{r.iterations},{r.residual!r},{err},{r.wall_time!r}")
-    return "\n".join(out) + "\n"
+    """One CSV row per scenario index, timing last (reference :379-387)."""
+    rows = [",".join(_CSV_COLUMNS)] + [",".join(_csv_cells(rec)) for rec in report.records]
+    return "\n".join(rows) + "\n"

@@ -113,13 +113,7 @@ def cmd_solve(args) -> int:
     out, wall = _solve_device(kind, model, base, args.seed, args.batch, args.spread, args.tol, args.step,
                               args.precond)
     results = (tm.results_from_arrays(out) if kind == "tx" else engine.zbus_results(model, out))
-    per = wall / len(results)
-    report = bm.BatchReport(
-        records=tuple(bm._record(i, r, per, getattr(r, "diagnostic", None))
-                      for i, r in enumerate(results)),
-        n_converged=sum(bool(r.converged) for r in results), total_wall_time=wall,
-        throughput=len(results) / wall if wall > 0 else float("inf"), worker_count=1,
-        results=tuple(results))
+    report = bm.report_from_results(results, wall)
     if args.verbose:
         print(f"{report.n_converged}/{len(results)} converged in {wall:.3f}s on the GPU",
               file=sys.stderr)
