@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -195,6 +196,15 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch,
                       (int)env_int("ACPF_NR_TASK_ELEMS", 512),
                       env_int("ACPF_NR_COLUMN_STORE", 1) != 0);
+    if (env_int("ACPF_DEBUG_SCHEDULE", 0)) {  // per-level shape of the factor schedule (stderr)
+      const NrSchedule& sc = p->sch;
+      for (int l = 0; l < sc.n_levels; ++l) {
+        const int r0 = sc.level_ptr[l], r1 = sc.level_ptr[l + 1];
+        std::fprintf(stderr, "level %d rows %d tasks %d maxl %d slots %d stream %d\n", l, r1 - r0,
+                     sc.level_task_ptr[l + 1] - sc.level_task_ptr[l], sc.level_maxl[l],
+                     sc.row_slot[r1] - sc.row_slot[r0], sc.row_sptr[r1] - sc.row_sptr[r0]);
+      }
+    }
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
     delete p;

@@ -19,7 +19,8 @@ def test_ybus_partition_flat_start_bitwise(tag, golden):
     y = m.y.csr
     np.testing.assert_array_equal(y.indptr, g["y_indptr"])
     np.testing.assert_array_equal(y.indices, g["y_indices"])
-    np.testing.assert_array_equal(y.data, g["y_data"])
+    # bitwise, signed zeros included (a plain == would accept -0.0 for +0.0)
+    np.testing.assert_array_equal(y.data.view(np.uint64), g["y_data"].view(np.uint64))
     np.testing.assert_array_equal(m.part.theta_block, g["theta_block"])
     np.testing.assert_array_equal(m.part.q_block, g["q_block"])
     st = pf.flat_start(m.net, m.part)
@@ -56,7 +57,7 @@ def test_zbus_model_bitwise(name, golden):
     y = pf.build_three_phase_ybus(net)
     np.testing.assert_array_equal(y.indptr, g["y_indptr"])
     np.testing.assert_array_equal(y.indices, g["y_indices"])
-    np.testing.assert_array_equal(y.data, g["y_data"])
+    np.testing.assert_array_equal(y.data.view(np.uint64), g["y_data"].view(np.uint64))
     m = pf.build_zbus_model(net)
     np.testing.assert_array_equal(m.v0, g["v0"])
     np.testing.assert_array_equal(m.non_slack, g["non_slack"])
