@@ -230,6 +230,18 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
 
   p->h_tpos = tpos;
   p->h_qidx = qidx;
+  // LU of the flat-start Jacobian, shared by every scenario's first step
+  std::vector<double> sh_vals;
+  bool shared0 = false;
+  if (env_int("ACPF_NR_SHARED0", 1)) {
+    try {
+      shared0 = nr_flat_start_factor(s, sc, n_bus, y_rowptr, y_col, y_re, y_im, qidx.data(), theta_init,
+                                     vmag_init, sh_vals);
+    } catch (const std::exception&) {
+      shared0 = false;
+    }
+  }
+  std::vector<int32_t> sh_col(s.col.begin(), s.col.end()), sh_diag(s.diag.begin(), s.diag.end());
   NrDeviceModel& d = p->dm;
   d.n_bus = n_bus;
   d.n_theta = n_theta;
@@ -293,6 +305,11 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
   up(const_cast<int32_t**>(&d.brow_sptr), sc.brow_sptr.data(), sc.brow_sptr.size());
   up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());
+  if (shared0) {
+    up(const_cast<double**>(&d.sh_vals), sh_vals.data(), sh_vals.size());
+    up(const_cast<int32_t**>(&d.sh_col), sh_col.data(), sh_col.size());
+    up(const_cast<int32_t**>(&d.sh_diag), sh_diag.data(), sh_diag.size());
+  }
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
   if (e != cudaSuccess) {

@@ -45,6 +45,11 @@ struct NrDeviceModel {
   int64_t n_block, n_scalar;  // arena elements per group (block / scalar region)
   int64_t off_lu, off_yx;                   // block region
   int64_t off_u, off_e, off_spec, off_th, off_vm;     // scalar region
+  // LU of the flat-start Jacobian shared by every scenario's first Newton step
+  // (nr_flat_start_factor); null when step 0 is factored per scenario
+  const double* sh_vals;   // [nnz_lu][4] L^ / inv(D) / U^, row-major 2x2
+  const int32_t* sh_col;   // [nnz_lu] block column of the slot
+  const int32_t* sh_diag;  // [n_rows] diagonal slot of the row
 };
 
 struct NrHostSchedule {
@@ -77,6 +82,7 @@ struct NrGraphCache {
   cudaStream_t capture = nullptr;  // private stream used only for capture
   cudaGraphExec_t head = nullptr;  // phasor, mismatch, check, D2H of the active count
   cudaGraphExec_t body = nullptr;  // factor levels, back levels, zero-pivot, step++
+  cudaGraphExec_t body0 = nullptr; // step 0 with the shared flat-start LU, step++
   int64_t groups = -1, batch = -1;
   double tol = 0.0;
   int max_newton = -1;

@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
   };
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
+  // step 0 with the shared flat-start LU needs no per-scenario Jacobian
+  const bool assemble = m.sh_vals == nullptr || *w.kstep > 0;
   for (int i = i0 + r; i < i1; i += 4) {
     const int p = __ldg(m.bus_row + i);
     if (p < 0) continue;  // slack: no equations
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
     //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
     //   [[H, N], [M, L]] = [[Re dS/dth, Re dS/dV], [Im dS/dth, Im dS/dV]]
     // with the PV padding rows/columns of the identity equation dV = 0.
+    if (!assemble) continue;
     const double2 ei = ld2(se, i);
     const int a0 = __ldg(m.asm_ptr + i), a1 = __ldg(m.asm_ptr + i + 1);
     for (int a = a0; a < a1; ++a) {
@@ -737,6 +740,52 @@ __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   }
 }
 
+// First Newton step with the LU of the flat-start Jacobian, which is the same
+// for every scenario (nr_flat_start_factor, computed once per plan): one warp
+// per scenario group runs the whole forward substitution (y_p = inv(D_p)
+// (b_p - sum_t L^_pt y_t)) and back substitution (x_p = y_p - sum_c U^_pc x_c)
+// over the rows in elimination order. The factors are read-only and shared by
+// every group (32 B per slot, L2-resident); only the group's y/x elements are
+// read and written. Lane = (half, sc, i): the two half-warps take alternate
+// slots of each row, lane pair (sc, 0/1) the two entries of scenario sc.
+__global__ void __launch_bounds__(128) nr_shared_step_kernel(NrDeviceModel m, NrWorkspace w) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, sc = (lane >> 1) & 7, i = lane & 1;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= w.groups || !w.gactive[g]) return;
+  double* const yx = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup) +
+                     (size_t)m.off_yx * kBlk + 2 * sc;
+  const double2* __restrict__ rows = reinterpret_cast<const double2*>(m.sh_vals);  // row i of slot t: [2t + i]
+  for (int p = 0; p < m.n_rows; ++p) {
+    const int t0 = __ldg(m.row_slot + p), td = __ldg(m.sh_diag + p);
+    double acc = half ? 0.0 : yx[(size_t)p * kBlk + i];
+    for (int t = t0 + half; t < td; t += 2) {
+      const int c = __ldg(m.sh_col + t);
+      const double2 l = __ldg(rows + 2 * t + i);
+      const double2 y = *reinterpret_cast<const double2*>(yx + (size_t)c * kBlk);
+      acc = fma(-l.y, y.y, fma(-l.x, y.x, acc));
+    }
+    acc += __shfl_xor_sync(kFull, acc, 16);
+    const double o = __shfl_xor_sync(kFull, acc, 1);
+    const double2 d = __ldg(rows + 2 * td + i);  // row i of inv(D_p)
+    const double y = d.x * (i ? o : acc) + d.y * (i ? acc : o);
+    if (!half) yx[(size_t)p * kBlk + i] = y;
+    __syncwarp();
+  }
+  for (int p = m.n_rows - 1; p >= 0; --p) {
+    const int td = __ldg(m.sh_diag + p), t1 = __ldg(m.row_slot + p + 1);
+    double part = 0.0;
+    for (int t = td + 1 + half; t < t1; t += 2) {
+      const int c = __ldg(m.sh_col + t);
+      const double2 u = __ldg(rows + 2 * t + i);
+      const double2 x = *reinterpret_cast<const double2*>(yx + (size_t)c * kBlk);
+      part = fma(u.y, x.y, fma(u.x, x.x, part));
+    }
+    part += __shfl_xor_sync(kFull, part, 16);
+    if (!half) yx[(size_t)p * kBlk + i] -= part;
+    __syncwarp();
+  }
+}
+
 // pipeline variants (ACPF_NR_VARIANT; measured one-step times on gb2224 x 65536
 // in DESIGN.md): ring of 8 x 8 elements (6 stages in flight, ~11 warps/SM),
 // 8 x 4 (2 in flight, 8 KB, ~19 warps/SM, the default) and 4 x 4
@@ -798,7 +847,8 @@ void launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWor
 void NrGraphCache::release() {
   if (head) cudaGraphExecDestroy(head);
   if (body) cudaGraphExecDestroy(body);
-  head = body = nullptr;
+  if (body0) cudaGraphExecDestroy(body0);
+  head = body = body0 = nullptr;
   groups = batch = -1;
   arena = nullptr;
 }
@@ -844,7 +894,15 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     nr_step_advance_kernel<<<1, 1, 0, st>>>(w);
     return cudaGetLastError();
   };
-  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 2;
+  // step 0 with the shared flat-start LU: no factorisation, one launch of
+  // substitutions per group (the zero-pivot case was excluded on the host)
+  const bool shared0 = m.sh_vals != nullptr;
+  auto body0 = [&](cudaStream_t st) -> cudaError_t {
+    nr_shared_step_kernel<<<blocks(groups), 32 * wpb, 0, st>>>(m, w);
+    nr_step_advance_kernel<<<1, 1, 0, st>>>(w);
+    return cudaGetLastError();
+  };
+  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 2, n_body0 = 2;
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
                      graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
@@ -861,7 +919,8 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
       if (gr) cudaGraphDestroy(gr);
       return ok;
     };
-    if (use_graphs && capture(head, &graphs->head) && capture(body, &graphs->body)) {
+    if (use_graphs && capture(head, &graphs->head) && capture(body, &graphs->body) &&
+        (!shared0 || capture(body0, &graphs->body0))) {
       graphs->groups = groups;
       graphs->batch = io.batch;
       graphs->tol = tol;
@@ -883,9 +942,13 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     if (*w.host_active == 0) break;
-    e = use_graphs ? cudaGraphLaunch(graphs->body, stream) : body(stream);
+    const bool first = shared0 && k == 0;
+    if (use_graphs)
+      e = cudaGraphLaunch(first ? graphs->body0 : graphs->body, stream);
+    else
+      e = first ? body0(stream) : body(stream);
     if (e != cudaSuccess) return e;
-    nl += n_body;
+    nl += first ? n_body0 : n_body;
   }
   nr_output_kernel<<<blocks(groups * nch), 32 * wpb, 0, stream>>>(m, w, io);
   ++nl;

@@ -19,6 +19,7 @@
 #include "nr_symbolic.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <set>
 #include <stdexcept>
@@ -441,6 +442,111 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   };
   make_tasks(o.level_ptr, o.row_sptr, o.level_task_ptr, o.task_row);
   make_tasks(o.blevel_ptr, o.brow_sptr, o.blevel_task_ptr, o.btask_row);
+}
+
+// The Jacobian at the flat start (transmission.py:169-177) depends only on
+// the network and the flat-start state, never on the specified injections, so
+// the first Newton step of every scenario factors the same matrix. It is
+// assembled here with the device formulas (nr_mismatch_kernel: dense_jacobian,
+// transmission.py:383-407, PV padding rows/columns dV = 0) and factored once in
+// the same unit-upper block form as nr_factor_kernel (Crout pair lists of s).
+// vals[4t + 2i + j] = entry (i, j) of slot t: L^ for L slots, inv(D_p) at the
+// diagonal slot, U^ = inv(D_p) A' for U slots. Returns false on an exact zero
+// pivot (the caller then factors step 0 per scenario as in every other step).
+bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, const int32_t* y_rowptr,
+                          const int32_t* y_col, const double* y_re, const double* y_im, const int32_t* qidx,
+                          const double* theta0, const double* vmag0, std::vector<double>& vals) {
+  const int nr = s.n_j;
+  const int64_t nslots = s.rowptr[nr];
+  std::vector<double> er(n_bus), ei(n_bus), ur(n_bus), ui(n_bus);
+  for (int i = 0; i < n_bus; ++i) {
+    er[i] = std::cos(theta0[i]);
+    ei[i] = std::sin(theta0[i]);
+    ur[i] = vmag0[i] * er[i];
+    ui[i] = vmag0[i] * ei[i];
+  }
+  std::vector<double> a(4 * nslots, 0.0);
+  std::vector<int64_t> where(nr, -1);
+  for (int i = 0; i < n_bus; ++i) {
+    const int p = o.bus_row[i];
+    if (p < 0) continue;
+    double ir = 0.0, ii = 0.0;  // I_i = sum_j Y_ij u_j
+    for (int e = y_rowptr[i]; e < y_rowptr[i + 1]; ++e) {
+      const int j = y_col[e];
+      ir += y_re[e] * ur[j] - y_im[e] * ui[j];
+      ii += y_re[e] * ui[j] + y_im[e] * ur[j];
+    }
+    for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
+    const bool pq = qidx[i] >= 0;
+    auto stamp = [&](int j, double yr, double yi) {
+      if (o.bus_row[j] < 0) return;  // slack column
+      const int64_t t = where[o.bus_row[j]];
+      if (t < 0) throw std::logic_error("flat-start assembly slot missing");
+      // wv = u_i conj(y E_j)
+      const double ye_r = yr * er[j] - yi * ei[j], ye_i = yr * ei[j] + yi * er[j];
+      const double wvr = ur[i] * ye_r + ui[i] * ye_i, wvi = ui[i] * ye_r - ur[i] * ye_i;
+      double dthr, dthi, dvr, dvi;
+      if (j != i) {  // dS_i/dth_j = -j u_i conj(y u_j)
+        const double yu_r = yr * ur[j] - yi * ui[j], yu_i = yr * ui[j] + yi * ur[j];
+        const double wtr = ur[i] * yu_r + ui[i] * yu_i, wti = ui[i] * yu_r - ur[i] * yu_i;
+        dthr = wti;
+        dthi = -wtr;
+        dvr = wvr;
+        dvi = wvi;
+      } else {  // dS_i/dth_i = j u_i conj(I_i - y u_i); dS_i/dV_i = wv + conj(I_i) E_i
+        const double yu_r = yr * ur[i] - yi * ui[i], yu_i = yr * ui[i] + yi * ur[i];
+        const double cr = ir - yu_r, ci = ii - yu_i;
+        const double wtr = ur[i] * cr + ui[i] * ci, wti = ui[i] * cr - ur[i] * ci;
+        dthr = -wti;
+        dthi = wtr;
+        dvr = wvr + (ir * er[i] + ii * ei[i]);
+        dvi = wvi + (ir * ei[i] - ii * er[i]);
+      }
+      const bool pqj = qidx[j] >= 0;
+      double* b = &a[4 * t];
+      b[0] = dthr;                                           // H
+      b[2] = pq ? dthi : 0.0;                                // M
+      b[1] = pqj ? dvr : 0.0;                                // N
+      b[3] = (pq && pqj) ? dvi : (j == i ? 1.0 : 0.0);       // L (PV padding: dV = 0)
+    };
+    bool have_diag = false;
+    for (int e = y_rowptr[i]; e < y_rowptr[i + 1]; ++e) have_diag |= (y_col[e] == i);
+    if (!have_diag) stamp(i, 0.0, 0.0);
+    for (int e = y_rowptr[i]; e < y_rowptr[i + 1]; ++e) stamp(y_col[e], y_re[e], y_im[e]);
+    for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = -1;
+  }
+  vals.assign(4 * nslots, 0.0);
+  for (int p = 0; p < nr; ++p) {
+    double inv[4] = {0, 0, 0, 0};
+    for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) {
+      double c[4] = {a[4 * t], a[4 * t + 1], a[4 * t + 2], a[4 * t + 3]};
+      for (int64_t k = s.pair_ptr[t]; k < s.pair_ptr[t + 1]; ++k) {
+        const double* l = &vals[4 * (int64_t)s.pair_l[k]];
+        const double* u = &vals[4 * (int64_t)s.pair_u[k]];
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) c[2 * i + j] -= l[2 * i] * u[j] + l[2 * i + 1] * u[2 + j];
+      }
+      double* v = &vals[4 * t];
+      if (t < s.diag[p]) {
+        for (int k = 0; k < 4; ++k) v[k] = c[k];
+      } else if (t == s.diag[p]) {
+        const double det = c[0] * c[3] - c[1] * c[2];
+        if (det == 0.0 || !std::isfinite(det)) return false;
+        const double rd = 1.0 / det;
+        inv[0] = c[3] * rd;
+        inv[1] = -c[1] * rd;
+        inv[2] = -c[2] * rd;
+        inv[3] = c[0] * rd;
+        for (int k = 0; k < 4; ++k) v[k] = inv[k];
+      } else {
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) v[2 * i + j] = inv[2 * i] * c[j] + inv[2 * i + 1] * c[2 + j];
+      }
+    }
+  }
+  for (double x : vals)
+    if (!std::isfinite(x)) return false;
+  return true;
 }
 
 }  // namespace acpf
