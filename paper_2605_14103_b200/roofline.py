@@ -25,6 +25,17 @@ def nr_bytes_per_scenario(iterations, n_bus: int, n_j: int, nnz_lu: int) -> np.n
     return k * 8.0 * (2 * nnz + 2 * n_bus + 3 * n_j) + 8.0 * (2 * n_bus + 2 * n_j)
 
 
+def nr_bytes_per_scenario_executed(iterations, n_bus: int, n_j: int, nnz_lu: int) -> np.ndarray:
+    """As nr_bytes_per_scenario, but the first Newton step solves with the
+    flat-start LU shared by every scenario (nr_flat_start_factor), so it moves
+    no per-scenario factor: K-1 factor passes plus the step-0 vectors."""
+    nnz = PINNED_NNZ_LU.get(n_bus, nnz_lu)
+    k = np.asarray(iterations, dtype=np.float64)
+    kf = np.maximum(k - 1.0, 0.0)
+    step0 = np.where(k > 0, 8.0 * (2 * n_bus + 3 * n_j), 0.0)
+    return kf * 8.0 * (2 * nnz + 2 * n_bus + 3 * n_j) + step0 + 8.0 * (2 * n_bus + 2 * n_j)
+
+
 def zbus_flops_per_scenario(iterations, n: int, n_l: int, n_loads: int) -> np.ndarray:
     k = np.asarray(iterations, dtype=np.float64)
     return (k + 1) * (8.0 * n * n_l + 4.0 * n + 20.0 * n_loads)

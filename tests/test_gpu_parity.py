@@ -237,3 +237,35 @@ def test_zbus_empty_and_ragged_batches(zb_models, golden):
         out = engine.zbus_solve_arrays(model, sw[:b], sd[:b], 1e-9, 100)
         np.testing.assert_array_equal(out["v"], full["v"][:b])
         np.testing.assert_array_equal(out["iterations"], g["iterations"][:b])
+
+
+@pytest.mark.parametrize("tag", ["case118", "gb2224"])
+def test_nr_shared_first_step_matches_per_scenario_factor(tag, tx_models, golden, monkeypatch):
+    """Step 0 on the flat-start LU shared by every scenario (nr_flat_start_factor)
+    against step 0 factored per scenario (ACPF_NR_SHARED0=0): the same flags and
+    iterations, states equal to rounding."""
+    g = golden(f"nr_{tag}")
+    model = tx_models[tag]
+    p, q = np.ascontiguousarray(g["p_spec"]), np.ascontiguousarray(g["q_spec"])
+    a = model.plan().solve(p, q, 1e-8, 20)
+    monkeypatch.setenv("ACPF_NR_SHARED0", "0")
+    per = _fresh_plan(model)
+    b = per.solve(p, q, 1e-8, 20)
+    np.testing.assert_array_equal(a["iterations"], b["iterations"])
+    np.testing.assert_array_equal(a["converged"], b["converged"])
+    assert np.abs(a["theta"] - b["theta"]).max() <= 1e-12
+    assert np.abs(a["vmag"] - b["vmag"]).max() <= 1e-12
+    # one step: the shared-LU step equals the per-scenario-factor step
+    a1 = model.plan().solve(p, q, 1e-8, 1)
+    b1 = per.solve(p, q, 1e-8, 1)
+    assert np.abs(a1["theta"] - b1["theta"]).max() <= 1e-12
+    assert np.abs(a1["vmag"] - b1["vmag"]).max() <= 1e-12
+
+
+def _fresh_plan(model):
+    """A new plan (model.plan() caches one per device) with the model's ordering;
+    ACPF_NR_SHARED0 is read when the plan is created."""
+    from paper_2605_14103_b200.transmission import flat_start, jacobian_ordering
+    st = flat_start(model.net, model.part)
+    return engine.NrPlan(model.y.csr, model.part.theta_block, model.part.q_block, st.theta, st.vmag,
+                         perm=jacobian_ordering(model))
