@@ -15,6 +15,7 @@
 #include <exception>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "acpf_internal.cuh"
@@ -87,6 +88,21 @@ int64_t env_int(const char* name, int64_t dflt) {
 
 using namespace acpf;
 
+// Second concurrent chunk solver of the host-pointer path (lane 1; lane 0
+// uses the plan's own workspace and graph cache): own stream, workspace,
+// staging set, pinned active counter and graph cache.
+struct NrLane {
+  DevArena work, stage;
+  NrWorkspace ws{};
+  int64_t groups = 0;
+  size_t stage_bytes = 0;
+  void* stage_base = nullptr;
+  int* host_active = nullptr;
+  NrGraphCache graphs;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_end = nullptr;
+};
+
 struct acpf_nr_plan {
   int device = 0;
   NrSymbolic sym;
@@ -115,6 +131,7 @@ struct acpf_nr_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
+  NrLane lanes[2];                      // concurrent chunk solvers (host-pointer path)
 };
 
 struct acpf_zbus_plan {
@@ -524,6 +541,185 @@ static acpf_status nr_solve_host(acpf_nr_plan* p, int64_t batch, int64_t chunk, 
   return ACPF_OK;
 }
 
+static acpf_status nr_lane_workspace(acpf_nr_plan* p, NrLane& L, int64_t groups) {
+  if (L.groups >= groups) return ACPF_OK;
+  L.work.release();
+  L.groups = 0;
+  const size_t S = (size_t)groups * kGroup;
+  NrWorkspace& w = L.ws;
+  void* ptr = nullptr;
+  bool ok = true;
+  auto get = [&](size_t bytes) -> void* {
+    if (!ok || L.work.alloc(&ptr, bytes) != cudaSuccess) {
+      ok = false;
+      return nullptr;
+    }
+    return ptr;
+  };
+  w.arena = (double*)get((size_t)groups * (p->sch.n_block * 4 + p->sch.n_scalar) * kGroup * 8);
+  w.fmax_bits = (unsigned long long*)get(S * 8);
+  w.flags = (int*)get(S * 4);
+  w.status = (int*)get(S * 4);
+  w.iters = (int*)get(S * 4);
+  w.fout = (double*)get(S * 8);
+  w.active = (uint8_t*)get(S);
+  w.gactive = (int*)get((size_t)groups * 4);
+  w.n_active = (int*)get(4);
+  w.kstep = (int*)get(4);
+  if (!ok) {
+    L.work.release();
+    cudaGetLastError();
+    set_error("acpf_nr_solve: device workspace allocation failed (" + std::to_string(groups) +
+              " groups, second chunk lane); lower ACPF_NR_CHUNK");
+    return ACPF_ENOMEM;
+  }
+  L.groups = groups;
+  return ACPF_OK;
+}
+
+// Host-pointer solve on two concurrent chunk lanes: even chunks on lane 0,
+// odd chunks on lane 1, each lane a stream that copies its chunk in, solves it
+// (its own host thread drives the Newton loop, which waits for the active
+// count every step) and copies the results out. Lane 1's first H2D is queued
+// behind lane 0's, so lane 0 starts solving while lane 1's inputs arrive and
+// lane 0's D2H runs while lane 1 finishes; the two solves share the GPU, so
+// their level launches fill each other's tails (a chunk solved alone loses
+// ~10% in launch tails against the whole batch).
+static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk, const double* p_spec,
+                                  const double* q_spec, double tol, int32_t max_newton, double* theta_out,
+                                  double* vmag_out, uint8_t* converged, int32_t* iterations,
+                                  double* final_mismatch_inf, int32_t* status, cudaStream_t st) {
+  const NrDeviceModel& d = p->dm;
+  const int64_t groups = chunk / kGroup;
+  const int64_t n_chunks = (batch + chunk - 1) / chunk;
+  const size_t set_b = (size_t)chunk * ((size_t)(d.n_theta + d.n_q) * 8 + (size_t)d.n_bus * 16 + 8 + 4 + 4 + 1) + 256;
+  struct Set {
+    double *ps, *qs, *th, *vm, *fn;
+    int32_t *it, *stt;
+    uint8_t* cv;
+  } sets[2];
+  NrWorkspace ws[2];
+  NrGraphCache* graphs[2];
+  for (int k = 0; k < 2; ++k) {
+    NrLane& L = p->lanes[k];
+    if (!L.st) ACPF_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    if (!L.ev_h2d) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_h2d, cudaEventDisableTiming));
+    if (!L.ev_end) ACPF_CUDA(cudaEventCreate(&L.ev_end));
+    acpf_status rc = ensure_stage(L.stage, L.stage_bytes, L.stage_base, set_b);
+    if (rc != ACPF_OK) return rc;
+    if (k == 0) {  // lane 0: the plan's workspace (sized for the chunk by the caller) and graphs
+      ws[0] = p->ws;
+      graphs[0] = nr_graphs(p);
+    } else {
+      if ((rc = nr_lane_workspace(p, L, groups)) != ACPF_OK) return rc;
+      if (!L.host_active && cudaMallocHost(&L.host_active, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("pinned host allocation failed");
+        return ACPF_ENOMEM;
+      }
+      ws[1] = L.ws;
+      ws[1].host_active = L.host_active;
+      graphs[1] = nr_graphs(p) ? &L.graphs : nullptr;
+    }
+    char* b = (char*)L.stage_base;
+    auto take = [&](size_t bytes) {
+      char* r = b;
+      b += (bytes + 15) & ~(size_t)15;
+      return r;
+    };
+    sets[k].ps = (double*)take((size_t)chunk * d.n_theta * 8);
+    sets[k].qs = (double*)take((size_t)chunk * d.n_q * 8);
+    sets[k].th = (double*)take((size_t)chunk * d.n_bus * 8);
+    sets[k].vm = (double*)take((size_t)chunk * d.n_bus * 8);
+    sets[k].fn = (double*)take((size_t)chunk * 8);
+    sets[k].it = (int32_t*)take((size_t)chunk * 4);
+    sets[k].stt = (int32_t*)take((size_t)chunk * 4);
+    sets[k].cv = (uint8_t*)take((size_t)chunk);
+  }
+  auto h2d = [&](int64_t c, cudaStream_t s) -> acpf_status {
+    const Set& S = sets[c & 1];
+    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    if (d.n_theta)
+      ACPF_CUDA(cudaMemcpyAsync(S.ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, s));
+    if (d.n_q) ACPF_CUDA(cudaMemcpyAsync(S.qs, q_spec + s0 * d.n_q, nb * d.n_q * 8, cudaMemcpyHostToDevice, s));
+    return ACPF_OK;
+  };
+  // order after the caller's stream, then lane 0's first H2D before lane 1's
+  ACPF_CUDA(cudaEventRecord(p->ev0, st));
+  cudaStream_t s0 = p->lanes[0].st, s1 = p->lanes[1].st;
+  ACPF_CUDA(cudaStreamWaitEvent(s0, p->ev0, 0));
+  ACPF_CUDA(cudaStreamWaitEvent(s1, p->ev0, 0));
+  acpf_status rc = h2d(0, s0);
+  if (rc != ACPF_OK) return rc;
+  if (n_chunks > 1) {
+    ACPF_CUDA(cudaEventRecord(p->lanes[0].ev_h2d, s0));
+    ACPF_CUDA(cudaStreamWaitEvent(s1, p->lanes[0].ev_h2d, 0));
+    if ((rc = h2d(1, s1)) != ACPF_OK) return rc;
+  }
+  acpf_status lrc[2] = {ACPF_OK, ACPF_OK};
+  std::string lerr[2];
+  int lnl[2] = {0, 0};
+  auto run = [&](int k) {
+    cudaSetDevice(p->device);
+    cudaStream_t s = p->lanes[k].st;
+    auto body = [&]() -> acpf_status {
+      for (int64_t c = k; c < n_chunks; c += 2) {
+        const Set& S = sets[k];
+        const int64_t c0 = c * chunk, nb = std::min(chunk, batch - c0);
+        if (c >= 2) {
+          acpf_status r = h2d(c, s);
+          if (r != ACPF_OK) return r;
+        }
+        NrBatchIO io{};
+        io.batch = nb;
+        io.p_spec = S.ps;
+        io.q_spec = S.qs;
+        io.theta_out = S.th;
+        io.vmag_out = S.vm;
+        io.fnorm = S.fn;
+        io.iterations = S.it;
+        io.status = S.stt;
+        io.converged = S.cv;
+        NrWorkspace wsb = ws[k];
+        wsb.groups = (nb + kGroup - 1) / kGroup;
+        int nl = 0;
+        ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, s, &nl, graphs[k]));
+        lnl[k] += nl;
+        ACPF_CUDA(cudaMemcpyAsync(theta_out + c0 * d.n_bus, S.th, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
+        ACPF_CUDA(cudaMemcpyAsync(vmag_out + c0 * d.n_bus, S.vm, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
+        if (final_mismatch_inf)
+          ACPF_CUDA(cudaMemcpyAsync(final_mismatch_inf + c0, S.fn, nb * 8, cudaMemcpyDeviceToHost, s));
+        if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + c0, S.it, nb * 4, cudaMemcpyDeviceToHost, s));
+        if (status) ACPF_CUDA(cudaMemcpyAsync(status + c0, S.stt, nb * 4, cudaMemcpyDeviceToHost, s));
+        if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + c0, S.cv, nb, cudaMemcpyDeviceToHost, s));
+      }
+      ACPF_CUDA(cudaEventRecord(p->lanes[k].ev_end, s));
+      ACPF_CUDA(cudaStreamSynchronize(s));
+      return ACPF_OK;
+    };
+    lrc[k] = body();
+    if (lrc[k] != ACPF_OK) lerr[k] = acpf_last_error();
+  };
+  if (n_chunks > 1) {
+    std::thread t1(run, 1);
+    run(0);
+    t1.join();
+  } else {
+    run(0);
+  }
+  for (int k = 0; k < 2; ++k)
+    if (lrc[k] != ACPF_OK) {
+      set_error(lerr[k]);
+      return lrc[k];
+    }
+  float ms = 0.0f, ms1 = 0.0f;
+  ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->lanes[0].ev_end));
+  if (n_chunks > 1) ACPF_CUDA(cudaEventElapsedTime(&ms1, p->ev0, p->lanes[1].ev_end));
+  p->last_ms = std::max(ms, ms1);  // wall time of the whole host-pointer solve incl. copies
+  p->last_launches = lnl[0] + lnl[1];
+  return ACPF_OK;
+}
+
 acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
                           const double* q_spec, double tol_mismatch, int32_t max_newton,
                           double* theta_out, double* vmag_out, uint8_t* converged,
@@ -552,14 +748,20 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   }
   chunk = std::min<int64_t>(chunk, batch);
   // host buffers: at least two chunks so transfers overlap the solves
-  if (!dev_ptrs && env_int("ACPF_NR_CHUNK", 0) <= 0 && batch >= 2 * 8192)
+  const int pipeline = (int)env_int("ACPF_NR_PIPELINE", 2);  // 0 serial, 1 copy stream, 2 two lanes
+  if (!dev_ptrs && env_int("ACPF_NR_CHUNK", 0) <= 0 && batch >= 2 * 8192) {
     chunk = std::min<int64_t>(chunk, (batch + 1) / 2);
+    if (pipeline == 2) chunk = std::min<int64_t>(chunk, 32768);  // two lane workspaces in flight
+  }
   chunk = ((chunk + kGroup - 1) / kGroup) * kGroup;
   const int64_t groups = chunk / kGroup;
   acpf_status rc = nr_ensure_workspace(p, groups);
   if (rc != ACPF_OK) return rc;
 
-  if (!dev_ptrs && env_int("ACPF_NR_PIPELINE", 1) != 0)
+  if (!dev_ptrs && pipeline == 2)
+    return nr_solve_lanes(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
+                          converged, iterations, final_mismatch_inf, status, st);
+  if (!dev_ptrs && pipeline == 1)
     return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
                          converged, iterations, final_mismatch_inf, status, st);
   // per-scenario byte sizes
@@ -668,6 +870,16 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
     p->graphs.release();
     if (p->graphs.capture) cudaStreamDestroy(p->graphs.capture);
     if (p->host_active) cudaFreeHost(p->host_active);
+    for (NrLane& L : p->lanes) {
+      L.graphs.release();
+      if (L.graphs.capture) cudaStreamDestroy(L.graphs.capture);
+      if (L.st) cudaStreamDestroy(L.st);
+      if (L.ev_h2d) cudaEventDestroy(L.ev_h2d);
+      if (L.ev_end) cudaEventDestroy(L.ev_end);
+      if (L.host_active) cudaFreeHost(L.host_active);
+      L.work.release();
+      L.stage.release();
+    }
     p->work.release();
     p->stage.release();
     p->model.release();

@@ -209,15 +209,18 @@ def test_nr_empty_and_ragged_batches(tx_models, golden):
         np.testing.assert_array_equal(out["iterations"], g["iterations"][:b])
 
 
-def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch):
-    # ragged chunks (ACPF_NR_CHUNK) through the pipelined host path and the
-    # device-pointer path give the same bits as one chunk
+@pytest.mark.parametrize("pipeline", ["0", "1", "2"])
+def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch, pipeline):
+    # ragged chunks (ACPF_NR_CHUNK) through the host paths (0 serial, 1 copy
+    # stream, 2 two concurrent chunk lanes) and the device-pointer path give
+    # the same bits as one chunk
     torch = pytest.importorskip("torch")
     model = pf.build_transmission_model(load_transmission("case118"))
     base = pf.transmission_base(model.net, model.part)
     p, q = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=1000, seed=1010))
     ref = model.plan().solve(p, q, 1e-8, 20)
     monkeypatch.setenv("ACPF_NR_CHUNK", "136")
+    monkeypatch.setenv("ACPF_NR_PIPELINE", pipeline)
     model2 = pf.build_transmission_model(load_transmission("case118"))
     chunked = model2.plan().solve(p, q, 1e-8, 20)
     np.testing.assert_array_equal(chunked["theta"], ref["theta"])
