@@ -988,7 +988,7 @@ static acpf_status zbus_solve_host(acpf_zbus_plan* p, int64_t batch, const doubl
   // Two staging sets; chunk c+1's H2D and chunk c's D2H run on a copy stream
   // while chunk c+1 computes, so the voltage read-back overlaps the solve.
   const ZbDeviceModel& d = p->dm;
-  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(1, env_int("ACPF_ZBUS_CHUNK", 32768)));
+  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(1, env_int("ACPF_ZBUS_CHUNK", 16384)));
   const size_t in_b = (size_t)(d.n_wye + d.n_delta) * 16;
   const size_t out_b = (size_t)d.n * 16 + 1 + 4 + 8 + 8 + 4 + 4;
   const size_t set_b = (size_t)chunk * (in_b + out_b) + 256;
