@@ -44,9 +44,15 @@ def single():
     p1.solve(pt, qt, 1e-8, 20, out=out_full, stream=s1)
 
 
+OFFSET = [0.0]  # seconds the second half starts after the first (phase offset)
+
+
 def dual():
-    ths = [threading.Thread(target=lambda pl=pl, hv=hv, o=o, s=s: pl.solve(*hv, 1e-8, 20, out=o, stream=s))
-           for pl, hv, o, s in ((p1, halves[0], outs[0], s1), (p2, halves[1], outs[1], s2))]
+    def second():
+        time.sleep(OFFSET[0])
+        p2.solve(*halves[1], 1e-8, 20, out=outs[1], stream=s2)
+    ths = [threading.Thread(target=lambda: p1.solve(*halves[0], 1e-8, 20, out=outs[0], stream=s1)),
+           threading.Thread(target=second)]
     for t in ths:
         t.start()
     for t in ths:
@@ -61,5 +67,9 @@ def seq():
 for name, fn in (("single", single), ("dual", dual), ("seq-halves", seq), ("single", single), ("dual", dual)):
     t = timed(fn)
     print(f"{name:10s} B={B}: {t * 1e3:8.1f} ms  {B / t:9.0f} flows/s", flush=True)
+for off in (0.010, 0.020, 0.040, 0.060):
+    OFFSET[0] = off
+    t = timed(dual)
+    print(f"dual+{off * 1e3:.0f}ms B={B}: {t * 1e3:8.1f} ms  {B / t:9.0f} flows/s", flush=True)
 conv = int(outs[0]["converged"].sum().item() + outs[1]["converged"].sum().item())
 print("dual converged", conv, "single", int(out_full["converged"].sum().item()))
