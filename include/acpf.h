@@ -136,7 +136,14 @@ acpf_status acpf_nr_plan_structure(acpf_nr_plan_t plan, int32_t* perm_out, int64
  *   theta_out, vmag_out [batch][n_bus]             (NewtonResult.state)
  *   converged [batch] u8, iterations [batch], final_mismatch_inf [batch],
  *   status [batch] (ACPF_NR_*).
- * Any output pointer except theta_out/vmag_out may be NULL.                */
+ * Any output pointer except theta_out/vmag_out may be NULL.
+ * The first Newton step of every scenario uses the LU of the flat-start
+ * Jacobian, which does not depend on the scenario (factored once at plan
+ * create; ACPF_NR_SHARED0=0 factors it per scenario instead).
+ * ACPF_HOST_PTRS: the batch is copied in chunks solved on two concurrent
+ * lanes (streams); the call drives the second lane from an internal host
+ * thread that is joined before it returns (ACPF_NR_PIPELINE=1: one stream
+ * plus a copy stream, 0: serial chunks).                                    */
 acpf_status acpf_nr_solve(acpf_nr_plan_t plan, int64_t batch, const double* p_spec,
                           const double* q_spec, double tol_mismatch, int32_t max_newton,
                           double* theta_out, double* vmag_out, uint8_t* converged,
