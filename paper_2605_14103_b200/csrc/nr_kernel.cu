@@ -314,15 +314,12 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
   // the scalar region is read-only here (only block elements are written), so
   // gathers go through the non-coherent path
   const double* __restrict__ su = gb.s + m.off_u * kGroup;  // u_j: su[2j*8], su[(2j+1)*8]
-  const double* __restrict__ se = gb.s + m.off_e * kGroup;
   double* __restrict__ blk = gb.b;
   auto ld2 = [](const double* __restrict__ base, int j) {
     return make_double2(__ldg(base + (size_t)(2 * j) * kGroup), __ldg(base + (size_t)(2 * j + 1) * kGroup));
   };
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
-  // step 0 with the shared flat-start LU needs no per-scenario Jacobian
-  const bool assemble = m.sh_vals == nullptr || *w.kstep > 0;
   for (int i = i0 + r; i < i1; i += 4) {
     const int p = __ldg(m.bus_row + i);
     if (p < 0) continue;  // slack: no equations
@@ -347,43 +344,82 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
       fmx = fmx < fabs(fq) ? fabs(fq) : fmx;
     }
     *reinterpret_cast<double2*>(&BL(blk, m.off_yx + p, 0)) = make_double2(-fp, -fq);
-    // 2x2 Jacobian block of every Ybus entry (i, j) into its LU slot:
-    //   dS_i/dth_j = -j u_i conj(y u_j)  (j != i);  dS_i/dth_i = j u_i conj(I_i - y u_i)
-    //   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
-    //   [[H, N], [M, L]] = [[Re dS/dth, Re dS/dV], [Im dS/dth, Im dS/dV]]
-    // with the PV padding rows/columns of the identity equation dV = 0.
-    if (!assemble) continue;
-    const double2 ei = ld2(se, i);
-    const int a0 = __ldg(m.asm_ptr + i), a1 = __ldg(m.asm_ptr + i + 1);
-    for (int a = a0; a < a1; ++a) {
-      const int slot = __ldg(m.asm_slot + a);
-      if (slot < 0) continue;  // slack column
-      const double2 y = __ldg(m.asm_y + a);
-      const int jb = __ldg(m.asm_j + a);
-      const double2 wv = mul_conj(u, cmul(y, ld2(se, jb)));
-      double2 dth, dv;
-      if (jb != i) {
-        const double2 wt = mul_conj(u, cmul(y, ld2(su, jb)));
-        dth = make_double2(wt.y, -wt.x);
-        dv = wv;
-      } else {
-        const double2 yu = cmul(y, u);
-        const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
-        dth = make_double2(-wt.y, wt.x);
-        dv = make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x));
-      }
-      const bool pqj = __ldg(m.qidx + jb) >= 0;
-      // column-major [[H, N], [M, L]]: H (0,0)->0, M (1,0)->1, N (0,1)->2, L (1,1)->3;
-      // one 16-byte store per block column (entries (0, j), (1, j) are adjacent)
-      double2* const col = reinterpret_cast<double2*>(&BL(blk, m.off_lu + slot, 0));
-      col[0] = make_double2(dth.x, pq ? dth.y : 0.0);
-      col[kGroup] = make_double2(pqj ? dv.x : 0.0, (pq && pqj) ? dv.y : (jb == i ? 1.0 : 0.0));
-    }
   }
   const int64_t s = g * kGroup + sc;
   // fmax of non-negative doubles is the max of their bit patterns
   if (fmx > 0.0) atomicMax(&w.fmax_bits[s], (unsigned long long)__double_as_longlong(fmx));
   if (bad) atomicOr(&w.flags[s], bad);
+}
+
+// Jacobian 2x2 blocks of every Ybus entry (i, j) straight into their LU slots,
+// for the groups still active after the exit checks (first kernel of a step's
+// body, so the final mismatch pass of a solve assembles nothing):
+//   dS_i/dth_j = -j u_i conj(y u_j)  (j != i);  dS_i/dth_i = j u_i conj(I_i - y u_i)
+//   dS_i/dV_j  =  u_i conj(y E_j) [+ conj(I_i) E_i if j == i]
+//   [[H, N], [M, L]] = [[Re dS/dth, Re dS/dV], [Im dS/dth, Im dS/dV]]
+// with the PV padding rows/columns of the identity equation dV = 0
+// (dense_jacobian, transmission.py:383-407). I_i = sum_j Y_ij u_j is
+// accumulated over the same assembly list (the Ybus row in order, slack
+// columns included), the diagonal block written after the row.
+#ifndef ACPF_JAC_MINB
+#define ACPF_JAC_MINB 8
+#endif
+__global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDeviceModel m, NrWorkspace w) {
+  const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
+  const int64_t g = item / nch;
+  if (g >= w.groups || !w.gactive[g]) return;
+  const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
+  const GroupBase gb = group_base(m, w, g, sc);
+  const double* __restrict__ su = gb.s + m.off_u * kGroup;
+  const double* __restrict__ se = gb.s + m.off_e * kGroup;
+  double* __restrict__ blk = gb.b;
+  auto ld2 = [](const double* __restrict__ base, int j) {
+    return make_double2(__ldg(base + (size_t)(2 * j) * kGroup), __ldg(base + (size_t)(2 * j + 1) * kGroup));
+  };
+  // column-major [[H, N], [M, L]]: H (0,0)->0, M (1,0)->1, N (0,1)->2, L (1,1)->3;
+  // one 16-byte store per block column (entries (0, j), (1, j) are adjacent)
+  auto put = [&](int slot, double2 dth, double2 dv, bool pq, bool pqj, bool diag) {
+    double2* const col = reinterpret_cast<double2*>(&BL(blk, m.off_lu + slot, 0));
+    col[0] = make_double2(dth.x, pq ? dth.y : 0.0);
+    col[kGroup] = make_double2(pqj ? dv.x : 0.0, (pq && pqj) ? dv.y : (diag ? 1.0 : 0.0));
+  };
+  for (int i = i0 + r; i < i1; i += 4) {
+    if (__ldg(m.bus_row + i) < 0) continue;  // slack: no equations
+    const double2 u = ld2(su, i);
+    const bool pq = __ldg(m.qidx + i) >= 0;
+    double2 acc = make_double2(0.0, 0.0);
+    int dslot = -1;
+    double2 dy = make_double2(0.0, 0.0);
+    const int a0 = __ldg(m.asm_ptr + i), a1 = __ldg(m.asm_ptr + i + 1);
+    for (int a = a0; a < a1; ++a) {
+      const int slot = __ldg(m.asm_slot + a);
+      const double2 y = __ldg(m.asm_y + a);
+      const int jb = __ldg(m.asm_j + a);
+      const double2 uj = ld2(su, jb);
+      acc.x += y.x * uj.x - y.y * uj.y;
+      acc.y += y.x * uj.y + y.y * uj.x;
+      if (jb == i) {
+        dslot = slot;
+        dy = y;
+        continue;
+      }
+      if (slot < 0) continue;  // slack column
+      const double2 wv = mul_conj(u, cmul(y, ld2(se, jb)));
+      const double2 wt = mul_conj(u, cmul(y, uj));
+      put(slot, make_double2(wt.y, -wt.x), wv, pq, __ldg(m.qidx + jb) >= 0, false);
+    }
+    if (dslot >= 0) {
+      const double2 ei = ld2(se, i);
+      const double2 wv = mul_conj(u, cmul(dy, ei));
+      const double2 yu = cmul(dy, u);
+      const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
+      put(dslot, make_double2(-wt.y, wt.x),
+          make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x)), pq, pq,
+          true);
+    }
+  }
 }
 
 __global__ void nr_check_kernel(NrWorkspace w, int64_t batch, int max_newton, double tol) {
@@ -886,6 +922,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     return cudaMemcpyAsync(w.host_active, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
   };
   auto body = [&](cudaStream_t st) -> cudaError_t {
+    nr_jacobian_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
     if (v == 3)
       launch_levels<V1>(m, hs, w, groups, st, true);
     else
@@ -902,7 +939,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     nr_step_advance_kernel<<<1, 1, 0, st>>>(w);
     return cudaGetLastError();
   };
-  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 2, n_body0 = 2;
+  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 3, n_body0 = 2;
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
                      graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
