@@ -125,6 +125,17 @@ acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_
                             int32_t n_theta, const int32_t* theta_block, int32_t n_q,
                             const int32_t* q_block, const int32_t* perm, acpf_nr_plan_info* info);
 
+/* Host-only (no GPU): solve J(x0) x = rhs with the LU of the flat-start
+ * Jacobian that every scenario's first Newton step shares (the factor
+ * acpf_nr_plan_create builds). rhs, x_out: len n_theta + n_q in the
+ * reference's unknown order [theta_block; q_block]. ACPF_ESTRUCT on a zero
+ * pivot. For checking the shared factor against a dense Jacobian.          */
+acpf_status acpf_nr_flat_start_solve(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                                     const double* y_re, const double* y_im, int32_t n_theta,
+                                     const int32_t* theta_block, int32_t n_q, const int32_t* q_block,
+                                     const double* theta_init, const double* vmag_init,
+                                     const int32_t* perm, const double* rhs, double* x_out);
+
 acpf_status acpf_nr_plan_info_get(acpf_nr_plan_t plan, acpf_nr_plan_info* info);
 
 /* Export the plan's ordering (len n_j) and LU row pointers (len n_j+1). */

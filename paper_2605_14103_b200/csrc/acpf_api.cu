@@ -360,6 +360,66 @@ acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_
   return ACPF_OK;
 }
 
+acpf_status acpf_nr_flat_start_solve(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                                     const double* y_re, const double* y_im, int32_t n_theta,
+                                     const int32_t* theta_block, int32_t n_q, const int32_t* q_block,
+                                     const double* theta_init, const double* vmag_init, const int32_t* perm,
+                                     const double* rhs, double* x_out) {
+  if (n_bus <= 0 || !y_rowptr || !y_col || !y_re || !y_im || n_theta < 0 || n_q < 0 ||
+      (n_theta && !theta_block) || (n_q && !q_block) || !theta_init || !vmag_init || !rhs || !x_out) {
+    set_error("acpf_nr_flat_start_solve: invalid argument");
+    return ACPF_EINVAL;
+  }
+  try {
+    // the same analysis, schedule and shared factor acpf_nr_plan_create builds
+    NrSymbolic first, s;
+    build_nr_symbolic(first, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, perm);
+    const std::vector<int32_t> lperm = level_sorted_perm(first);
+    build_nr_symbolic(s, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, lperm.data());
+    NrSchedule sc;
+    build_nr_schedule(s, y_rowptr, y_col, y_re, y_im, sc, 512, true);
+    std::vector<int32_t> qidx(n_bus, -1);
+    for (int k = 0; k < n_q; ++k) qidx[q_block[k]] = k;
+    std::vector<double> v;
+    if (!nr_flat_start_factor(s, sc, n_bus, y_rowptr, y_col, y_re, y_im, qidx.data(), theta_init, vmag_init, v)) {
+      set_error("acpf_nr_flat_start_solve: zero pivot in the flat-start Jacobian");
+      return ACPF_ESTRUCT;
+    }
+    // rhs / x in the reference's unknown order [theta_block; q_block]; a PV
+    // bus's padded V unknown has the identity equation dV = 0
+    const int nr = s.n_j;
+    std::vector<double> y(2 * (size_t)nr, 0.0);
+    for (int k = 0; k < n_theta; ++k) y[2 * (size_t)sc.bus_row[theta_block[k]]] = rhs[k];
+    for (int k = 0; k < n_q; ++k) y[2 * (size_t)sc.bus_row[q_block[k]] + 1] = rhs[n_theta + k];
+    for (int p = 0; p < nr; ++p) {  // y_p = inv(D_p) (b_p - sum_t L^_pt y_t)
+      double a0 = y[2 * p], a1 = y[2 * p + 1];
+      for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) {
+        const double* l = &v[4 * t];
+        const double* yc = &y[2 * (size_t)s.col[t]];
+        a0 -= l[0] * yc[0] + l[1] * yc[1];
+        a1 -= l[2] * yc[0] + l[3] * yc[1];
+      }
+      const double* d = &v[4 * s.diag[p]];
+      y[2 * p] = d[0] * a0 + d[1] * a1;
+      y[2 * p + 1] = d[2] * a0 + d[3] * a1;
+    }
+    for (int p = nr - 1; p >= 0; --p) {  // x_p = y_p - sum_c U^_pc x_c
+      for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t) {
+        const double* u = &v[4 * t];
+        const double* xc = &y[2 * (size_t)s.col[t]];
+        y[2 * p] -= u[0] * xc[0] + u[1] * xc[1];
+        y[2 * p + 1] -= u[2] * xc[0] + u[3] * xc[1];
+      }
+    }
+    for (int k = 0; k < n_theta; ++k) x_out[k] = y[2 * (size_t)sc.bus_row[theta_block[k]]];
+    for (int k = 0; k < n_q; ++k) x_out[n_theta + k] = y[2 * (size_t)sc.bus_row[q_block[k]] + 1];
+  } catch (const std::exception& ex) {
+    set_error(std::string("acpf_nr_flat_start_solve: ") + ex.what());
+    return ACPF_EINVAL;
+  }
+  return ACPF_OK;
+}
+
 acpf_status acpf_nr_plan_info_get(acpf_nr_plan_t p, acpf_nr_plan_info* info) {
   if (!p || !info) {
     set_error("acpf_nr_plan_info_get: null argument");

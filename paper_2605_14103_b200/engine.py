@@ -28,7 +28,8 @@ ZB_CONVERGED, ZB_MAX_ITER, ZB_FLOOR = range(3)
 
 EXPORTED = (
     "acpf_last_error", "acpf_abi_version", "acpf_device_count",
-    "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_plan_info_get", "acpf_nr_plan_structure",
+    "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
+    "acpf_nr_plan_structure",
     "acpf_nr_solve", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
     "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
@@ -88,6 +89,7 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_device_count": (I32, []),
         "acpf_nr_plan_create": (I32, [I32, I32, P, P, P, P, I32, P, I32, P, P, P, P, P]),
         "acpf_nr_analyze": (I32, [I32, P, P, I32, P, I32, P, P, P]),
+        "acpf_nr_flat_start_solve": (I32, [I32, P, P, P, P, I32, P, I32, P, P, P, P, P, P]),
         "acpf_nr_plan_info_get": (I32, [P, P]),
         "acpf_nr_plan_structure": (I32, [P, P, P]),
         "acpf_nr_solve": (I32, [P, I64, P, P, D, I32, P, P, P, P, P, P, U32, P]),
@@ -170,6 +172,29 @@ def nr_analyze(y_csr, theta_block, q_block, perm=None) -> dict:
     _check(lib.acpf_nr_analyze(y.shape[0], _ptr(rowptr), _ptr(col), tb.size, _ptr(tb), qb.size,
                                _ptr(qb), _ptr(pm), C.byref(info)))
     return {f: getattr(info, f) for f, _ in NrPlanInfo._fields_}
+
+
+def nr_flat_start_solve(y_csr, theta_block, q_block, theta_init, vmag_init, rhs, perm=None):
+    """Host-only: x = J(x0)^-1 rhs with the flat-start LU shared by every
+    scenario's first Newton step (acpf_nr_flat_start_solve)."""
+    lib = load_library()
+    y = y_csr.tocsr()
+    y.sort_indices()
+    rowptr = np.ascontiguousarray(y.indptr, dtype=np.int32)
+    col = np.ascontiguousarray(y.indices, dtype=np.int32)
+    yr = np.ascontiguousarray(y.data.real, dtype=np.float64)
+    yi = np.ascontiguousarray(y.data.imag, dtype=np.float64)
+    tb = np.ascontiguousarray(theta_block, dtype=np.int32)
+    qb = np.ascontiguousarray(q_block, dtype=np.int32)
+    th = np.ascontiguousarray(theta_init, dtype=np.float64)
+    vm = np.ascontiguousarray(vmag_init, dtype=np.float64)
+    b = np.ascontiguousarray(rhs, dtype=np.float64)
+    x = np.empty_like(b)
+    pm = None if perm is None else np.ascontiguousarray(perm, dtype=np.int32)
+    _check(lib.acpf_nr_flat_start_solve(y.shape[0], _ptr(rowptr), _ptr(col), _ptr(yr), _ptr(yi), tb.size,
+                                        _ptr(tb), qb.size, _ptr(qb) if qb.size else None, _ptr(th), _ptr(vm),
+                                        _ptr(pm), _ptr(b), _ptr(x)))
+    return x
 
 
 def _out_array(shape, dtype, device):

@@ -66,3 +66,19 @@ def test_no_cpu_fallback_without_gpu():
     m = pf.build_transmission_model(load_transmission("case14"))
     with pytest.raises(engine.EngineUnavailable):
         pf.newton_solve(m)
+
+
+@pytest.mark.parametrize("case", ["case14", "case118", "gb2224"])
+def test_flat_start_lu_solves_dense_jacobian(case):
+    """The LU shared by every scenario's first Newton step (host-built, what the
+    device's step 0 substitutes with) solves the flat-start Jacobian of
+    dense_jacobian (transmission.py:383-407) to rounding."""
+    model = pf.build_transmission_model(load_transmission(case))
+    st = tx.flat_start(model.net, model.part)
+    j = tx.dense_jacobian(st, model.y, model.part)
+    rhs = np.random.default_rng(7).standard_normal(j.shape[0])
+    x = engine.nr_flat_start_solve(model.y.csr, model.part.theta_block, model.part.q_block, st.theta,
+                                   st.vmag, rhs, perm=tx.jacobian_ordering(model))
+    ref = np.linalg.solve(j, rhs)
+    assert np.abs(x - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
+    assert np.abs(j @ x - rhs).max() <= 1e-9 * max(1.0, np.abs(rhs).max())
