@@ -291,8 +291,6 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
     }
     double sn, cs;
     sincos(t, &sn, &cs);
-    SL(gb.s, m.off_e + 2 * i) = cs;
-    SL(gb.s, m.off_e + 2 * i + 1) = sn;
     SL(gb.s, m.off_u + 2 * i) = v * cs;
     SL(gb.s, m.off_u + 2 * i + 1) = v * sn;
     neg |= v <= 0.0;
@@ -373,7 +371,7 @@ __global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDevic
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
   const GroupBase gb = group_base(m, w, g, sc);
   const double* __restrict__ su = gb.s + m.off_u * kGroup;
-  const double* __restrict__ se = gb.s + m.off_e * kGroup;
+  const double* __restrict__ svm = gb.s + m.off_vm * kGroup;  // V_j: svm[j*8]
   double* __restrict__ blk = gb.b;
   auto ld2 = [](const double* __restrict__ base, int j) {
     return make_double2(__ldg(base + (size_t)(2 * j) * kGroup), __ldg(base + (size_t)(2 * j + 1) * kGroup));
@@ -406,14 +404,18 @@ __global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDevic
         continue;
       }
       if (slot < 0) continue;  // slack column
-      const double2 wv = mul_conj(u, cmul(y, ld2(se, jb)));
+      // u_i conj(y E_j) = u_i conj(y u_j) / V_j (V_j real): no E gather
       const double2 wt = mul_conj(u, cmul(y, uj));
+      const double rv = 1.0 / __ldg(svm + (size_t)jb * kGroup);
+      const double2 wv = make_double2(wt.x * rv, wt.y * rv);
       put(slot, make_double2(wt.y, -wt.x), wv, pq, __ldg(m.qidx + jb) >= 0, false);
     }
     if (dslot >= 0) {
-      const double2 ei = ld2(se, i);
-      const double2 wv = mul_conj(u, cmul(dy, ei));
+      const double rv = 1.0 / __ldg(svm + (size_t)i * kGroup);
+      const double2 ei = make_double2(u.x * rv, u.y * rv);  // E_i = u_i / V_i
       const double2 yu = cmul(dy, u);
+      const double2 wv0 = mul_conj(u, yu);
+      const double2 wv = make_double2(wv0.x * rv, wv0.y * rv);
       const double2 wt = mul_conj(u, make_double2(acc.x - yu.x, acc.y - yu.y));
       put(dslot, make_double2(-wt.y, wt.x),
           make_double2(wv.x + (acc.x * ei.x + acc.y * ei.y), wv.y + (acc.x * ei.y - acc.y * ei.x)), pq, pq,
