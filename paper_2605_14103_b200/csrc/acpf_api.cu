@@ -248,12 +248,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   p->h_tpos = tpos;
   p->h_qidx = qidx;
   // LU of the flat-start Jacobian, shared by every scenario's first step
-  std::vector<double> sh_vals;
+  std::vector<double> sh_vals, sh_s0;
   bool shared0 = false;
   if (env_int("ACPF_NR_SHARED0", 1)) {
     try {
       shared0 = nr_flat_start_factor(s, sc, n_bus, y_rowptr, y_col, y_re, y_im, qidx.data(), theta_init,
-                                     vmag_init, sh_vals);
+                                     vmag_init, sh_vals, &sh_s0);
     } catch (const std::exception&) {
       shared0 = false;
     }
@@ -326,6 +326,12 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     up(const_cast<double**>(&d.sh_vals), sh_vals.data(), sh_vals.size());
     up(const_cast<int32_t**>(&d.sh_col), sh_col.data(), sh_col.size());
     up(const_cast<int32_t**>(&d.sh_diag), sh_diag.data(), sh_diag.size());
+    // the step-0 mismatch reads the flat-start S_i instead of gathering (the
+    // V <= 0 exit check at step 0 then needs V > 0 everywhere at the flat start)
+    bool vpos = true;
+    for (int i = 0; i < n_bus; ++i) vpos = vpos && vmag_init[i] > 0.0;
+    if (vpos && env_int("ACPF_NR_S0", 1))
+      up(const_cast<double2**>(&d.sh_s0), reinterpret_cast<const double2*>(sh_s0.data()), (size_t)n_bus);
   }
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);

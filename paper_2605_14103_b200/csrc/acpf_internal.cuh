@@ -50,6 +50,7 @@ struct NrDeviceModel {
   const double* sh_vals;   // [nnz_lu][4] L^ / inv(D) / U^, row-major 2x2
   const int32_t* sh_col;   // [nnz_lu] block column of the slot
   const int32_t* sh_diag;  // [n_rows] diagonal slot of the row
+  const double2* sh_s0;    // [n_bus] S_i at the flat start (step-0 mismatch), or null
 };
 
 struct NrHostSchedule {

@@ -274,8 +274,10 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   if (g >= w.groups || !w.gactive[g]) return;
   const int i0 = (int)(item % nch) * kBusChunk, i1 = min(m.n_bus, i0 + kBusChunk);
   const GroupBase gb = group_base(m, w, g, sc);
-  const bool upd = *w.kstep > 0 && w.active[g * kGroup + sc];
+  const int k = *w.kstep;
+  const bool upd = k > 0 && w.active[g * kGroup + sc];
   bool neg = false;
+  if (k == 0 && m.sh_s0) return;  // flat start: S_i shared (nr_mismatch_kernel), V > 0 checked on the host
   for (int i = i0 + r; i < i1; i += 4) {
     double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
     if (upd) {
@@ -318,19 +320,24 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
   };
   double fmx = 0.0;
   int bad = 0;  // bit0 NaN, bit1 Inf
+  const bool s0 = m.sh_s0 != nullptr && *w.kstep == 0;
   for (int i = i0 + r; i < i1; i += 4) {
     const int p = __ldg(m.bus_row + i);
     if (p < 0) continue;  // slack: no equations
-    double2 acc = make_double2(0.0, 0.0);
-    const int e1 = __ldg(m.y_rowptr + i + 1);
-    for (int e = __ldg(m.y_rowptr + i); e < e1; ++e) {
-      const double2 y = __ldg(m.y_val + e);
-      const double2 uj = ld2(su, __ldg(m.y_col + e));
-      acc.x += y.x * uj.x - y.y * uj.y;
-      acc.y += y.x * uj.y + y.y * uj.x;
+    double2 sv;
+    if (s0) {
+      sv = __ldg(m.sh_s0 + i);  // step 0: every scenario sits at the flat start
+    } else {
+      double2 acc = make_double2(0.0, 0.0);
+      const int e1 = __ldg(m.y_rowptr + i + 1);
+      for (int e = __ldg(m.y_rowptr + i); e < e1; ++e) {
+        const double2 y = __ldg(m.y_val + e);
+        const double2 uj = ld2(su, __ldg(m.y_col + e));
+        acc.x += y.x * uj.x - y.y * uj.y;
+        acc.y += y.x * uj.y + y.y * uj.x;
+      }
+      sv = mul_conj(ld2(su, i), acc);  // S_i = u_i conj(I_i)
     }
-    const double2 u = ld2(su, i);
-    const double2 sv = mul_conj(u, acc);  // S_i = u_i conj(I_i)
     const bool pq = __ldg(m.qidx + i) >= 0;
     const double fp = sv.x - __ldg(gb.s + (m.off_spec + 2 * p) * kGroup);
     bad |= isnan(fp) ? 1 : (isinf(fp) ? 2 : 0);

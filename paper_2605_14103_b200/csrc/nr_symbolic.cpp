@@ -455,7 +455,8 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
 // pivot (the caller then factors step 0 per scenario as in every other step).
 bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, const int32_t* y_rowptr,
                           const int32_t* y_col, const double* y_re, const double* y_im, const int32_t* qidx,
-                          const double* theta0, const double* vmag0, std::vector<double>& vals) {
+                          const double* theta0, const double* vmag0, std::vector<double>& vals,
+                          std::vector<double>* s0) {
   const int nr = s.n_j;
   const int64_t nslots = s.rowptr[nr];
   std::vector<double> er(n_bus), ei(n_bus), ur(n_bus), ui(n_bus);
@@ -467,6 +468,7 @@ bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, c
   }
   std::vector<double> a(4 * nslots, 0.0);
   std::vector<int64_t> where(nr, -1);
+  if (s0) s0->assign(2 * (size_t)n_bus, 0.0);
   for (int i = 0; i < n_bus; ++i) {
     const int p = o.bus_row[i];
     if (p < 0) continue;
@@ -475,6 +477,10 @@ bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, c
       const int j = y_col[e];
       ir += y_re[e] * ur[j] - y_im[e] * ui[j];
       ii += y_re[e] * ui[j] + y_im[e] * ur[j];
+    }
+    if (s0) {  // S_i = u_i conj(I_i) at the flat start (the step-0 mismatch of every scenario)
+      (*s0)[2 * i] = ur[i] * ir + ui[i] * ii;
+      (*s0)[2 * i + 1] = ui[i] * ir - ur[i] * ii;
     }
     for (int64_t t = s.rowptr[p]; t < s.rowptr[p + 1]; ++t) where[s.col[t]] = t;
     const bool pq = qidx[i] >= 0;

@@ -85,7 +85,8 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
 // scenario (see nr_symbolic.cpp); false on a zero pivot or non-finite value.
 bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, const int32_t* y_rowptr,
                           const int32_t* y_col, const double* y_re, const double* y_im, const int32_t* qidx,
-                          const double* theta0, const double* vmag0, std::vector<double>& vals);
+                          const double* theta0, const double* vmag0, std::vector<double>& vals,
+                          std::vector<double>* s0 = nullptr);
 
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
