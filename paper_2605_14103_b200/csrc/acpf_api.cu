@@ -665,8 +665,9 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
     uint8_t* cv;
   } sets[2];
   NrWorkspace ws[2];
-  NrGraphCache* graphs[2];
-  for (int k = 0; k < 2; ++k) {
+  NrGraphCache* graphs[2] = {nullptr, nullptr};
+  const int n_lanes = n_chunks > 1 ? 2 : 1;  // one chunk: no second workspace
+  for (int k = 0; k < n_lanes; ++k) {
     NrLane& L = p->lanes[k];
     if (!L.st) ACPF_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
     if (!L.ev_h2d) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_h2d, cudaEventDisableTiming));
@@ -773,7 +774,7 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   } else {
     run(0);
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < n_lanes; ++k)
     if (lrc[k] != ACPF_OK) {
       set_error(lerr[k]);
       return lrc[k];
