@@ -277,7 +277,7 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   o.n_block = o.off_yx + nr;
   int64_t e = 0;
   o.off_u = e;     e += 2 * (int64_t)nb;
-  o.off_e = e;     e += 2 * (int64_t)nb;
+  o.off_e = -1;    // no E = e^{j theta} vector: the Jacobian uses u_j / V_j
   o.off_spec = e;  e += 2 * (int64_t)nr;   // p_spec, q_spec per block row (0 for PV's q)
   o.off_th = e;    e += nb;
   o.off_vm = e;    e += nb;
