@@ -209,8 +209,8 @@ def test_nr_empty_and_ragged_batches(tx_models, golden):
         np.testing.assert_array_equal(out["iterations"], g["iterations"][:b])
 
 
-@pytest.mark.parametrize("pipeline", ["0", "1", "2"])
-def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch, pipeline):
+@pytest.mark.parametrize("pipeline,chunk", [("0", "136"), ("1", "136"), ("2", "136"), ("2", "232"), ("2", "1000")])
+def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch, pipeline, chunk):
     # ragged chunks (ACPF_NR_CHUNK) through the host paths (0 serial, 1 copy
     # stream, 2 two concurrent chunk lanes) and the device-pointer path give
     # the same bits as one chunk
@@ -219,7 +219,7 @@ def test_nr_chunked_and_pipelined_paths_agree(tx_models, monkeypatch, pipeline):
     base = pf.transmission_base(model.net, model.part)
     p, q = pf.make_scenario_arrays(base, pf.ScenarioSpec(count=1000, seed=1010))
     ref = model.plan().solve(p, q, 1e-8, 20)
-    monkeypatch.setenv("ACPF_NR_CHUNK", "136")
+    monkeypatch.setenv("ACPF_NR_CHUNK", chunk)  # 136: 8 chunks; 232: 5 (odd, ragged); 1000: one
     monkeypatch.setenv("ACPF_NR_PIPELINE", pipeline)
     model2 = pf.build_transmission_model(load_transmission("case118"))
     chunked = model2.plan().solve(p, q, 1e-8, 20)
