@@ -366,6 +366,12 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
 // (dense_jacobian, transmission.py:383-407). I_i = sum_j Y_ij u_j is
 // accumulated over the same assembly list (the Ybus row in order, slack
 // columns included), the diagonal block written after the row.
+// 1 / V_j for the dV terms: gathered (default) or |u_j| recomputed (ACPF_EXP_VABS)
+#ifdef ACPF_EXP_VABS
+#define ACPF_INV_V(uv, j) (1.0 / sqrt((uv).x * (uv).x + (uv).y * (uv).y))
+#else
+#define ACPF_INV_V(uv, j) (1.0 / __ldg(svm + (size_t)(j) * kGroup))
+#endif
 #ifndef ACPF_JAC_MINB
 #define ACPF_JAC_MINB 8
 #endif
@@ -413,12 +419,12 @@ __global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDevic
       if (slot < 0) continue;  // slack column
       // u_i conj(y E_j) = u_i conj(y u_j) / V_j (V_j real): no E gather
       const double2 wt = mul_conj(u, cmul(y, uj));
-      const double rv = 1.0 / __ldg(svm + (size_t)jb * kGroup);
+      const double rv = ACPF_INV_V(uj, jb);
       const double2 wv = make_double2(wt.x * rv, wt.y * rv);
       put(slot, make_double2(wt.y, -wt.x), wv, pq, __ldg(m.qidx + jb) >= 0, false);
     }
     if (dslot >= 0) {
-      const double rv = 1.0 / __ldg(svm + (size_t)i * kGroup);
+      const double rv = ACPF_INV_V(u, i);
       const double2 ei = make_double2(u.x * rv, u.y * rv);  // E_i = u_i / V_i
       const double2 yu = cmul(dy, u);
       const double2 wv0 = mul_conj(u, yu);
