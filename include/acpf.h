@@ -161,8 +161,13 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t plan, int64_t batch, const double* p_sp
                           int32_t* iterations, double* final_mismatch_inf, int32_t* status,
                           uint32_t flags, void* cuda_stream);
 
-/* Device time (ms) of the last acpf_nr_solve's Newton kernel launches,
- * measured with CUDA events on the solve stream; and their launch count. */
+/* Time (ms) of the last acpf_nr_solve, measured with CUDA events, and the
+ * number of kernel launches it made. Device pointers (and the host-pointer
+ * serial / copy-stream pipelines, ACPF_NR_PIPELINE=0/1): the device time of
+ * the Newton kernel launches on the solve stream. Host pointers on the
+ * default two-lane pipeline: the wall time of the whole call on the device,
+ * from the first H2D to the last D2H (copies included), since the two lanes'
+ * kernels overlap each other and the copies. */
 acpf_status acpf_nr_last_timing(acpf_nr_plan_t plan, double* kernel_ms, int32_t* launches);
 
 acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t plan);

@@ -132,10 +132,17 @@ def apply_multipliers(base, multipliers):
                                 delta_s=base.delta_s * m[kinds == "delta"])
 
 
-def make_scenarios(base, spec: ScenarioSpec) -> list:
-    """Full seeded batch as scenario objects (reference :154-159)."""
-    mult = generate_load_multipliers(spec, base.n_elements)
-    return [apply_multipliers(base, mult[i]) for i in range(spec.count)]
+def make_scenarios(base, spec: ScenarioSpec):
+    """Full seeded batch as scenario objects (reference :154-159).
+
+    Returned as a sequence of scenario objects backed by the stacked arrays
+    (results.TransmissionScenarios / DistributionScenarios; every item is
+    bitwise ``apply_multipliers(base, m_i)``), which the GPU solvers consume
+    without re-stacking."""
+    from .results import DistributionScenarios, TransmissionScenarios
+    a, b = make_scenario_arrays(base, spec)
+    cls = TransmissionScenarios if isinstance(base, TransmissionBase) else DistributionScenarios
+    return cls(a, b)
 
 
 def make_scenario_arrays(base, spec: ScenarioSpec, start: int = 0,
@@ -205,18 +212,69 @@ def _failure(exc: BaseException) -> str:
     return f"{type(exc).__name__}: {exc}"
 
 
-def _run_batched(solver, scenarios: list, warmup: bool):
-    """One device call for the whole batch; per-scenario time = total / count."""
+def _run_batched(solver, scenarios, warmup: bool):
+    """One device call for the whole batch; per-scenario time = total / count.
+
+    Isolation as the reference's ``_timed_solve`` (batch.py:230-252): the
+    warm-up never aborts the run; scenarios the solver rejects come back as
+    records with ``error`` set and result ``None``; if the batched call itself
+    raises, every scenario is re-solved on its own so only the poisoned ones
+    fail."""
     if warmup:
-        solver.solve_batch(scenarios[:1])
+        try:
+            solver.solve_batch(scenarios[:1])
+        except Exception:
+            pass
     t0 = time.perf_counter()
     try:
-        results, err = list(solver.solve_batch(scenarios)), None
-    except Exception as exc:  # a whole-batch failure becomes one error per record
-        results, err = [None] * len(scenarios), _failure(exc)
+        results = solver.solve_batch(scenarios)
+    except Exception:
+        results = None
+    if results is None:
+        outcomes = []
+        for k in range(len(scenarios)):
+            try:
+                one = solver.solve_batch(scenarios[k:k + 1])
+                errs = getattr(one, "errors", {}) or {}
+                r, err = (None, errs[0]) if 0 in errs else (one[0], None)
+            except Exception as exc:
+                r, err = None, _failure(exc)
+            outcomes.append((r, err))
+        total = time.perf_counter() - t0
+        share = total / len(scenarios)
+        return [(r, share, err) for r, err in outcomes], total
     total = time.perf_counter() - t0
     share = total / len(scenarios)
-    return [(r, share, err) for r in results], total
+    errors = getattr(results, "errors", {}) or {}
+    if hasattr(results, "converged") and callable(results.converged):
+        return _BatchedOutcome(results, share, errors), total
+    return [(None, share, errors[k]) if k in errors else (r, share, None)
+            for k, r in enumerate(results)], total
+
+
+class _BatchedOutcome:
+    """Array-backed outcomes of a batched solve (results.NewtonResults /
+    ZbusResults): records are built from the stacked arrays, result objects
+    only on demand."""
+
+    def __init__(self, results, share: float, errors: dict):
+        self.results, self.share, self.errors = results, share, errors
+
+    def records(self) -> tuple:
+        conv = self.results.converged()
+        its = self.results.iterations()
+        resid = self.results.residuals()
+        diag = self.results.diagnostics()
+        out = []
+        for k in range(conv.size):
+            if k in self.errors:
+                out.append(ScenarioRecord(k, False, 0, float("inf"), self.share, self.errors[k]))
+            else:
+                out.append(ScenarioRecord(k, bool(conv[k]), int(its[k]), float(resid[k]), self.share, diag[k]))
+        return tuple(out)
+
+    def result_objects(self) -> tuple:
+        return tuple(None if k in self.errors else self.results[k] for k in range(len(self.results)))
 
 
 def _run_serial(solver, scenarios: list, warmup: bool):
@@ -239,14 +297,19 @@ def _run_serial(solver, scenarios: list, warmup: bool):
 
 
 def _report(outcomes, total: float, worker_count: int, keep_results: bool) -> BatchReport:
-    records = tuple(_record(k, res, wall, err) for k, (res, wall, err) in enumerate(outcomes))
+    if isinstance(outcomes, _BatchedOutcome):
+        records = outcomes.records()
+        results = outcomes.result_objects() if keep_results else ()
+    else:
+        records = tuple(_record(k, res, wall, err) for k, (res, wall, err) in enumerate(outcomes))
+        results = tuple(res for res, _, _ in outcomes) if keep_results else ()
     return BatchReport(
         records=records,
         n_converged=sum(rec.converged for rec in records),
         total_wall_time=total,
         throughput=len(records) / total if total > 0 else float("inf"),
         worker_count=worker_count,
-        results=tuple(res for res, _, _ in outcomes) if keep_results else (),
+        results=results,
     )
 
 
@@ -274,8 +337,9 @@ def run_batch(
     """
     if worker_count < 1:
         raise ValueError("worker_count must be >= 1")
-    scenarios = list(scenarios)
-    if not scenarios:
+    if not hasattr(scenarios, "arrays"):
+        scenarios = list(scenarios)
+    if len(scenarios) == 0:
         raise ValueError("empty scenario batch")
     run = _run_batched if hasattr(solver, "solve_batch") else _run_serial
     outcomes, total = run(solver, scenarios, warmup)

@@ -651,6 +651,8 @@ static acpf_status nr_lane_workspace(acpf_nr_plan* p, NrLane& L, int64_t groups)
 // lane 0's D2H runs while lane 1 finishes; the two solves share the GPU, so
 // their level launches fill each other's tails (a chunk solved alone loses
 // ~10% in launch tails against the whole batch).
+constexpr acpf_status kLaneFallback = 1;  // internal: second lane unavailable
+
 static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk, const double* p_spec,
                                   const double* q_spec, double tol, int32_t max_newton, double* theta_out,
                                   double* vmag_out, uint8_t* converged, int32_t* iterations,
@@ -678,7 +680,9 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
       ws[0] = p->ws;
       graphs[0] = nr_graphs(p);
     } else {
-      if ((rc = nr_lane_workspace(p, L, groups)) != ACPF_OK) return rc;
+      // lane 1's workspace; if it does not fit, the caller falls back to the
+      // single-workspace copy-stream pipeline (nr_solve_host)
+      if ((rc = nr_lane_workspace(p, L, groups)) != ACPF_OK) return kLaneFallback;
       if (!L.host_active && cudaMallocHost(&L.host_active, sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         set_error("pinned host allocation failed");
@@ -715,7 +719,7 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   ACPF_CUDA(cudaEventRecord(p->ev0, st));
   cudaStream_t s0 = p->lanes[0].st, s1 = p->lanes[1].st;
   ACPF_CUDA(cudaStreamWaitEvent(s0, p->ev0, 0));
-  ACPF_CUDA(cudaStreamWaitEvent(s1, p->ev0, 0));
+  if (n_lanes > 1) ACPF_CUDA(cudaStreamWaitEvent(s1, p->ev0, 0));  // lane 1 exists only for >1 chunk
   acpf_status rc = h2d(0, s0);
   if (rc != ACPF_OK) return rc;
   if (n_chunks > 1) {
@@ -782,7 +786,7 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   float ms = 0.0f, ms1 = 0.0f;
   ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->lanes[0].ev_end));
   if (n_chunks > 1) ACPF_CUDA(cudaEventElapsedTime(&ms1, p->ev0, p->lanes[1].ev_end));
-  p->last_ms = std::max(ms, ms1);  // wall time of the whole host-pointer solve incl. copies
+  p->last_ms = std::max(ms, ms1);  // wall time of the whole host-pointer solve incl. copies (acpf.h)
   p->last_launches = lnl[0] + lnl[1];
   return ACPF_OK;
 }
@@ -804,18 +808,22 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   const bool dev_ptrs = flags & ACPF_DEVICE_PTRS;
 
   int64_t chunk = env_int("ACPF_NR_CHUNK", 0);
+  const int pipeline = (int)env_int("ACPF_NR_PIPELINE", 2);  // 0 serial, 1 copy stream, 2 two lanes
+  // host buffers with >= 2 chunks on two lanes hold two workspaces at once
+  const bool two_lanes = !dev_ptrs && pipeline == 2 && batch >= 2 * 8192;
   if (chunk <= 0) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const int64_t have_groups = p->ws_groups;
-    const int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
+    // the plan's existing workspaces are reusable, so they count as free
+    const int64_t have_groups = p->ws_groups + (two_lanes ? p->lanes[1].groups : 0);
+    int64_t budget = (int64_t)(free_b * 0.6) + have_groups * p->bytes_per_group;
+    if (two_lanes) budget /= 2;
     int64_t groups = std::max<int64_t>(1, budget / std::max<int64_t>(1, p->bytes_per_group));
     groups = std::min<int64_t>(groups, 16384);
     chunk = groups * kGroup;
   }
   chunk = std::min<int64_t>(chunk, batch);
   // host buffers: at least two chunks so transfers overlap the solves
-  const int pipeline = (int)env_int("ACPF_NR_PIPELINE", 2);  // 0 serial, 1 copy stream, 2 two lanes
   if (!dev_ptrs && env_int("ACPF_NR_CHUNK", 0) <= 0 && batch >= 2 * 8192) {
     chunk = std::min<int64_t>(chunk, (batch + 1) / 2);
     if (pipeline == 2) chunk = std::min<int64_t>(chunk, 32768);  // two lane workspaces in flight
@@ -825,9 +833,14 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   acpf_status rc = nr_ensure_workspace(p, groups);
   if (rc != ACPF_OK) return rc;
 
-  if (!dev_ptrs && pipeline == 2)
-    return nr_solve_lanes(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
-                          converged, iterations, final_mismatch_inf, status, st);
+  if (!dev_ptrs && pipeline == 2) {
+    rc = nr_solve_lanes(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
+                        converged, iterations, final_mismatch_inf, status, st);
+    if (rc != kLaneFallback) return rc;
+    cudaGetLastError();  // lane 1 did not fit: one workspace, copy-stream pipeline
+    return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
+                         converged, iterations, final_mismatch_inf, status, st);
+  }
   if (!dev_ptrs && pipeline == 1)
     return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
                          converged, iterations, final_mismatch_inf, status, st);
@@ -1058,7 +1071,9 @@ static acpf_status zbus_solve_host(acpf_zbus_plan* p, int64_t batch, const doubl
   const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(1, env_int("ACPF_ZBUS_CHUNK", 16384)));
   const size_t in_b = (size_t)(d.n_wye + d.n_delta) * 16;
   const size_t out_b = (size_t)d.n * 16 + 1 + 4 + 8 + 8 + 4 + 4;
-  const size_t set_b = (size_t)chunk * (in_b + out_b) + 256;
+  // each staging set (and every buffer inside it) starts on a 256-byte
+  // boundary: the kernels read s_wye/s_delta/v as double2
+  const size_t set_b = (((size_t)chunk * (in_b + out_b) + 8 * 256) + 255) & ~(size_t)255;
   acpf_status rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, 2 * set_b);
   if (rc != ACPF_OK) return rc;
   if (!p->copy_stream) ACPF_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
@@ -1077,16 +1092,21 @@ static acpf_status zbus_solve_host(acpf_zbus_plan* p, int64_t batch, const doubl
   } sets[2];
   for (int k = 0; k < 2; ++k) {
     char* b = (char*)p->stage_base + k * set_b;
+    auto take = [&](size_t bytes) {
+      char* r = b;
+      b += (bytes + 255) & ~(size_t)255;
+      return r;
+    };
     Set& S = sets[k];
-    S.sw = (double2*)b; b += (size_t)chunk * d.n_wye * 16;
-    S.sd = (double2*)b; b += (size_t)chunk * d.n_delta * 16;
-    S.vo = (double2*)b; b += (size_t)chunk * d.n * 16;
-    S.fd = (double*)b; b += (size_t)chunk * 8;
-    S.rs = (double*)b; b += (size_t)chunk * 8;
-    S.it = (int32_t*)b; b += (size_t)chunk * 4;
-    S.stt = (int32_t*)b; b += (size_t)chunk * 4;
-    S.fs = (int32_t*)b; b += (size_t)chunk * 4;
-    S.cv = (uint8_t*)b;
+    S.sw = (double2*)take((size_t)chunk * d.n_wye * 16);
+    S.sd = (double2*)take((size_t)chunk * d.n_delta * 16);
+    S.vo = (double2*)take((size_t)chunk * d.n * 16);
+    S.fd = (double*)take((size_t)chunk * 8);
+    S.rs = (double*)take((size_t)chunk * 8);
+    S.it = (int32_t*)take((size_t)chunk * 4);
+    S.stt = (int32_t*)take((size_t)chunk * 4);
+    S.fs = (int32_t*)take((size_t)chunk * 4);
+    S.cv = (uint8_t*)take((size_t)chunk);
   }
   std::vector<cudaEvent_t> tev(2 * nchunks, nullptr);
   for (auto& e : tev) ACPF_CUDA(cudaEventCreate(&e));

@@ -366,13 +366,16 @@ class NrPlan:
         self._fd_eps = epsilon
 
     def solve_gmres(self, p_spec, q_spec, tol: float, max_newton: int, precond: str = "fd",
-                    gmres_tol: float = 1e-8, restart: int = 60, max_outer: int = 10, stream=None) -> dict:
+                    gmres_tol: float = 1e-8, restart: int = 60, max_outer: int = 10, stream=None,
+                    out: dict | None = None) -> dict:
         """The reference's Newton step (matrix-free GMRES, FD or no
         preconditioner) for a stacked batch (acpf_nr_solve_gmres)."""
         dev = _is_device(p_spec)
         b = int(p_spec.shape[0])
-        out = self.alloc_outputs(b, like=p_spec if dev else None)
-        if dev:
+        if out is not None:
+            pass
+        elif dev:
+            out = self.alloc_outputs(b, like=p_spec)
             import torch
             kw = dict(device=p_spec.device)
             out["gmres_steps"] = torch.zeros((b, max_newton), dtype=torch.int32, **kw)
@@ -380,6 +383,7 @@ class NrPlan:
             out["gmres_diag_k"] = torch.zeros(b, dtype=torch.int32, **kw)
             out["gmres_diag_relres"] = torch.zeros(b, dtype=torch.float64, **kw)
         else:
+            out = self.alloc_outputs(b)
             out["gmres_steps"] = np.zeros((b, max_newton), dtype=np.int32)
             out["gmres_diag"] = np.zeros(b, dtype=np.int32)
             out["gmres_diag_k"] = np.zeros(b, dtype=np.int32)
@@ -567,12 +571,15 @@ def zbus_reduce(y_nn, rhs0, l_index, device: int = 0):
     return zl, v0
 
 
-def zbus_plan_for(model, device: int | None = None) -> ZbusPlan:
+def zbus_plan_for(model, device: int | None = None, slot: int = 0) -> ZbusPlan:
+    """The model's plan on ``device`` (one per (device, slot): a plan is driven
+    by one host thread at a time, include/acpf.h)."""
     device = 0 if device is None else device
-    plan = model._plans.get(device)
+    key = device if slot == 0 else (device, slot)
+    plan = model._plans.get(key)
     if plan is None:
         plan = ZbusPlan(model, device)
-        model._plans[device] = plan
+        model._plans[key] = plan
     return plan
 
 
@@ -605,17 +612,9 @@ def zbus_floor_message(model, v: np.ndarray, slot: int) -> str:
 
 
 def zbus_results(model, out: dict) -> list:
-    from .distribution import FixedPointResult
-    res = []
-    for k in range(out["v"].shape[0]):
-        v = out["v"][k].copy()
-        st = int(out["status"][k])
-        diag = zbus_floor_message(model, v, int(out["floor_slot"][k])) if st == ZB_FLOOR else None
-        res.append(FixedPointResult(
-            v=v, converged=bool(out["converged"][k]), iterations=int(out["iterations"][k]),
-            final_delta=float(out["final_delta"][k]), residual_inf=float(out["residual_inf"][k]),
-            diagnostic=diag))
-    return res
+    """FixedPointResult records of stacked Z-Bus outputs (results.ZbusResults)."""
+    from .results import ZbusResults
+    return list(ZbusResults(model, out))
 
 
 @dataclass

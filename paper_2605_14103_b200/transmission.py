@@ -114,15 +114,23 @@ class TransmissionModel:
     ordering: str = "mmd"
     _plans: dict = field(default_factory=dict, repr=False)
 
-    def plan(self, device: int = 0):
+    def plan(self, device: int = 0, slot: int = 0):
+        """The device plan (one per (device, slot); a plan is driven by one
+        host thread at a time, include/acpf.h)."""
         from . import engine
-        p = self._plans.get(device)
+        key = device if slot == 0 else (device, slot)
+        p = self._plans.get(key)
         if p is None:
             st = flat_start(self.net, self.part)
-            perm = jacobian_ordering(self) if self.ordering == "mmd" else None
+            if self.ordering == "mmd":
+                perm = self._plans.get("_perm")
+                if perm is None:
+                    perm = self._plans["_perm"] = jacobian_ordering(self)
+            else:
+                perm = None
             p = engine.NrPlan(self.y.csr, self.part.theta_block, self.part.q_block, st.theta,
                               st.vmag, device=device, perm=perm)
-            self._plans[device] = p
+            self._plans[key] = p
         return p
 
 
@@ -196,13 +204,17 @@ def jacobian_ordering(model: TransmissionModel) -> np.ndarray:
 
 
 def stack_transmission_scenarios(model: TransmissionModel, scenarios) -> tuple:
-    b = len(scenarios)
-    p = np.empty((b, model.part.n_theta))
-    q = np.empty((b, model.part.n_q))
-    for k, sc in enumerate(scenarios):
-        p[k] = sc.p_spec
-        q[k] = sc.q_spec
+    """Scenarios -> contiguous (p_spec[B, n_theta], q_spec[B, n_q]); raises on a malformed one."""
+    (p, q), _, errors = _stack(model, scenarios)
+    if errors:
+        raise ValueError(next(iter(errors.values())))
     return p, q
+
+
+def _stack(model: TransmissionModel, scenarios):
+    from .results import TransmissionScenarios, stack_checked
+    return stack_checked(scenarios, ("p_spec", "q_spec"), (model.part.n_theta, model.part.n_q),
+                         np.float64, TransmissionScenarios)
 
 
 def _check_options(opts: NewtonOptions | None, start) -> NewtonOptions:
@@ -214,60 +226,82 @@ def _check_options(opts: NewtonOptions | None, start) -> NewtonOptions:
     return opts
 
 
+def status_diagnostic(out: dict, k: int):
+    """The reference's diagnostic text for row k of the engine outputs
+    (transmission.py:351, :356, :366-376; zero pivot: the engine's own)."""
+    st = int(out["status"][k])
+    if st in _STATUS_TEXT:
+        return _STATUS_TEXT[st]
+    if st == 4:
+        return f"zero pivot in the static-pivot LU at Newton iteration {int(out['iterations'][k])}"
+    if "gmres_diag" in out:
+        kind, kk = int(out["gmres_diag"][k]), int(out["gmres_diag_k"][k])
+        if kind == 1:
+            return f"GMRES breakdown at Newton iteration {kk}"
+        if kind == 2:
+            return (f"GMRES stagnated at Newton iteration {kk} "
+                    f"(relres {float(out['gmres_diag_relres'][k]):.2e})")
+    return None
+
+
 def results_from_arrays(out: dict, index=None) -> list:
     """Per-scenario NewtonResult records from the stacked engine outputs
     (with the GMRES step's per-iteration counts and diagnostics when present,
     transmission.py:366-376)."""
-    res = []
-    rng = range(out["theta"].shape[0]) if index is None else index
-    gm = "gmres_steps" in out
-    for k in rng:
-        st = int(out["status"][k])
-        it = int(out["iterations"][k])
-        per = ()
-        diag = None
-        if gm:
-            per = tuple(int(c) for c in out["gmres_steps"][k][:it])
-            kind, kk = int(out["gmres_diag"][k]), int(out["gmres_diag_k"][k])
-            if kind == 1:
-                diag = f"GMRES breakdown at Newton iteration {kk}"
-            elif kind == 2:
-                diag = (f"GMRES stagnated at Newton iteration {kk} "
-                        f"(relres {float(out['gmres_diag_relres'][k]):.2e})")
-        if st in _STATUS_TEXT:
-            diag = _STATUS_TEXT[st]
-        elif st == 4:
-            diag = f"zero pivot in the static-pivot LU at Newton iteration {it}"
-        res.append(NewtonResult(
-            state=PolarState(out["theta"][k].copy(), out["vmag"][k].copy()),
-            converged=bool(out["converged"][k]), iterations=it,
-            final_mismatch_inf=float(out["final_mismatch_inf"][k]), per_iteration_gmres=per,
-            diagnostic=diag))
-    return res
+    from .results import NewtonResults
+    res = NewtonResults(out)
+    rng = range(len(res)) if index is None else index
+    return [res[k] for k in rng]
+
+
+_FAILED_ROW = {"converged": 0, "iterations": 0, "final_mismatch_inf": np.inf, "status": -1,
+               "theta": np.nan, "vmag": np.nan}
 
 
 def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = None,
-                       device: int | None = None) -> list:
+                       device: int | None = None, devices=None):
     """Solve a list of scenarios on the GPU; order preserved.
 
     Each record equals ``newton_solve(model, scenario, opts)`` of the
-    reference (flags, iteration counts; state within 1e-8).
+    reference (flags, iteration counts; state within 1e-8). Returns a
+    sequence of ``NewtonResult`` backed by the stacked outputs
+    (results.NewtonResults). ``devices=[...]`` shards the batch into
+    contiguous ranges over several GPUs (one plan and host thread each);
+    ``device`` picks a single GPU. A malformed scenario becomes a failed
+    record (NaN state, diagnostic = the error) instead of failing the batch,
+    as the reference's batch driver isolates it (batch.py:237-239).
     """
+    from .results import NewtonResults, scatter_rows, solve_sharded
     model = _as_model(net_or_model)
     opts = _check_options(opts, None)
-    scenarios = list(scenarios)
-    if not scenarios:
-        return []
-    p, q = stack_transmission_scenarios(model, scenarios)
-    plan = model.plan(0 if device is None else device)
-    if opts.step == "gmres":
-        if getattr(plan, "_fd_eps", None) != opts.epsilon:
-            plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, opts.epsilon)
-        out = plan.solve_gmres(p, q, opts.tol_mismatch, opts.max_newton, opts.precond, opts.gmres.tol,
-                               opts.gmres.restart, opts.gmres.max_outer)
-    else:
-        out = plan.solve(p, q, opts.tol_mismatch, opts.max_newton)
-    return results_from_arrays(out)
+    if len(scenarios) == 0:
+        return NewtonResults({k: np.empty((0,) if k not in ("theta", "vmag") else (0, len(model.net.buses)))
+                              for k in _FAILED_ROW})
+    (p, q), idx, errors = _stack(model, scenarios)
+    devs = list(devices) if devices is not None else [0 if device is None else device]
+    gm = opts.step == "gmres"
+    b = p.shape[0]
+    out = model.plan(devs[0]).alloc_outputs(b)
+    if gm:
+        out["gmres_steps"] = np.zeros((b, opts.max_newton), dtype=np.int32)
+        out["gmres_diag"] = np.zeros(b, dtype=np.int32)
+        out["gmres_diag_k"] = np.zeros(b, dtype=np.int32)
+        out["gmres_diag_relres"] = np.zeros(b)
+
+    def shard(slot, dev, lo, hi, view):
+        plan = model.plan(dev, slot)
+        if gm:
+            if getattr(plan, "_fd_eps", None) != opts.epsilon:
+                plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, opts.epsilon)
+            plan.solve_gmres(p[lo:hi], q[lo:hi], opts.tol_mismatch, opts.max_newton, opts.precond,
+                             opts.gmres.tol, opts.gmres.restart, opts.gmres.max_outer, out=view)
+        else:
+            plan.solve(p[lo:hi], q[lo:hi], opts.tol_mismatch, opts.max_newton, out=view)
+
+    if b:
+        solve_sharded(b, devs, shard, out)
+    fill = dict(_FAILED_ROW, gmres_steps=0, gmres_diag=0, gmres_diag_k=0, gmres_diag_relres=0.0)
+    return NewtonResults(scatter_rows(out, idx, len(scenarios), fill), errors)
 
 
 def newton_solve(net_or_model, scenario: TransmissionScenario | None = None,
@@ -281,15 +315,18 @@ def newton_solve(net_or_model, scenario: TransmissionScenario | None = None,
 
 
 class GpuNewtonSolver:
-    """Batched solver object for :func:`.batch.run_batch`."""
+    """Batched solver object for :func:`.batch.run_batch` (``devices``: shard
+    the batch over several GPUs, results.solve_sharded)."""
 
-    def __init__(self, model: TransmissionModel, opts: NewtonOptions | None = None, device: int = 0):
+    def __init__(self, model: TransmissionModel, opts: NewtonOptions | None = None, device: int = 0,
+                 devices=None):
         self.model = model
         self.opts = opts or NewtonOptions()
         self.device = device
+        self.devices = list(devices) if devices is not None else None
 
-    def solve_batch(self, scenarios) -> list:
-        return batch_newton_solve(self.model, scenarios, self.opts, self.device)
+    def solve_batch(self, scenarios):
+        return batch_newton_solve(self.model, scenarios, self.opts, self.device, devices=self.devices)
 
     def __call__(self, scenario):
         return self.solve_batch([scenario])[0]
