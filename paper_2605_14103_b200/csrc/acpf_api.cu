@@ -212,7 +212,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     build_nr_symbolic(p->sym, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, lperm.data());
     build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch,
                       (int)env_int("ACPF_NR_TASK_ELEMS", 512),
-                      env_int("ACPF_NR_COLUMN_STORE", 1) != 0);
+                      env_int("ACPF_NR_COLUMN_STORE", 1) != 0,
+                      (int)env_int("ACPF_NR_TAIL", 0));  // dense tail: measured break-even, off
     if (env_int("ACPF_DEBUG_SCHEDULE", 0)) {  // per-level shape of the factor schedule (stderr)
       const NrSchedule& sc = p->sch;
       for (int l = 0; l < sc.n_levels; ++l) {
@@ -221,6 +222,8 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
                      sc.level_task_ptr[l + 1] - sc.level_task_ptr[l], sc.level_maxl[l],
                      sc.row_slot[r1] - sc.row_slot[r0], sc.row_sptr[r1] - sc.row_sptr[r0]);
       }
+      std::fprintf(stderr, "tail rows %d (from row %d, level %d), %zu tail slots, back levels %d\n", sc.tail_T,
+                   sc.tail_row0, sc.tail_level, sc.tail_slot.size() / 2, sc.n_blevels);
     }
   } catch (const std::exception& ex) {
     set_error(std::string("symbolic analysis: ") + ex.what());
@@ -281,6 +284,14 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   p->hs.n_levels = sc.n_levels;
   p->hs.n_blevels = sc.n_blevels;
   p->hs.max_l = sc.max_l;
+  p->hs.tail_level = sc.tail_level;
+  p->hs.n_tail_class = (int)sc.tail_class_maxl.size();
+  p->hs.tail_variant = (int)env_int("ACPF_NR_TAIL_VARIANT", 2);
+  p->hs.tail_class_ptr = sc.tail_class_ptr.data();
+  p->hs.tail_class_maxl = sc.tail_class_maxl.data();
+  d.tail_row0 = sc.tail_row0;
+  d.tail_T = sc.tail_T;
+  d.n_tail_slot = (int)(sc.tail_slot.size() / 2);
   {
     // factor pipeline variant: the requested one if its shared memory (ring +
     // the longest L part of a row) fits one SM, else the next smaller one
@@ -322,6 +333,10 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   up(const_cast<uint32_t**>(&d.brow), sc.brow.data(), sc.brow.size());
   up(const_cast<int32_t**>(&d.brow_sptr), sc.brow_sptr.data(), sc.brow_sptr.size());
   up(const_cast<uint32_t**>(&d.stream), sc.stream.data(), sc.stream.size());
+  if (d.n_tail_slot)
+    up(const_cast<int2**>(&d.tail_slot), reinterpret_cast<const int2*>(sc.tail_slot.data()),
+       (size_t)d.n_tail_slot);
+  if (!sc.tail_trow.empty()) up(const_cast<int32_t**>(&d.tail_trow), sc.tail_trow.data(), sc.tail_trow.size());
   if (shared0) {
     up(const_cast<double**>(&d.sh_vals), sh_vals.data(), sh_vals.size());
     up(const_cast<int32_t**>(&d.sh_col), sh_col.data(), sh_col.size());

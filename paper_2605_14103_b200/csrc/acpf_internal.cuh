@@ -51,6 +51,10 @@ struct NrDeviceModel {
   const int32_t* sh_col;   // [nnz_lu] block column of the slot
   const int32_t* sh_diag;  // [n_rows] diagonal slot of the row
   const double2* sh_s0;    // [n_bus] S_i at the flat start (step-0 mismatch), or null
+  // dense tail (NrSchedule::tail_*): rows tail_row0 .. n_rows-1
+  int tail_row0, tail_T, n_tail_slot;
+  const int2* tail_slot;   // [n_tail_slot] (storage element, dense block position)
+  const int32_t* tail_trow;  // [tail_T] row of each tail-level task, in class order
 };
 
 struct NrHostSchedule {
@@ -58,6 +62,11 @@ struct NrHostSchedule {
   const int32_t* level_maxl;       // [n_levels]
   const int32_t* blevel_task_ptr;  // [n_blevels+1]
   int n_levels, n_blevels, max_l;
+  int tail_level;  // factor level of the tail rows (group-major tasks), -1: no tail
+  int n_tail_class;
+  int tail_variant;  // pipeline shape of the tail level (nr_kernel.cu V0..V3)
+  const int32_t* tail_class_ptr;   // [n_tail_class+1] task ranges into tail_trow
+  const int32_t* tail_class_maxl;  // [n_tail_class] row-buffer blocks of the class
   int variant;  // factor/back pipeline shape (nr_kernel.cu: 0 = 8x8 ring, 1 = 8x4, 2 = 4x4, 3 = mixed (default))
 };
 

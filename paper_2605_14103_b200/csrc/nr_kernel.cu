@@ -508,16 +508,21 @@ __device__ __forceinline__ void pipe_setup(P& pp, const NrDeviceModel& m, const 
 // scenario groups). Lane (r, sc) owns entry (i, j) = (r/2, r%2) of every
 // block of scenario sc of each group of the unit; the NG groups share every
 // address computation (their copies sit 256 B apart in each ring slot).
+//
+// gmajor (the tail level): consecutive CTAs take the ntask row tasks of one
+// unit, so the non-tail U^ blocks every tail row of a group gathers are
+// reused from L2 while that group's rows are in flight.
 template <class P>
-__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units) {
+__global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorkspace w, int task0, int64_t units,
+                                                       int ntask, int gmajor) {
   constexpr int NG = P::NG, CH = P::CH;
   constexpr int kSlot = P::kSlot;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x, r = lane >> 3, sc = lane & 7;
   const int bi = r >> 1, bj = r & 1;
   const int64_t task = blockIdx.x;
-  const int64_t g0 = (task % units) * NG;
-  const int tk = task0 + (int)(task / units);
+  const int64_t g0 = (gmajor ? task / ntask : task % units) * NG;
+  const int tk = task0 + (int)(gmajor ? task % ntask : task / units);
   const unsigned live = unit_live<NG>(w, g0);
   if (!live) return;
   const size_t gstride = (size_t)(m.n_block * kBlk + m.n_scalar * kGroup);
@@ -533,7 +538,9 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   // this lane's entry of LU element 0 of group 0 (stores index it by slot)
   double* const luw = &BL(gb0, m.off_lu, ce);
   const uint32_t lrow = lbuf + offL;
-  const int p0 = m.task_row[tk], p1 = m.task_row[tk + 1];
+  // tail level: one row per task, listed in m.tail_trow (class order)
+  const int p0 = gmajor ? m.tail_trow[tk] : m.task_row[tk];
+  const int p1 = gmajor ? p0 + 1 : m.task_row[tk + 1];
   P pp;
   pipe_setup(pp, m, w, g0, live, ring, lane);
   pp.begin(m.stream, m.row_sptr[p0], m.row_sptr[p1]);
@@ -631,6 +638,13 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
           yacc[h] = fma(-li1, yt.y, fma(-li0, yt.x, yacc[h]));
         }
         pp.q += 1;
+      } else if (info & kSlotTail) {
+        // tail row, tail column: A_pt minus the non-tail updates, stored raw
+        // for the dense tail factorisation (nr_tail_kernel)
+        const size_t st = (size_t)(uint32_t)__shfl_sync(kFull, wstore, t - tw) * kBlk;
+#pragma unroll
+        for (int h = 0; h < NG; ++h)
+          if ((live >> h) & 1u) luw[h * gstride + st] = a[h];
       } else {
         const size_t st = (size_t)(uint32_t)__shfl_sync(kFull, wstore, t - tw) * kBlk;
 #pragma unroll
@@ -657,11 +671,17 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         break;
       }
     }
+    if (p >= m.tail_row0) {  // tail row: b_p - sum over non-tail t of L^_pt y_t, raw
 #pragma unroll
-    for (int h = 0; h < NG; ++h) {  // y_p = inv(U_pp) (b_p - sum_t L^_pt y_t)
-      const double o = __shfl_xor_sync(kFull, yacc[h], 16);  // the other row
-      const double y = ir0[h] * (bi ? o : yacc[h]) + ir1[h] * (bi ? yacc[h] : o);
-      if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = y;
+      for (int h = 0; h < NG; ++h)
+        if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = yacc[h];
+    } else {
+#pragma unroll
+      for (int h = 0; h < NG; ++h) {  // y_p = inv(U_pp) (b_p - sum_t L^_pt y_t)
+        const double o = __shfl_xor_sync(kFull, yacc[h], 16);  // the other row
+        const double y = ir0[h] * (bi ? o : yacc[h]) + ir1[h] * (bi ? yacc[h] : o);
+        if (bj == 0 && ((live >> h) & 1u)) BL(gb0 + h * gstride, m.off_yx + p, bi) = y;
+      }
     }
     __syncwarp();  // lbuf of this row complete before the next row of the task reuses it
   }
@@ -837,12 +857,252 @@ __global__ void __launch_bounds__(128) nr_shared_step_kernel(NrDeviceModel m, Nr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dense tail: on-chip LU of the top of the elimination tree (FP64 DMMA)
+// ---------------------------------------------------------------------------
+//
+// The last T block rows of the level-sorted order (NrSchedule::tail_*; for
+// gb2224 the 62 single-row "chain" levels plus one 2-row level: 64 rows,
+// 2,332+ of the 4,096 blocks filled, 49% of all Crout updates) have almost no
+// parallelism left in the sparse schedule: each level is one row and every
+// row re-gathers the U^ rows of all earlier tail rows from HBM. Instead, the
+// tail level of nr_factor_kernel applies only the updates from non-tail rows
+// (all tail rows in parallel) and stores the partial blocks raw; this kernel
+// then finishes the block LU of the 2T x 2T matrix (2T <= 128) per scenario
+// entirely on chip, right-looking in the same unit-upper 2x2-block form
+// (A = L^ U^, L^_kk = D_k, U^ = D^-1 U), with the right-hand side carried as
+// an extra column (forward substitution), followed by the back substitution.
+// The tail's U^ never goes to HBM; only x of the tail rows is written, and
+// the non-tail back substitution reads it like any other x_c.
+//
+// One CTA per scenario, 16 warps; warp w keeps scalar rows 8w..8w+7 of the
+// whole matrix (17 column tiles of 8, tile 16 = the right-hand side at column
+// 128) in registers as mma.m8n8k4.f64 accumulator fragments. Per panel of 8
+// scalar columns (4 block columns):
+//   (a) the panel column and the panel rows go to shared memory;
+//   (b) one warp factors the 8 x 8 diagonal block (4 block steps: D^-1, U^,
+//       update) - L^11, D^-1, U^11;
+//   (c) the panel rows' U^ blocks right of the panel and their y (one thread
+//       per column: forward substitution with L^11, D^-1) and the L^ blocks
+//       of the rows below (one thread per row: forward with U^11);
+//   (d) every warp below the panel updates its accumulators with two DMMAs
+//       per column tile: C -= L^(rows, panel) U^(panel, columns).
+// Pivot blocks are checked for exact zero like the sparse kernel (flag 8).
+constexpr int kTW = 16;           // warps: one 8-row strip each
+constexpr int kTRows = 2 * kTailMaxRows;  // 128 scalar rows
+constexpr int kTYCol = kTRows;    // the right-hand side column
+constexpr int kTTiles = kTRows / 8 + 1;
+constexpr int kTLd = 148;         // U row stride: 148 = 4 (mod 16), conflict-free B fragments (4 rows x 8 cols)
+constexpr int kTPcLd = 12;        // panel-column stride: conflict-free A fragments (8 rows x 4 cols)
+constexpr size_t kTailSmem = ((size_t)kTRows * kTLd + (size_t)kTRows * kTPcLd + 16 + 2 * kTRows) * 8 + 16;
+
+__device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, NrWorkspace w) {
+  extern __shared__ __align__(16) double tsm[];
+  double* const U = tsm;                  // [kTRows][kTLd]
+  double* const Pc = U + kTRows * kTLd;   // [kTRows][kTPcLd]
+  double* const Dv = Pc + kTRows * kTPcLd;  // [4][2x2] pivot inverses of the current panel
+  double* const xs = Dv + 16;             // [kTRows] solution
+  int* const zflag = reinterpret_cast<int*>(xs + 2 * kTRows);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t s = blockIdx.x;
+  const int64_t g = s / kGroup;
+  const int sc = (int)(s % kGroup);
+  if (g >= w.groups || !w.gactive[g] || !w.active[s]) return;
+  const int T = m.tail_T, n2 = 2 * T, np = (n2 + 7) >> 3;
+  const double* const gsrc = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup) + 2 * sc;
+
+  // ---- load: zero, identity on the padding, scatter the tail blocks and y
+  for (int i = tid; i < 8 * np * kTLd; i += kTW * 32) U[i] = 0.0;
+  __syncthreads();
+  for (int r = n2 + tid; r < 8 * np; r += kTW * 32) U[r * kTLd + r] = 1.0;
+  for (int k = tid; k < m.n_tail_slot; k += kTW * 32) {
+    const int2 e = __ldg(m.tail_slot + k);
+    const double* src = gsrc + (size_t)e.x * kBlk;  // column j of the block at +16 j
+    const double2 c0 = *reinterpret_cast<const double2*>(src);
+    const double2 c1 = *reinterpret_cast<const double2*>(src + 2 * kGroup);
+    const int i = e.y / T, j = e.y - (e.y / T) * T;
+    double* d = U + (2 * i) * kTLd + 2 * j;
+    d[0] = c0.x;
+    d[kTLd] = c0.y;
+    d[1] = c1.x;
+    d[kTLd + 1] = c1.y;
+  }
+  for (int i = tid; i < T; i += kTW * 32) {
+    const double2 y = *reinterpret_cast<const double2*>(gsrc + (size_t)(m.off_yx + m.tail_row0 + i) * kBlk);
+    U[(2 * i) * kTLd + kTYCol] = y.x;
+    U[(2 * i + 1) * kTLd + kTYCol] = y.y;
+  }
+  if (tid == 0) *zflag = 0;
+  __syncthreads();
+  const int crow = 8 * wid + (lane >> 2), ccol = 2 * (lane & 3);
+  double C[kTTiles][2];
+#pragma unroll
+  for (int j = 0; j < kTTiles; ++j) {
+    const double2 v = *reinterpret_cast<const double2*>(U + crow * kTLd + 8 * j + ccol);
+    C[j][0] = v.x;
+    C[j][1] = v.y;
+  }
+  __syncthreads();
+
+  for (int p = 0; p < np; ++p) {
+    const int r0 = 8 * p;
+    // (a) panel column -> Pc (rows >= r0); panel rows -> U
+    if (wid >= p && wid < np) {
+#pragma unroll
+      for (int j = 0; j < kTTiles - 1; ++j)
+        if (j == p) *reinterpret_cast<double2*>(Pc + crow * kTPcLd + ccol) = make_double2(C[j][0], C[j][1]);
+    }
+    if (wid == p) {
+#pragma unroll
+      for (int j = 0; j < kTTiles; ++j)
+        if (j >= p && (j < np || j == kTTiles - 1))
+          *reinterpret_cast<double2*>(U + crow * kTLd + 8 * j + ccol) = make_double2(C[j][0], C[j][1]);
+    }
+    __syncthreads();
+    // (b) the 8 x 8 diagonal block, 4 block steps (warp 0)
+    double* const Dg = U + r0 * kTLd + r0;
+    if (wid == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double a00 = Dg[(2 * k) * kTLd + 2 * k], a01 = Dg[(2 * k) * kTLd + 2 * k + 1];
+        const double a10 = Dg[(2 * k + 1) * kTLd + 2 * k], a11 = Dg[(2 * k + 1) * kTLd + 2 * k + 1];
+        const double det = a00 * a11 - a01 * a10;
+        const double rd = 1.0 / det;
+        const double i00 = a11 * rd, i01 = -a01 * rd, i10 = -a10 * rd, i11 = a00 * rd;
+        if (lane == 0) {
+          Dv[4 * k] = i00;
+          Dv[4 * k + 1] = i01;
+          Dv[4 * k + 2] = i10;
+          Dv[4 * k + 3] = i11;
+          if (det == 0.0 && r0 + 2 * k < n2) *zflag = 1;
+        }
+        // U^ blocks (k, mb), mb = k+1..3: lanes 0 .. 4(3-k)-1, one entry each
+        const int nu = 4 * (3 - k);
+        double u = 0.0;
+        int ui = 0, uc = 0;
+        if (lane < nu) {
+          ui = (lane & 3) >> 1;
+          uc = 2 * (k + 1 + (lane >> 2)) + (lane & 1);
+          const double f0 = Dg[(2 * k) * kTLd + uc], f1 = Dg[(2 * k + 1) * kTLd + uc];
+          u = ui ? i10 * f0 + i11 * f1 : i00 * f0 + i01 * f1;
+        }
+        __syncwarp();
+        if (lane < nu) Dg[(2 * k + ui) * kTLd + uc] = u;
+        __syncwarp();
+        // trailing entries of the block: F(ri, ci) -= L^(ri, 2k..) U^(2k.., ci)
+        const int nr = 6 - 2 * k;
+        for (int e = lane; e < nr * nr; e += 32) {
+          const int ri = 2 * k + 2 + e / nr, ci = 2 * k + 2 + e % nr;
+          Dg[ri * kTLd + ci] -= Dg[ri * kTLd + 2 * k] * Dg[(2 * k) * kTLd + ci] +
+                                Dg[ri * kTLd + 2 * k + 1] * Dg[(2 * k + 1) * kTLd + ci];
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // (c) panel rows right of the panel (thread per column, incl. y) and the
+    //     L^ blocks of the rows below (thread per row)
+    {
+      const int ncol = 8 * np - r0 - 8;
+      if (tid <= ncol) {
+        const int c = tid < ncol ? r0 + 8 + tid : kTYCol;
+        double x[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) x[r] = Dg[r * kTLd + (c - r0)];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int mb = 0; mb < k; ++mb) {
+            x[2 * k] -= Dg[(2 * k) * kTLd + 2 * mb] * x[2 * mb] + Dg[(2 * k) * kTLd + 2 * mb + 1] * x[2 * mb + 1];
+            x[2 * k + 1] -=
+                Dg[(2 * k + 1) * kTLd + 2 * mb] * x[2 * mb] + Dg[(2 * k + 1) * kTLd + 2 * mb + 1] * x[2 * mb + 1];
+          }
+          const double a = x[2 * k], b = x[2 * k + 1];
+          x[2 * k] = Dv[4 * k] * a + Dv[4 * k + 1] * b;
+          x[2 * k + 1] = Dv[4 * k + 2] * a + Dv[4 * k + 3] * b;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Dg[r * kTLd + (c - r0)] = x[r];
+      }
+      const int t = tid - 256;
+      if (t >= 0 && t < ncol) {
+        double* const row = Pc + (r0 + 8 + t) * kTPcLd;
+        double x[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = row[c];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+#pragma unroll
+          for (int mb = 0; mb < k; ++mb) {
+            x[2 * k] -= x[2 * mb] * Dg[(2 * mb) * kTLd + 2 * k] + x[2 * mb + 1] * Dg[(2 * mb + 1) * kTLd + 2 * k];
+            x[2 * k + 1] -=
+                x[2 * mb] * Dg[(2 * mb) * kTLd + 2 * k + 1] + x[2 * mb + 1] * Dg[(2 * mb + 1) * kTLd + 2 * k + 1];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) row[c] = x[c];
+      }
+    }
+    __syncthreads();
+    // (d) C -= L^(strip, panel) U^(panel, tiles right of the panel) on the DMMA pipe
+    if (wid > p && wid < np) {
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const double a = -Pc[crow * kTPcLd + 4 * s2 + (lane & 3)];
+        const double* const ub = U + (r0 + 4 * s2 + (lane & 3)) * kTLd + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < kTTiles; ++j)
+          if (j > p && (j < np || j == kTTiles - 1)) dmma_t(C[j][0], C[j][1], a, ub[8 * j]);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- back substitution x = U^-1 y (unit block upper), panel by panel from
+  // the bottom: warp 0 solves the panel's 8 x 8 unit upper block, then every
+  // row above subtracts the panel's contribution from its y (thread per row)
+  for (int p = np - 1; p >= 0; --p) {
+    const int r0 = 8 * p;
+    if (wid == 0) {
+      double t = lane < 8 ? U[(r0 + lane) * kTLd + kTYCol] : 0.0;
+      const double* const row = U + (r0 + (lane & 7)) * kTLd + r0;
+#pragma unroll
+      for (int k = 3; k >= 1; --k) {
+        const double x0 = __shfl_sync(kFull, t, 2 * k), x1 = __shfl_sync(kFull, t, 2 * k + 1);
+        if (lane < 2 * k) t -= row[2 * k] * x0 + row[2 * k + 1] * x1;
+      }
+      if (lane < 8) xs[r0 + lane] = t;
+    }
+    __syncthreads();
+    if (tid < r0) {
+      double* const row = U + tid * kTLd;
+      double acc = row[kTYCol];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc -= row[r0 + c] * xs[r0 + c];
+      row[kTYCol] = acc;
+    }
+    __syncthreads();
+  }
+  // ---- x of the tail rows -> the y/x elements (the non-tail back substitution reads them)
+  double* const gdst = w.arena + (size_t)g * (m.n_block * kBlk + m.n_scalar * kGroup) + 2 * sc;
+  for (int i = tid; i < T; i += kTW * 32)
+    *reinterpret_cast<double2*>(gdst + (size_t)(m.off_yx + m.tail_row0 + i) * kBlk) =
+        make_double2(xs[2 * i], xs[2 * i + 1]);
+  if (tid == 0 && *zflag) atomicOr(&w.flags[s], 8);
+}
+
 // pipeline variants (ACPF_NR_VARIANT; measured one-step times on gb2224 x 65536
 // in DESIGN.md): ring of 8 x 8 elements (6 stages in flight, ~11 warps/SM),
 // 8 x 4 (2 in flight, 8 KB, ~19 warps/SM, the default) and 4 x 4
 using V0 = PipeLdgsts<1, 8, 8>;
 using V1 = PipeLdgsts<1, 8, 4>;
 using V2 = PipeLdgsts<1, 4, 4>;
+using V3 = PipeLdgsts<1, 8, 16>;  // tail level (experiment): 14 stages of 8 in flight
 
 template <class F>
 auto with_variant(int v, F&& f) {  // 3 (mixed) sizes like 1
@@ -866,12 +1126,31 @@ size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
 
 namespace {
 
+template <class Q>
+void launch_tail_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t units,
+                       cudaStream_t stream) {
+  for (int c = 0; c < hs.n_tail_class; ++c) {  // one launch per row-buffer class, group-major
+    const int k0 = hs.tail_class_ptr[c], nt = hs.tail_class_ptr[c + 1] - k0;
+    nr_factor_kernel<Q><<<(unsigned)(units * nt), 32, Q::smem_bytes() + (size_t)hs.tail_class_maxl[c] * Q::kSlot,
+                          stream>>>(m, w, k0, units, nt, 1);
+  }
+}
+
 template <class P>
 void launch_factor_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t units,
                          int l, cudaStream_t stream) {
+  if (l == hs.tail_level) {
+    switch (hs.tail_variant) {
+      case 0: launch_tail_level<V0>(m, hs, w, units, stream); break;
+      case 1: launch_tail_level<V1>(m, hs, w, units, stream); break;
+      case 2: launch_tail_level<V2>(m, hs, w, units, stream); break;
+      default: launch_tail_level<V3>(m, hs, w, units, stream); break;
+    }
+    return;
+  }
   const int k0 = hs.level_task_ptr[l], nt = hs.level_task_ptr[l + 1] - k0;
   nr_factor_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes() + (size_t)hs.level_maxl[l] * P::kSlot, stream>>>(
-      m, w, k0, units);
+      m, w, k0, units, nt, 0);
 }
 
 // mixed: levels with several tasks per group take the 4x4 ring (more
@@ -887,6 +1166,8 @@ void launch_levels(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWor
     else
       launch_factor_level<P>(m, hs, w, units, l, stream);
   }
+  if (m.tail_T > 0)
+    nr_tail_kernel<<<(unsigned)(groups * kGroup), kTW * 32, kTailSmem, stream>>>(m, w);
   for (int l = 0; l < hs.n_blevels; ++l) {
     const int k0 = hs.blevel_task_ptr[l], nt = hs.blevel_task_ptr[l + 1] - k0;
     nr_back_kernel<P><<<(unsigned)(units * nt), 32, P::smem_bytes(), stream>>>(m, w, k0, units);
@@ -919,6 +1200,19 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
                                 (int)(P::smem_bytes() + (size_t)hs.max_l * P::kSlot));
   });
   if (e != cudaSuccess) return e;
+  if (m.tail_T > 0) {
+    e = cudaFuncSetAttribute(nr_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmem);
+    if (e != cudaSuccess) return e;
+    int cap = 0;
+    for (int c = 0; c < hs.n_tail_class; ++c) cap = cap > hs.tail_class_maxl[c] ? cap : hs.tail_class_maxl[c];
+    auto attr = [&](auto q) {
+      using Q = decltype(q);
+      return cudaFuncSetAttribute(nr_factor_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(Q::smem_bytes() + (size_t)cap * Q::kSlot));
+    };
+    e = hs.tail_variant == 0 ? attr(V0{}) : hs.tail_variant == 1 ? attr(V1{}) : hs.tail_variant == 2 ? attr(V2{}) : attr(V3{});
+    if (e != cudaSuccess) return e;
+  }
   const int64_t groups = (io.batch + kGroup - 1) / kGroup;
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int wpb = 4;
@@ -954,7 +1248,8 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     nr_step_advance_kernel<<<1, 1, 0, st>>>(w);
     return cudaGetLastError();
   };
-  const int n_head = 3, n_body = hs.n_levels + hs.n_blevels + 3, n_body0 = 2;
+  const int n_head = 3, n_body0 = 2;
+  const int n_body = hs.n_levels + hs.n_blevels + 3 + (m.tail_T > 0 ? hs.n_tail_class : 0);
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
                      graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {

@@ -268,7 +268,7 @@ std::vector<int32_t> level_sorted_perm(const NrSymbolic& s) {
 
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
                        const double* y_re, const double* y_im, NrSchedule& o, int task_elems,
-                       bool column_store) {
+                       bool column_store, int tail_max) {
   const int nr = s.n_j, nb = s.n_bus;
   if (s.n_q != 0) throw std::logic_error("block schedule expects a bus-level symbolic analysis");
   // ---- arena layout
@@ -352,13 +352,38 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     blev[p] = l;
   }
   o.n_levels = lev[nr - 1] + 1;
+  // ---- dense tail: the longest suffix of whole levels with at most
+  // min(tail_max, kTailMaxRows) rows; those rows become one level
+  {
+    std::vector<int> cnt(o.n_levels, 0);
+    for (int p = 0; p < nr; ++p) ++cnt[lev[p]];
+    const int cap = std::min(tail_max, kTailMaxRows);
+    int T = 0, l = o.n_levels - 1;
+    while (l >= 0 && T + cnt[l] <= cap) T += cnt[l--];
+    o.tail_T = T;
+    o.tail_row0 = nr - T;
+    o.tail_level = T > 0 ? l + 1 : -1;
+    for (int p = o.tail_row0; p < nr; ++p) lev[p] = l + 1;
+    if (T > 0) o.n_levels = l + 2;
+  }
+  const int n0 = o.tail_row0;
+  // back levels of the non-tail rows: the tail's x is known before they run
+  for (int p = nr - 1; p >= 0; --p) {
+    int l = 0;
+    if (p < n0)
+      for (int64_t t = s.diag[p] + 1; t < s.rowptr[p + 1]; ++t)
+        if (s.col[t] < n0) l = std::max(l, blev[s.col[t]] + 1);
+    blev[p] = l;
+  }
   o.n_blevels = 0;
-  for (int p = 0; p < nr; ++p) o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
+  for (int p = 0; p < n0; ++p) o.n_blevels = std::max(o.n_blevels, blev[p] + 1);
   o.level_ptr.assign(o.n_levels + 1, 0);
   o.level_maxl.assign(o.n_levels, 0);
   for (int p = 0; p < nr; ++p) {
     o.level_ptr[lev[p] + 1] = p + 1;
-    o.level_maxl[lev[p]] = std::max<int>(o.level_maxl[lev[p]], (int)(s.diag[p] - s.rowptr[p]));
+    int nl = 0;  // L blocks kept in the row buffer (tail rows: the non-tail columns only)
+    for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) nl += (p < n0 || s.col[t] < n0) ? 1 : 0;
+    o.level_maxl[lev[p]] = std::max<int>(o.level_maxl[lev[p]], nl);
   }
 
   // ---- factor stream: per block row b_p, then per slot: assembled block
@@ -371,39 +396,54 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
   o.slot_info.assign(s.nnz_lu, 0);
   o.row_slot.assign(nr + 1, 0);
   o.row_sptr.assign(nr + 1, 0);
+  o.tail_slot.clear();
   for (int p = 0; p < nr; ++p) {
     const int64_t r0 = s.rowptr[p], r1 = s.rowptr[p + 1];
     o.row_slot[p + 1] = (int32_t)r1;
     gw(o.off_yx + p, 0);
     for (int64_t t = r0; t < r1; ++t) {
+      // a tail row's slot in a tail column keeps only the updates from
+      // non-tail rows m (pairs are in ascending m) and is stored raw
+      const bool tail = p >= n0 && s.col[t] >= n0;
       uint32_t info = 0;
-      if (t == s.diag[p]) info |= kSlotDiag;
+      if (tail) {
+        info |= kSlotTail;
+        o.tail_slot.push_back(st[t]);
+        o.tail_slot.push_back((p - n0) * o.tail_T + (s.col[t] - n0));
+      } else {
+        if (t == s.diag[p]) info |= kSlotDiag;
+        if (t < s.diag[p]) info |= kSlotL;
+      }
       if (t == r1 - 1) info |= kSlotRowEnd;
-      if (t < s.diag[p]) info |= kSlotL;
       const bool fill = s.slot_type[t] == 8;
       if (fill) info |= kSlotFill;
-      const int64_t cnt = s.pair_ptr[t + 1] - s.pair_ptr[t];
+      int64_t q1 = s.pair_ptr[t + 1];
+      if (tail)
+        for (q1 = s.pair_ptr[t]; q1 < s.pair_ptr[t + 1] && s.col[s.pair_l[q1]] < n0; ++q1) {
+        }
+      const int64_t cnt = q1 - s.pair_ptr[t];
       if (cnt >= 65536) throw std::length_error("too many updates for one slot");
       info |= (uint32_t)cnt << 16;
       o.slot_info[t] = info;
       if (!fill) gw(o.off_lu + st[t], 0);
-      for (int64_t q = s.pair_ptr[t]; q < s.pair_ptr[t + 1]; ++q)
+      for (int64_t q = s.pair_ptr[t]; q < q1; ++q)
         gw(o.off_lu + st[s.pair_u[q]], (int)(s.pair_l[q] - r0));
-      if (t < s.diag[p]) gw(o.off_yx + s.col[t], 0);  // y_t (unit-upper form: no pivot inverse)
+      if (info & kSlotL) gw(o.off_yx + s.col[t], 0);  // y_t (unit-upper form: no pivot inverse)
     }
     o.row_sptr[p + 1] = (int32_t)o.stream.size();
   }
   // ---- back stream: rows by back level; per row y_p, then (U^_pc, x_c)
-  std::vector<int32_t> border(nr);
-  for (int p = 0; p < nr; ++p) border[p] = p;
+  // (tail rows are solved by the dense tail kernel and have no back rows)
+  std::vector<int32_t> border(n0);
+  for (int p = 0; p < n0; ++p) border[p] = p;
   std::stable_sort(border.begin(), border.end(), [&](int a, int b) {
     return blev[a] != blev[b] ? blev[a] < blev[b] : a > b;
   });
-  o.brow.resize(nr);
-  o.brow_sptr.assign(nr + 1, 0);
+  o.brow.resize(n0);
+  o.brow_sptr.assign(n0 + 1, 0);
   o.blevel_ptr.assign(o.n_blevels + 1, 0);
   o.brow_sptr[0] = (int32_t)o.stream.size();
-  for (int r = 0; r < nr; ++r) {
+  for (int r = 0; r < n0; ++r) {
     const int p = border[r];
     const int64_t cnt = s.rowptr[p + 1] - s.diag[p] - 1;
     if (p >= (1 << 20) || cnt >= 2048) throw std::length_error("back row too large");
@@ -441,6 +481,29 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     trow.push_back(lptr[nl]);
   };
   make_tasks(o.level_ptr, o.row_sptr, o.level_task_ptr, o.task_row);
+  o.tail_trow.clear();
+  o.tail_class_ptr.assign(1, 0);
+  o.tail_class_maxl.clear();
+  if (o.tail_T > 0) {
+    std::vector<int> nl(nr, 0);
+    for (int p = n0; p < nr; ++p)
+      for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) nl[p] += s.col[t] < n0 ? 1 : 0;
+    const int bounds[] = {16, 32, 48, 64, 1 << 30};
+    int lo = -1;
+    for (int hi : bounds) {
+      int mx = 0;
+      for (int p = n0; p < nr; ++p)
+        if (nl[p] > lo && nl[p] <= hi) {
+          o.tail_trow.push_back(p);
+          mx = std::max(mx, nl[p]);
+        }
+      if ((int)o.tail_trow.size() > o.tail_class_ptr.back()) {
+        o.tail_class_ptr.push_back((int)o.tail_trow.size());
+        o.tail_class_maxl.push_back(mx);
+      }
+      lo = hi;
+    }
+  }
   make_tasks(o.blevel_ptr, o.brow_sptr, o.blevel_task_ptr, o.btask_row);
 }
 

@@ -69,17 +69,35 @@ struct NrSchedule {
   // gather stream, word = block element index | lpos << 22
   std::vector<uint32_t> stream;
   int64_t n_stream = 0;
+  // Dense tail (nr_kernel.cu, nr_tail_kernel): the last tail_T block rows of
+  // the level-sorted order (a suffix of whole levels, 2 tail_T <= 128). Their
+  // Crout rows run as ONE factor level (tail_level) that only applies the
+  // updates from non-tail rows and stores the partial values raw; the
+  // on-chip dense LU of the tail (DMMA) finishes the factorisation, the
+  // forward and the back substitution of the tail rows.
+  int tail_row0 = 0;   // first tail row (= n_rows without a tail)
+  int tail_T = 0;
+  int tail_level = -1; // factor level of the tail rows, -1 without a tail
+  // [slots][2]: storage element of a tail-column slot of a tail row, its
+  // dense block position i * tail_T + j (i, j relative to tail_row0)
+  std::vector<int32_t> tail_slot;
+  // the tail level's tasks: one row each, grouped into classes by the length
+  // of the row buffer they need (non-tail L blocks), one launch per class so
+  // the short rows are not held to the occupancy of the longest one
+  std::vector<int32_t> tail_trow, tail_class_ptr, tail_class_maxl;
 };
 
 constexpr uint32_t kSlotDiag = 1u << 5;
 constexpr uint32_t kSlotRowEnd = 1u << 6;
 constexpr uint32_t kSlotL = 1u << 8;
 constexpr uint32_t kSlotFill = 1u << 9;
+constexpr uint32_t kSlotTail = 1u << 10;  // tail-column slot of a tail row: store the partial value raw
+constexpr int kTailMaxRows = 64;          // 2 x 64 scalar rows: one DMMA strip of 8 rows per warp
 
 // s: NrSymbolic built on the non-slack buses (n_theta = #non-slack, n_q = 0)
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
                        const double* y_re, const double* y_im, NrSchedule& out,
-                       int task_elems = 512, bool column_store = true);
+                       int task_elems = 512, bool column_store = true, int tail_max = 0);
 
 // LU of the flat-start Jacobian, shared by the first Newton step of every
 // scenario (see nr_symbolic.cpp); false on a zero pivot or non-finite value.

@@ -272,3 +272,24 @@ def _fresh_plan(model):
     st = flat_start(model.net, model.part)
     return engine.NrPlan(model.y.csr, model.part.theta_block, model.part.q_block, st.theta, st.vmag,
                          perm=jacobian_ordering(model))
+
+
+@pytest.mark.parametrize("tag", ["case14", "case118", "gb2224"])
+def test_nr_dense_tail_variant_matches_reference(tag, golden, monkeypatch):
+    """The dense-tail factorisation (ACPF_NR_TAIL, off by default: the top of
+    the elimination tree factored on chip with DMMA, nr_tail_kernel) gives the
+    reference's flags and iterations and states within 1e-8; on case14 the
+    tail is the whole matrix (no sparse level at all)."""
+    monkeypatch.setenv("ACPF_NR_TAIL", "64")
+    g = golden(f"nr_{tag}")
+    model = pf.build_transmission_model(load_transmission(TX[tag]))
+    out = model.plan().solve(np.ascontiguousarray(g["p_spec"]), np.ascontiguousarray(g["q_spec"]), 1e-8, 20)
+    np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
+    np.testing.assert_array_equal(out["iterations"], g["iterations"])
+    if "theta" in g:
+        assert np.abs(out["theta"] - g["theta"]).max() <= TOL_TH
+        assert np.abs(out["vmag"] - g["vmag"]).max() <= TOL_V
+    sc = pf.base_scenario(model.net, model.part)
+    h = model.plan().solve(np.ascontiguousarray(50 * sc.p_spec[None]), np.ascontiguousarray(50 * sc.q_spec[None]),
+                           1e-8, 20)
+    assert int(h["iterations"][0]) == int(g["huge_iterations"])
