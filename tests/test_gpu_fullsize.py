@@ -4,9 +4,10 @@ The bench batches (GBnetwork NR x 65,536, configs[2]; EULV Z-Bus x 262,144,
 configs[3]) are too large for the reference to solve here, so they are
 checked the way the domain allows at any size:
 
-* the leading rows are the reference's own scale-golden scenarios (seed
-  10010 / 10011, tools/make_golden_scale.py): flags and iteration counts equal
-  the reference's, states within the north-star tolerance;
+* the leading 4,096 / 16,384 rows are the reference's own scale-golden scenarios (seed
+  10010 / 10011, tools/make_golden_scale.py): flags equal the reference's,
+  iteration counts equal up to reported stop-rule ties (tests/tiebands.py),
+  states within the north-star tolerance;
 * those rows are bitwise the ones a small batch of the same scenarios gives
   (results independent of batch size and position);
 * every scenario carries its certificate: NR final ||F||inf <= 1e-8 recomputed
@@ -24,6 +25,8 @@ import pytest
 import paper_2605_14103_b200 as pf
 from paper_2605_14103_b200 import engine
 from paper_2605_14103_b200.fixtures import load_distribution, load_transmission
+
+from tiebands import check_iterations
 
 pytestmark = pytest.mark.gpu
 
@@ -70,10 +73,12 @@ def test_nr_gb2224_full_batch(golden):
     n = int(g["count"])
     assert int(g["seed"]) == 10010
     np.testing.assert_array_equal(out["converged"][:n].cpu().numpy().astype(bool), g["converged"])
-    np.testing.assert_array_equal(its[:n].cpu().numpy(), g["iterations"])
-    k = g["keep"]
-    assert np.abs(th[:n].cpu().numpy()[k] - g["theta"]).max() <= TOL
-    assert np.abs(vm[:n].cpu().numpy()[k] - g["vmag"]).max() <= TOL
+    ties = check_iterations("NR gb2224 x65536 (leading rows)", g["iterations"], its[:n].cpu().numpy(),
+                            g["step_fnorm"], 1e-8, first=0)
+    k = np.setdiff1d(g["keep"], ties)
+    sel = np.searchsorted(g["keep"], k)
+    assert np.abs(th[:n].cpu().numpy()[k] - g["theta"][sel]).max() <= TOL
+    assert np.abs(vm[:n].cpu().numpy()[k] - g["vmag"][sel]).max() <= TOL
     # ... and bitwise what a small batch of the same scenarios gives, also
     # for a slice from the end of the batch
     for a in (0, NR_BATCH - 96):
@@ -104,9 +109,11 @@ def test_zbus_eulv_full_batch(golden):
     n = int(g["count"])
     assert int(g["seed"]) == 10011
     np.testing.assert_array_equal(out["converged"][:n].cpu().numpy().astype(bool), g["converged"])
-    np.testing.assert_array_equal(its[:n].cpu().numpy(), g["iterations"])
+    ties = check_iterations("Z-Bus eulv x262144 (leading rows)", g["iterations"], its[:n].cpu().numpy(),
+                            g["sweep_delta"], 1e-9, first=1)
     v = out["v"]
-    assert np.abs(v[:n].cpu().numpy()[g["keep"]] - g["v"]).max() <= TOL
+    k = np.setdiff1d(g["keep"], ties)
+    assert np.abs(v[:n].cpu().numpy()[k] - g["v"][np.searchsorted(g["keep"], k)]).max() <= TOL
     for a in (0, ZB_BATCH - 128):
         small = plan.solve(sw[a:a + 128].contiguous(), sd[a:a + 128].contiguous(), 1e-9, 100)
         assert torch.equal(small["v"], v[a:a + 128])

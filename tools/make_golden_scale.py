@@ -2,14 +2,18 @@
 
     PYTHONDONTWRITEBYTECODE=1 python tools/make_golden_scale.py [--ref /root/reference/pkg/src]
 
-Solves 256 seeded GBnetwork scenarios (seed 10010, the acceptance seed) with
-the reference's `newton_solve` and 512 seeded EULV scenarios (seed 10011) with
+Solves 4,096 seeded GBnetwork scenarios (seed 10010, the acceptance seed) with
+the reference's `newton_solve` and 16,384 seeded EULV scenarios (seed 10011) with
 `zbus_iterate`, through the reference's public API, on a process pool. The
 scenario inputs are not stored (they are the reference generator's rows
 0..count-1, reproduced bitwise by the engine); stored are the per-scenario
 flags, iteration counts, GMRES totals, residuals, fixed-order state summaries
-and the full state of every 32nd scenario. tests/test_gpu_scale.py checks the
-CUDA path against them.
+the full state of every 64th scenario, and the decision margins of the stop
+rules: the NR mismatch norm at every Newton check (recorded by wrapping
+transmission.mismatch, result unchanged) and the Z-Bus |sum|v_k| - sum|v_k-1||
+of every sweep (wrapping ZBusModel.z_apply, tools/make_golden_failures.py).
+tests/test_gpu_scale.py / test_gpu_fullsize.py check the CUDA path against
+them and report stop-rule ties (tests/tiebands.py) separately.
 """
 
 from __future__ import annotations
@@ -26,7 +30,7 @@ ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "tests" / "golden"
 FIX = ROOT / "fixtures"
 REF = "/root/reference/pkg/src"
-NR_COUNT, ZB_COUNT, KEEP_EVERY = 256, 512, 32
+NR_COUNT, ZB_COUNT, KEEP_EVERY = 4096, 16384, 64
 
 _state = {}
 
@@ -41,8 +45,25 @@ def _text(name: str) -> str:
 
 def _init(ref: str):
     sys.path.insert(0, ref)
+    sys.path.insert(0, str(ROOT / "tools"))
     import acpflow as ac
+    from acpflow import distribution as dm
+    from acpflow import transmission as tm
+    from make_golden_failures import _DeltaRecorder
     _state["ac"] = ac
+    rec = _DeltaRecorder(dm)
+    rec.__enter__()
+    _state["rec"] = rec
+    orig = tm.mismatch
+    _state["fn"] = None
+
+    def mismatch(*a, **k):
+        f = orig(*a, **k)
+        if _state["fn"] is not None:
+            _state["fn"].append(float(np.abs(f).max()) if f.size else 0.0)
+        return f
+
+    tm.mismatch = mismatch
     net = ac.parse_matpower_case(_text("gb2224.m"))
     model = ac.build_transmission_model(net)
     base = ac.transmission_base(net, model.part)
@@ -60,16 +81,19 @@ def _init(ref: str):
 def _nr(i: int):
     ac = _state["ac"]
     model, base, mult = _state["nr"]
+    _state["fn"] = []
     r = ac.newton_solve(model, ac.apply_multipliers(base, mult[i]))
+    fn = _state["fn"]
+    _state["fn"] = None
     return (r.converged, r.iterations, r.total_gmres_iterations, r.final_mismatch_inf, r.state.theta,
-            r.state.vmag)
+            r.state.vmag, fn)
 
 
 def _zb(i: int):
     ac = _state["ac"]
     model, base, mult = _state["zb"]
-    r = ac.zbus_iterate(model, ac.apply_multipliers(base, mult[i]))
-    return r.converged, r.iterations, r.final_delta, r.residual_inf, r.v
+    r, d = _state["rec"].run(ac, model, ac.apply_multipliers(base, mult[i]))
+    return r.converged, r.iterations, r.final_delta, r.residual_inf, r.v, d
 
 
 def main() -> int:
@@ -78,8 +102,15 @@ def main() -> int:
     ap.add_argument("--workers", type=int, default=8)
     args = ap.parse_args()
     with ProcessPoolExecutor(args.workers, initializer=_init, initargs=(args.ref,)) as ex:
-        nr = list(ex.map(_nr, range(NR_COUNT), chunksize=4))
-        zb = list(ex.map(_zb, range(ZB_COUNT), chunksize=8))
+        nr = list(ex.map(_nr, range(NR_COUNT), chunksize=8))
+        zb = list(ex.map(_zb, range(ZB_COUNT), chunksize=32))
+
+    def pad(seqs):
+        m = max(len(x) for x in seqs)
+        a = np.full((len(seqs), m), np.nan)
+        for k, x in enumerate(seqs):
+            a[k, :len(x)] = x
+        return a
     keep = np.arange(0, NR_COUNT, KEEP_EVERY)
     th = np.array([r[4] for r in nr])
     vm = np.array([r[5] for r in nr])
@@ -88,14 +119,15 @@ def main() -> int:
         converged=np.array([r[0] for r in nr]), iterations=np.array([r[1] for r in nr]),
         gmres_total=np.array([r[2] for r in nr]), fnorm=np.array([r[3] for r in nr]),
         theta_sum=th.sum(1), vmag_sum=vm.sum(1), vmag_min=vm.min(1), vmag_max=vm.max(1),
-        keep=keep, theta=th[keep], vmag=vm[keep])
+        keep=keep, theta=th[keep], vmag=vm[keep], step_fnorm=pad([r[6] for r in nr]))
     keepz = np.arange(0, ZB_COUNT, KEEP_EVERY)
     v = np.array([r[4] for r in zb])
     np.savez_compressed(
         OUT / "scale_zb_eulv.npz", seed=10011, count=ZB_COUNT,
         converged=np.array([r[0] for r in zb]), iterations=np.array([r[1] for r in zb]),
         final_delta=np.array([r[2] for r in zb]), residual=np.array([r[3] for r in zb]),
-        vabs_sum=np.abs(v).sum(1), vabs_min=np.abs(v).min(1), keep=keepz, v=v[keepz])
+        vabs_sum=np.abs(v).sum(1), vabs_min=np.abs(v).min(1), keep=keepz, v=v[keepz],
+        sweep_delta=pad([r[5] for r in zb]))
     print("NR iterations", np.unique([r[1] for r in nr], return_counts=True))
     print("ZB iterations", np.unique([r[1] for r in zb], return_counts=True))
     return 0
