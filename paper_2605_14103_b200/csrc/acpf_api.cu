@@ -674,7 +674,21 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
                                   double* final_mismatch_inf, int32_t* status, cudaStream_t st) {
   const NrDeviceModel& d = p->dm;
   const int64_t groups = chunk / kGroup;
-  const int64_t n_chunks = (batch + chunk - 1) / chunk;
+  // chunk boundaries: a short first and last chunk (the first H2D and the
+  // last D2H are the only copies nothing overlaps), full chunks between; the
+  // two lanes take alternate chunks and end up with equal shares
+  std::vector<int64_t> cbeg;
+  {
+    const int64_t edge = ((std::min(chunk, batch / 8) + kGroup - 1) / kGroup) * kGroup;
+    if (batch > 2 * chunk || edge < 1024 || env_int("ACPF_NR_EDGE_CHUNKS", 1) == 0) {
+      for (int64_t s0 = 0; s0 < batch; s0 += chunk) cbeg.push_back(s0);
+    } else {  // [edge, (B - 2 edge) / 2, (B - 2 edge) / 2, edge]
+      const int64_t mid = ((batch - 2 * edge) / 2 + kGroup - 1) / kGroup * kGroup;
+      for (int64_t s0 : {(int64_t)0, edge, edge + mid, batch - edge}) cbeg.push_back(s0);
+    }
+    cbeg.push_back(batch);
+  }
+  const int64_t n_chunks = (int64_t)cbeg.size() - 1;
   const size_t set_b = (size_t)chunk * ((size_t)(d.n_theta + d.n_q) * 8 + (size_t)d.n_bus * 16 + 8 + 4 + 4 + 1) + 256;
   struct Set {
     double *ps, *qs, *th, *vm, *fn;
@@ -724,7 +738,7 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   }
   auto h2d = [&](int64_t c, cudaStream_t s) -> acpf_status {
     const Set& S = sets[c & 1];
-    const int64_t s0 = c * chunk, nb = std::min(chunk, batch - s0);
+    const int64_t s0 = cbeg[c], nb = cbeg[c + 1] - cbeg[c];
     if (d.n_theta)
       ACPF_CUDA(cudaMemcpyAsync(S.ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, s));
     if (d.n_q) ACPF_CUDA(cudaMemcpyAsync(S.qs, q_spec + s0 * d.n_q, nb * d.n_q * 8, cudaMemcpyHostToDevice, s));
@@ -751,7 +765,7 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
     auto body = [&]() -> acpf_status {
       for (int64_t c = k; c < n_chunks; c += 2) {
         const Set& S = sets[k];
-        const int64_t c0 = c * chunk, nb = std::min(chunk, batch - c0);
+        const int64_t c0 = cbeg[c], nb = cbeg[c + 1] - cbeg[c];
         if (c >= 2) {
           acpf_status r = h2d(c, s);
           if (r != ACPF_OK) return r;
