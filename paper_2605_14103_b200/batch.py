@@ -23,6 +23,8 @@ from typing import Any, Callable, Sequence
 
 import numpy as np
 
+from . import hostmem
+
 from .distribution import DistributionScenario, ZBusModel
 from .network import BusPartition, TransmissionNetwork
 
@@ -163,11 +165,18 @@ def make_scenario_arrays(base, spec: ScenarioSpec, start: int = 0,
         q[:, base.load_elements] *= m
         p = base.p_gen[None, :] - p
         q = base.q_gen[None, :] - q
-        return (np.ascontiguousarray(p[:, base.part.theta_block]),
-                np.ascontiguousarray(q[:, base.part.q_block]))
+        # page-locked result tables (hostmem): the solves copy them at PCIe rate
+        op = hostmem.empty((b, base.part.theta_block.size))
+        oq = hostmem.empty((b, base.part.q_block.size))
+        np.take(p, base.part.theta_block, axis=1, out=op)
+        np.take(q, base.part.q_block, axis=1, out=oq)
+        return op, oq
     kinds = np.array(base.load_kinds)
-    return (np.ascontiguousarray(base.wye_s[None, :] * m[:, kinds == "wye"]),
-            np.ascontiguousarray(base.delta_s[None, :] * m[:, kinds == "delta"]))
+    ow = hostmem.empty((m.shape[0], int((kinds == "wye").sum())), np.complex128)
+    od = hostmem.empty((m.shape[0], int((kinds == "delta").sum())), np.complex128)
+    np.multiply(base.wye_s[None, :], m[:, kinds == "wye"], out=ow)
+    np.multiply(base.delta_s[None, :], m[:, kinds == "delta"], out=od)
+    return ow, od
 
 
 # ---------------------------------------------------------------------------

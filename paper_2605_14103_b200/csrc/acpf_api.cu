@@ -491,7 +491,8 @@ static acpf_status nr_ensure_workspace(acpf_nr_plan* p, int64_t groups) {
   w.active = (uint8_t*)get(S);
   w.gactive = (int*)get((size_t)groups * 4);
   w.n_active = (int*)get(4);
-  w.kstep = (int*)get(4);
+  w.kstep = (int*)get(8);  // [0] Newton step, [1] kernels launched by the device loop
+  if (ok) ok = cudaMemset(w.kstep, 0, 8) == cudaSuccess;
   if (!ok) {
     p->work.release();
     cudaGetLastError();
@@ -527,6 +528,14 @@ static acpf_status ensure_stage(DevArena& arena, size_t& have, void*& base, size
 
 // Host-pointer solve pipelined over two staging sets: the H2D of chunk c+1
 // and the D2H of chunk c-1 run on a copy stream while chunk c solves.
+// kernels the device-side Newton loop launched since the last call (and reset)
+static int nr_take_device_launches(const NrWorkspace& w) {
+  int v[2] = {0, 0};
+  if (!w.kstep || cudaMemcpy(v, w.kstep, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  cudaMemset(w.kstep + 1, 0, sizeof(int));
+  return v[1];
+}
+
 static acpf_status nr_solve_host(acpf_nr_plan* p, int64_t batch, int64_t chunk, const double* p_spec,
                                  const double* q_spec, double tol, int32_t max_newton, double* theta_out,
                                  double* vmag_out, uint8_t* converged, int32_t* iterations,
@@ -618,7 +627,7 @@ static acpf_status nr_solve_host(acpf_nr_plan* p, int64_t batch, int64_t chunk, 
   ACPF_CUDA(cudaStreamSynchronize(cs));
   ACPF_CUDA(cudaStreamSynchronize(st));
   p->last_ms = total_ms;
-  p->last_launches = launches;
+  p->last_launches = launches + nr_take_device_launches(p->ws);
   return ACPF_OK;
 }
 
@@ -646,7 +655,8 @@ static acpf_status nr_lane_workspace(acpf_nr_plan* p, NrLane& L, int64_t groups)
   w.active = (uint8_t*)get(S);
   w.gactive = (int*)get((size_t)groups * 4);
   w.n_active = (int*)get(4);
-  w.kstep = (int*)get(4);
+  w.kstep = (int*)get(8);  // [0] Newton step, [1] kernels launched by the device loop
+  if (ok) ok = cudaMemset(w.kstep, 0, 8) == cudaSuccess;
   if (!ok) {
     L.work.release();
     cudaGetLastError();
@@ -816,7 +826,8 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->lanes[0].ev_end));
   if (n_chunks > 1) ACPF_CUDA(cudaEventElapsedTime(&ms1, p->ev0, p->lanes[1].ev_end));
   p->last_ms = std::max(ms, ms1);  // wall time of the whole host-pointer solve incl. copies (acpf.h)
-  p->last_launches = lnl[0] + lnl[1];
+  p->last_launches = lnl[0] + lnl[1] + nr_take_device_launches(ws[0]) +
+                     (n_lanes > 1 ? nr_take_device_launches(ws[1]) : 0);
   return ACPF_OK;
 }
 
@@ -949,7 +960,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   }
   ACPF_CUDA(cudaStreamSynchronize(st));
   p->last_ms = total_ms;
-  p->last_launches = launches;
+  p->last_launches = launches + nr_take_device_launches(p->ws);
   return ACPF_OK;
 }
 

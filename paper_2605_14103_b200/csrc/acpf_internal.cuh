@@ -83,7 +83,8 @@ struct NrWorkspace {
   int* gactive;     // [groups]
   int* n_active;    // device counter
   int* host_active; // pinned host mirror
-  int* kstep;       // device Newton step counter (kernels read it; graphs stay step-independent)
+  int* kstep;       // [0] device Newton step counter (kernels read it; graphs stay step-independent),
+                    // [1] kernels launched by the device-side loop (nr_count_kernel), summed per solve
 };
 
 // Captured per-step launch sequences (CUDA graphs), cached by the plan and
@@ -93,10 +94,12 @@ struct NrGraphCache {
   cudaGraphExec_t head = nullptr;  // phasor, mismatch, check, D2H of the active count
   cudaGraphExec_t body = nullptr;  // factor levels, back levels, zero-pivot, step++
   cudaGraphExec_t body0 = nullptr; // step 0 with the shared flat-start LU, step++
+  cudaGraphExec_t solve = nullptr; // the whole solve with the Newton loop on the device (conditional nodes)
   int64_t groups = -1, batch = -1;
   double tol = 0.0;
   int max_newton = -1;
   const double* arena = nullptr;
+  const void* io_key[4] = {nullptr, nullptr, nullptr, nullptr};  // io pointers baked into `solve`
   void release();
 };
 

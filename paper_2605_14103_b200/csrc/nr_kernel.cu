@@ -45,6 +45,8 @@
 
 #include "acpf_internal.cuh"
 
+#include <cstdlib>
+
 namespace acpf {
 
 namespace {
@@ -269,6 +271,7 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
 __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item == 0 && threadIdx.x == 0) *w.n_active = 0;  // nr_check_kernel counts into it after this launch
   const int nch = (m.n_bus + kBusChunk - 1) / kBusChunk;
   const int64_t g = item / nch;
   if (g >= w.groups || !w.gactive[g]) return;
@@ -788,6 +791,21 @@ __global__ void nr_zero_pivot_kernel(NrWorkspace w, int64_t batch) {
 
 __global__ void nr_step_advance_kernel(NrWorkspace w) { *w.kstep += 1; }
 
+// device-side Newton loop (conditional graph nodes): continue while any
+// scenario is active after the exit checks
+__global__ void nr_cond_kernel(const int* n_active, cudaGraphConditionalHandle a, cudaGraphConditionalHandle b) {
+  const unsigned go = *n_active > 0 ? 1u : 0u;
+  cudaGraphSetConditional(a, go);
+  cudaGraphSetConditional(b, go);
+}
+
+// kernels the device loop launched in this solve (heads = bodies + 1)
+__global__ void nr_count_kernel(NrWorkspace w, int n_head, int n_body, int n_body0, int shared0) {
+  const int k = *w.kstep;
+  const int bodies = shared0 && k > 0 ? n_body0 + (k - 1) * n_body : k * n_body;
+  w.kstep[1] += 1 + (k + 1) * n_head + bodies + 1 + 1;  // init, heads, bodies, output, this kernel
+}
+
 __global__ void nr_output_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1180,7 +1198,9 @@ void NrGraphCache::release() {
   if (head) cudaGraphExecDestroy(head);
   if (body) cudaGraphExecDestroy(body);
   if (body0) cudaGraphExecDestroy(body0);
-  head = body = body0 = nullptr;
+  if (solve) cudaGraphExecDestroy(solve);
+  head = body = body0 = solve = nullptr;
+  for (auto& k : io_key) k = nullptr;
   groups = batch = -1;
   arena = nullptr;
 }
@@ -1225,8 +1245,6 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   auto head = [&](cudaStream_t st) -> cudaError_t {
     nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
     nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
-    cudaError_t r = cudaMemsetAsync(w.n_active, 0, sizeof(int), st);
-    if (r != cudaSuccess) return r;
     nr_check_kernel<<<blocks(groups), 32 * wpb, 0, st>>>(w, io.batch, max_newton, tol);
     return cudaMemcpyAsync(w.host_active, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
   };
@@ -1250,9 +1268,129 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   };
   const int n_head = 3, n_body0 = 2;
   const int n_body = hs.n_levels + hs.n_blevels + 3 + (m.tail_T > 0 ? hs.n_tail_class : 0);
+  // ---- device-side Newton loop: the whole solve is one graph,
+  //   init -> head -> cond -> IF(active){ step-0 body } ->
+  //   WHILE(active){ head -> cond -> IF(active){ body } } -> output -> count
+  // so a solve makes no host round trip per Newton step (the exit test of
+  // _newton_loop, transmission.py:347-359, is evaluated by nr_cond_kernel).
+  static const bool devloop = [] {
+    const char* v = std::getenv("ACPF_NR_DEVLOOP");
+    return !(v && v[0] == '0');
+  }();
+  if (graphs && devloop) {
+    const void* key[4] = {io.p_spec, io.q_spec, io.theta_out, io.iterations};
+    bool hit = graphs->solve && graphs->groups == groups && graphs->batch == io.batch && graphs->tol == tol &&
+               graphs->max_newton == max_newton && graphs->arena == w.arena;
+    for (int i = 0; i < 4; ++i) hit = hit && graphs->io_key[i] == key[i];
+    if (!hit) {
+      graphs->release();
+      bool ok = graphs->capture || cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) == cudaSuccess;
+      cudaStream_t c1 = nullptr, c2 = nullptr;
+      ok = ok && cudaStreamCreateWithFlags(&c1, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaStreamCreateWithFlags(&c2, cudaStreamNonBlocking) == cudaSuccess;
+      cudaGraph_t g = nullptr;
+      const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+      auto head_dev = [&](cudaStream_t st) {
+        nr_phasor_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
+        nr_mismatch_kernel<<<blocks(groups * nch), 32 * wpb, 0, st>>>(m, w);
+        nr_check_kernel<<<blocks(groups), 32 * wpb, 0, st>>>(w, io.batch, max_newton, tol);
+      };
+      // append a conditional node at the capture position of `st`; returns its body graph
+      auto add_cond = [&](cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType t) {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaGraph_t bodyg = nullptr;
+        if (cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd) != cudaSuccess) return bodyg;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = t;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        if (cudaGraphAddNode(&node, cg, deps, nd, &cp) != cudaSuccess) return bodyg;
+        if (cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+          return bodyg;
+        return cp.conditional.phGraph_out[0];
+      };
+      auto graph_of = [&](cudaStream_t st) {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr);
+        return cg;
+      };
+      const bool shared0_ok = shared0;
+      cudaGraph_t tmp = nullptr;
+      if (ok) ok = cudaStreamBeginCapture(graphs->capture, mode) == cudaSuccess;
+      if (ok) {
+        cudaStream_t s0 = graphs->capture;
+        cudaGraph_t root = graph_of(s0);
+        cudaGraphConditionalHandle h_w, h_i0;
+        ok = cudaGraphConditionalHandleCreate(&h_w, root, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
+             cudaGraphConditionalHandleCreate(&h_i0, root, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+        nr_init_kernel<<<blocks(groups), 32 * wpb, 0, s0>>>(m, w, io);
+        head_dev(s0);
+        nr_cond_kernel<<<1, 1, 0, s0>>>(w.n_active, h_i0, h_w);
+        cudaGraph_t b0 = ok ? add_cond(s0, h_i0, cudaGraphCondTypeIf) : nullptr;
+        ok = ok && b0;
+        if (ok) {  // step 0 (shared flat-start LU, or a full factorisation)
+          ok = cudaStreamBeginCaptureToGraph(c1, b0, nullptr, nullptr, 0, mode) == cudaSuccess;
+          if (ok) {
+            if (shared0_ok) body0(c1); else body(c1);
+            ok = cudaStreamEndCapture(c1, &tmp) == cudaSuccess;
+          }
+        }
+        cudaGraph_t wb = ok ? add_cond(s0, h_w, cudaGraphCondTypeWhile) : nullptr;
+        ok = ok && wb;
+        if (ok) {  // while body: head, cond, IF(active){ body }
+          ok = cudaStreamBeginCaptureToGraph(c1, wb, nullptr, nullptr, 0, mode) == cudaSuccess;
+          if (ok) {
+            cudaGraphConditionalHandle h_i;
+            ok = cudaGraphConditionalHandleCreate(&h_i, wb, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+            head_dev(c1);
+            nr_cond_kernel<<<1, 1, 0, c1>>>(w.n_active, h_i, h_w);
+            cudaGraph_t ib = ok ? add_cond(c1, h_i, cudaGraphCondTypeIf) : nullptr;
+            ok = ok && ib;
+            if (ok) {
+              ok = cudaStreamBeginCaptureToGraph(c2, ib, nullptr, nullptr, 0, mode) == cudaSuccess;
+              if (ok) {
+                body(c2);
+                ok = cudaStreamEndCapture(c2, &tmp) == cudaSuccess;
+              }
+            }
+            ok = (cudaStreamEndCapture(c1, &tmp) == cudaSuccess) && ok;
+          }
+        }
+        nr_output_kernel<<<blocks(groups * nch), 32 * wpb, 0, s0>>>(m, w, io);
+        nr_count_kernel<<<1, 1, 0, s0>>>(w, n_head + 1, n_body, n_body0, shared0_ok ? 1 : 0);
+        ok = (cudaStreamEndCapture(s0, &g) == cudaSuccess) && ok && g;
+      }
+      ok = ok && cudaGraphInstantiate(&graphs->solve, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      if (c1) cudaStreamDestroy(c1);
+      if (c2) cudaStreamDestroy(c2);
+      if (ok) {
+        graphs->groups = groups;
+        graphs->batch = io.batch;
+        graphs->tol = tol;
+        graphs->max_newton = max_newton;
+        graphs->arena = w.arena;
+        for (int i = 0; i < 4; ++i) graphs->io_key[i] = key[i];
+      } else {
+        graphs->release();
+        cudaGetLastError();
+      }
+    }
+    if (graphs->solve) {
+      if (launches) *launches = 0;  // counted on the device (w.kstep[1])
+      return cudaGraphLaunch(graphs->solve, stream);
+    }
+  }
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
-                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
+                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head ||
+                     graphs->solve)) {
     graphs->release();
     if (!graphs->capture && cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) != cudaSuccess)
       use_graphs = false;

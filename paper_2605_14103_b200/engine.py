@@ -306,10 +306,11 @@ class NrPlan:
                 "final_mismatch_inf": torch.empty(b, dtype=torch.float64, **kw),
                 "status": torch.empty(b, dtype=torch.int32, **kw),
             }
+        from . import hostmem
         return {
-            "theta": np.empty((b, self.n_bus)), "vmag": np.empty((b, self.n_bus)),
-            "converged": np.empty(b, dtype=np.uint8), "iterations": np.empty(b, dtype=np.int32),
-            "final_mismatch_inf": np.empty(b), "status": np.empty(b, dtype=np.int32),
+            "theta": hostmem.empty((b, self.n_bus)), "vmag": hostmem.empty((b, self.n_bus)),
+            "converged": hostmem.empty(b, np.uint8), "iterations": hostmem.empty(b, np.int32),
+            "final_mismatch_inf": hostmem.empty(b), "status": hostmem.empty(b, np.int32),
         }
 
     def last_timing(self) -> tuple:
@@ -465,11 +466,12 @@ class ZbusPlan:
                 "status": torch.empty(b, dtype=torch.int32, **kw),
                 "floor_slot": torch.empty(b, dtype=torch.int32, **kw),
             }
+        from . import hostmem
         return {
-            "v": np.empty((b, self.n), dtype=np.complex128),
-            "converged": np.empty(b, dtype=np.uint8), "iterations": np.empty(b, dtype=np.int32),
-            "final_delta": np.empty(b), "residual_inf": np.empty(b),
-            "status": np.empty(b, dtype=np.int32), "floor_slot": np.empty(b, dtype=np.int32),
+            "v": hostmem.empty((b, self.n), np.complex128),
+            "converged": hostmem.empty(b, np.uint8), "iterations": hostmem.empty(b, np.int32),
+            "final_delta": hostmem.empty(b), "residual_inf": hostmem.empty(b),
+            "status": hostmem.empty(b, np.int32), "floor_slot": hostmem.empty(b, np.int32),
         }
 
     def solve(self, s_wye, s_delta, tol: float, max_iter: int, out: dict | None = None,
