@@ -213,7 +213,7 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
     build_nr_schedule(p->sym, y_rowptr, y_col, y_re, y_im, p->sch,
                       (int)env_int("ACPF_NR_TASK_ELEMS", 512),
                       env_int("ACPF_NR_COLUMN_STORE", 1) != 0,
-                      (int)env_int("ACPF_NR_TAIL", 0));  // dense tail: measured break-even, off
+                      (int)env_int("ACPF_NR_TAIL", kTailMaxRows));  // dense tail
     if (env_int("ACPF_DEBUG_SCHEDULE", 0)) {  // per-level shape of the factor schedule (stderr)
       const NrSchedule& sc = p->sch;
       for (int l = 0; l < sc.n_levels; ++l) {

@@ -94,12 +94,24 @@ struct NrGraphCache {
   cudaGraphExec_t head = nullptr;  // phasor, mismatch, check, D2H of the active count
   cudaGraphExec_t body = nullptr;  // factor levels, back levels, zero-pivot, step++
   cudaGraphExec_t body0 = nullptr; // step 0 with the shared flat-start LU, step++
-  cudaGraphExec_t solve = nullptr; // the whole solve with the Newton loop on the device (conditional nodes)
   int64_t groups = -1, batch = -1;
   double tol = 0.0;
   int max_newton = -1;
   const double* arena = nullptr;
-  const void* io_key[4] = {nullptr, nullptr, nullptr, nullptr};  // io pointers baked into `solve`
+  // whole solves with the Newton loop on the device (conditional nodes),
+  // one per (chunk size, tolerances, workspace, io pointers) seen recently
+  struct Solve {
+    cudaGraphExec_t exec = nullptr;
+    int64_t batch = -1;
+    double tol = 0.0;
+    int max_newton = -1;
+    const double* arena = nullptr;
+    const void* io[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t used = 0;
+  };
+  static constexpr int kSolves = 4;
+  Solve solves[kSolves];
+  uint64_t tick = 0;
   void release();
 };
 

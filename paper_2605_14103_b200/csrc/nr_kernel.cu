@@ -1198,9 +1198,11 @@ void NrGraphCache::release() {
   if (head) cudaGraphExecDestroy(head);
   if (body) cudaGraphExecDestroy(body);
   if (body0) cudaGraphExecDestroy(body0);
-  if (solve) cudaGraphExecDestroy(solve);
-  head = body = body0 = solve = nullptr;
-  for (auto& k : io_key) k = nullptr;
+  head = body = body0 = nullptr;
+  for (auto& e : solves) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    e = Solve{};
+  }
   groups = batch = -1;
   arena = nullptr;
 }
@@ -1279,11 +1281,18 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   }();
   if (graphs && devloop) {
     const void* key[4] = {io.p_spec, io.q_spec, io.theta_out, io.iterations};
-    bool hit = graphs->solve && graphs->groups == groups && graphs->batch == io.batch && graphs->tol == tol &&
-               graphs->max_newton == max_newton && graphs->arena == w.arena;
-    for (int i = 0; i < 4; ++i) hit = hit && graphs->io_key[i] == key[i];
-    if (!hit) {
-      graphs->release();
+    NrGraphCache::Solve* slot = nullptr;
+    for (auto& e : graphs->solves) {
+      bool hit = e.exec && e.batch == io.batch && e.tol == tol && e.max_newton == max_newton && e.arena == w.arena;
+      for (int i = 0; i < 4; ++i) hit = hit && e.io[i] == key[i];
+      if (hit) slot = &e;
+    }
+    if (!slot) {
+      slot = &graphs->solves[0];  // the least recently used entry is rebuilt
+      for (auto& e : graphs->solves)
+        if (e.used < slot->used) slot = &e;
+      if (slot->exec) cudaGraphExecDestroy(slot->exec);
+      *slot = NrGraphCache::Solve{};
       bool ok = graphs->capture || cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) == cudaSuccess;
       cudaStream_t c1 = nullptr, c2 = nullptr;
       ok = ok && cudaStreamCreateWithFlags(&c1, cudaStreamNonBlocking) == cudaSuccess &&
@@ -1366,31 +1375,31 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
         nr_count_kernel<<<1, 1, 0, s0>>>(w, n_head + 1, n_body, n_body0, shared0_ok ? 1 : 0);
         ok = (cudaStreamEndCapture(s0, &g) == cudaSuccess) && ok && g;
       }
-      ok = ok && cudaGraphInstantiate(&graphs->solve, g, 0) == cudaSuccess;
+      ok = ok && cudaGraphInstantiate(&slot->exec, g, 0) == cudaSuccess;
       if (g) cudaGraphDestroy(g);
       if (c1) cudaStreamDestroy(c1);
       if (c2) cudaStreamDestroy(c2);
       if (ok) {
-        graphs->groups = groups;
-        graphs->batch = io.batch;
-        graphs->tol = tol;
-        graphs->max_newton = max_newton;
-        graphs->arena = w.arena;
-        for (int i = 0; i < 4; ++i) graphs->io_key[i] = key[i];
+        slot->batch = io.batch;
+        slot->tol = tol;
+        slot->max_newton = max_newton;
+        slot->arena = w.arena;
+        for (int i = 0; i < 4; ++i) slot->io[i] = key[i];
       } else {
-        graphs->release();
+        if (slot->exec) cudaGraphExecDestroy(slot->exec);
+        *slot = NrGraphCache::Solve{};
         cudaGetLastError();
       }
     }
-    if (graphs->solve) {
+    if (slot->exec) {
+      slot->used = ++graphs->tick;
       if (launches) *launches = 0;  // counted on the device (w.kstep[1])
-      return cudaGraphLaunch(graphs->solve, stream);
+      return cudaGraphLaunch(slot->exec, stream);
     }
   }
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
-                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head ||
-                     graphs->solve)) {
+                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
     graphs->release();
     if (!graphs->capture && cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) != cudaSuccess)
       use_graphs = false;

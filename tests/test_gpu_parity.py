@@ -275,12 +275,12 @@ def _fresh_plan(model):
 
 
 @pytest.mark.parametrize("tag", ["case14", "case118", "gb2224"])
-def test_nr_dense_tail_variant_matches_reference(tag, golden, monkeypatch):
-    """The dense-tail factorisation (ACPF_NR_TAIL, off by default: the top of
-    the elimination tree factored on chip with DMMA, nr_tail_kernel) gives the
-    reference's flags and iterations and states within 1e-8; on case14 the
-    tail is the whole matrix (no sparse level at all)."""
-    monkeypatch.setenv("ACPF_NR_TAIL", "64")
+def test_nr_without_dense_tail_matches_reference(tag, golden, monkeypatch):
+    """The all-sparse factorisation (ACPF_NR_TAIL=0: no dense tail, every
+    level through nr_factor_kernel) gives the reference's flags and
+    iterations and states within 1e-8, like the default dense-tail path (on
+    case14 the default tail is the whole matrix)."""
+    monkeypatch.setenv("ACPF_NR_TAIL", "0")
     g = golden(f"nr_{tag}")
     model = pf.build_transmission_model(load_transmission(TX[tag]))
     out = model.plan().solve(np.ascontiguousarray(g["p_spec"]), np.ascontiguousarray(g["q_spec"]), 1e-8, 20)
