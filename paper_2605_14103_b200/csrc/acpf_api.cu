@@ -101,6 +101,11 @@ struct NrLane {
   NrGraphCache graphs;
   cudaStream_t st = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_end = nullptr;
+  // prefetch pipeline: inputs in / results out on their own copy streams,
+  // two staging sets (the next chunk's H2D and the last chunk's D2H overlap
+  // the current chunk's solve)
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
 };
 
 struct acpf_nr_plan {
@@ -704,16 +709,25 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
     double *ps, *qs, *th, *vm, *fn;
     int32_t *it, *stt;
     uint8_t* cv;
-  } sets[2];
+  } sets[2][2];  // [lane][staging set]
   NrWorkspace ws[2];
   NrGraphCache* graphs[2] = {nullptr, nullptr};
   const int n_lanes = n_chunks > 1 ? 2 : 1;  // one chunk: no second workspace
   for (int k = 0; k < n_lanes; ++k) {
     NrLane& L = p->lanes[k];
     if (!L.st) ACPF_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    if (!L.cs_in) ACPF_CUDA(cudaStreamCreateWithFlags(&L.cs_in, cudaStreamNonBlocking));
+    if (!L.cs_out) ACPF_CUDA(cudaStreamCreateWithFlags(&L.cs_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      if (!L.ev_in[i]) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_in[i], cudaEventDisableTiming));
+      if (!L.ev_done[i]) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_done[i], cudaEventDisableTiming));
+      if (!L.ev_out[i]) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_out[i], cudaEventDisableTiming));
+    }
     if (!L.ev_h2d) ACPF_CUDA(cudaEventCreateWithFlags(&L.ev_h2d, cudaEventDisableTiming));
     if (!L.ev_end) ACPF_CUDA(cudaEventCreate(&L.ev_end));
-    acpf_status rc = ensure_stage(L.stage, L.stage_bytes, L.stage_base, set_b);
+    // two staging sets when the lane solves more than one chunk
+    const int nset = n_chunks > 2 ? 2 : 1;
+    acpf_status rc = ensure_stage(L.stage, L.stage_bytes, L.stage_base, nset * set_b);
     if (rc != ACPF_OK) return rc;
     if (k == 0) {  // lane 0: the plan's workspace (sized for the chunk by the caller) and graphs
       ws[0] = p->ws;
@@ -731,55 +745,84 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
       ws[1].host_active = L.host_active;
       graphs[1] = nr_graphs(p) ? &L.graphs : nullptr;
     }
-    char* b = (char*)L.stage_base;
-    auto take = [&](size_t bytes) {
-      char* r = b;
-      b += (bytes + 15) & ~(size_t)15;
-      return r;
-    };
-    sets[k].ps = (double*)take((size_t)chunk * d.n_theta * 8);
-    sets[k].qs = (double*)take((size_t)chunk * d.n_q * 8);
-    sets[k].th = (double*)take((size_t)chunk * d.n_bus * 8);
-    sets[k].vm = (double*)take((size_t)chunk * d.n_bus * 8);
-    sets[k].fn = (double*)take((size_t)chunk * 8);
-    sets[k].it = (int32_t*)take((size_t)chunk * 4);
-    sets[k].stt = (int32_t*)take((size_t)chunk * 4);
-    sets[k].cv = (uint8_t*)take((size_t)chunk);
+    for (int i = 0; i < 2; ++i) {
+      char* b = (char*)L.stage_base + (size_t)(i % nset) * set_b;
+      auto take = [&](size_t bytes) {
+        char* r = b;
+        b += (bytes + 15) & ~(size_t)15;
+        return r;
+      };
+      Set& S = sets[k][i];
+      S.ps = (double*)take((size_t)chunk * d.n_theta * 8);
+      S.qs = (double*)take((size_t)chunk * d.n_q * 8);
+      S.th = (double*)take((size_t)chunk * d.n_bus * 8);
+      S.vm = (double*)take((size_t)chunk * d.n_bus * 8);
+      S.fn = (double*)take((size_t)chunk * 8);
+      S.it = (int32_t*)take((size_t)chunk * 4);
+      S.stt = (int32_t*)take((size_t)chunk * 4);
+      S.cv = (uint8_t*)take((size_t)chunk);
+    }
   }
+  // chunk c runs on lane c & 1 as that lane's (c >> 1)-th chunk, staging set (c >> 1) & 1
+  auto set_of = [&](int64_t c) -> Set& { return sets[c & 1][(c >> 1) & 1]; };
   auto h2d = [&](int64_t c, cudaStream_t s) -> acpf_status {
-    const Set& S = sets[c & 1];
+    const Set& S = set_of(c);
     const int64_t s0 = cbeg[c], nb = cbeg[c + 1] - cbeg[c];
     if (d.n_theta)
       ACPF_CUDA(cudaMemcpyAsync(S.ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, s));
     if (d.n_q) ACPF_CUDA(cudaMemcpyAsync(S.qs, q_spec + s0 * d.n_q, nb * d.n_q * 8, cudaMemcpyHostToDevice, s));
     return ACPF_OK;
   };
-  // order after the caller's stream, then lane 0's first H2D before lane 1's
+  auto d2h = [&](int64_t c, cudaStream_t s) -> acpf_status {
+    const Set& S = set_of(c);
+    const int64_t c0 = cbeg[c], nb = cbeg[c + 1] - cbeg[c];
+    ACPF_CUDA(cudaMemcpyAsync(theta_out + c0 * d.n_bus, S.th, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
+    ACPF_CUDA(cudaMemcpyAsync(vmag_out + c0 * d.n_bus, S.vm, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
+    if (final_mismatch_inf) ACPF_CUDA(cudaMemcpyAsync(final_mismatch_inf + c0, S.fn, nb * 8, cudaMemcpyDeviceToHost, s));
+    if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + c0, S.it, nb * 4, cudaMemcpyDeviceToHost, s));
+    if (status) ACPF_CUDA(cudaMemcpyAsync(status + c0, S.stt, nb * 4, cudaMemcpyDeviceToHost, s));
+    if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + c0, S.cv, nb, cudaMemcpyDeviceToHost, s));
+    return ACPF_OK;
+  };
+  // order after the caller's stream; lane 0's first H2D goes before lane 1's
   ACPF_CUDA(cudaEventRecord(p->ev0, st));
-  cudaStream_t s0 = p->lanes[0].st, s1 = p->lanes[1].st;
-  ACPF_CUDA(cudaStreamWaitEvent(s0, p->ev0, 0));
-  if (n_lanes > 1) ACPF_CUDA(cudaStreamWaitEvent(s1, p->ev0, 0));  // lane 1 exists only for >1 chunk
-  acpf_status rc = h2d(0, s0);
-  if (rc != ACPF_OK) return rc;
-  if (n_chunks > 1) {
-    ACPF_CUDA(cudaEventRecord(p->lanes[0].ev_h2d, s0));
-    ACPF_CUDA(cudaStreamWaitEvent(s1, p->lanes[0].ev_h2d, 0));
-    if ((rc = h2d(1, s1)) != ACPF_OK) return rc;
+  for (int k = 0; k < n_lanes; ++k) {
+    NrLane& L = p->lanes[k];
+    ACPF_CUDA(cudaStreamWaitEvent(L.st, p->ev0, 0));
+    ACPF_CUDA(cudaStreamWaitEvent(L.cs_in, p->ev0, 0));
+    ACPF_CUDA(cudaStreamWaitEvent(L.cs_out, p->ev0, 0));
+  }
+  {
+    acpf_status rc = h2d(0, p->lanes[0].cs_in);
+    if (rc != ACPF_OK) return rc;
+    ACPF_CUDA(cudaEventRecord(p->lanes[0].ev_in[0], p->lanes[0].cs_in));
+    if (n_lanes > 1) {
+      ACPF_CUDA(cudaStreamWaitEvent(p->lanes[1].cs_in, p->lanes[0].ev_in[0], 0));
+      if ((rc = h2d(1, p->lanes[1].cs_in)) != ACPF_OK) return rc;
+      ACPF_CUDA(cudaEventRecord(p->lanes[1].ev_in[0], p->lanes[1].cs_in));
+    }
   }
   acpf_status lrc[2] = {ACPF_OK, ACPF_OK};
   std::string lerr[2];
   int lnl[2] = {0, 0};
+  // ACPF_NR_TRACE=1: per-chunk event timeline of the lanes on stderr
+  static const bool trace = env_int("ACPF_NR_TRACE", 0) != 0;
+  std::vector<cudaEvent_t> tev(trace ? 4 * n_chunks : 0);
+  for (auto& e : tev) ACPF_CUDA(cudaEventCreate(&e));
+  auto mark = [&](int64_t c, int what, cudaStream_t s) {
+    if (trace) cudaEventRecord(tev[4 * c + what], s);
+  };
   auto run = [&](int k) {
     cudaSetDevice(p->device);
-    cudaStream_t s = p->lanes[k].st;
+    NrLane& L = p->lanes[k];
     auto body = [&]() -> acpf_status {
       for (int64_t c = k; c < n_chunks; c += 2) {
-        const Set& S = sets[k];
-        const int64_t c0 = cbeg[c], nb = cbeg[c + 1] - cbeg[c];
-        if (c >= 2) {
-          acpf_status r = h2d(c, s);
-          if (r != ACPF_OK) return r;
-        }
+        const int j = (int)((c >> 1) & 1);
+        const Set& S = set_of(c);
+        const int64_t nb = cbeg[c + 1] - cbeg[c];
+        // the solve waits for its inputs only
+        ACPF_CUDA(cudaStreamWaitEvent(L.st, L.ev_in[j], 0));
+        mark(c, 1, L.st);
         NrBatchIO io{};
         io.batch = nb;
         io.p_spec = S.ps;
@@ -793,18 +836,31 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
         NrWorkspace wsb = ws[k];
         wsb.groups = (nb + kGroup - 1) / kGroup;
         int nl = 0;
-        ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, s, &nl, graphs[k]));
+        ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol, max_newton, L.st, &nl, graphs[k]));
         lnl[k] += nl;
-        ACPF_CUDA(cudaMemcpyAsync(theta_out + c0 * d.n_bus, S.th, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
-        ACPF_CUDA(cudaMemcpyAsync(vmag_out + c0 * d.n_bus, S.vm, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, s));
-        if (final_mismatch_inf)
-          ACPF_CUDA(cudaMemcpyAsync(final_mismatch_inf + c0, S.fn, nb * 8, cudaMemcpyDeviceToHost, s));
-        if (iterations) ACPF_CUDA(cudaMemcpyAsync(iterations + c0, S.it, nb * 4, cudaMemcpyDeviceToHost, s));
-        if (status) ACPF_CUDA(cudaMemcpyAsync(status + c0, S.stt, nb * 4, cudaMemcpyDeviceToHost, s));
-        if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + c0, S.cv, nb, cudaMemcpyDeviceToHost, s));
+        mark(c, 2, L.st);
+        ACPF_CUDA(cudaEventRecord(L.ev_done[j], L.st));
+        // prefetch the lane's next chunk into the other staging set once
+        // that set's previous results have been copied out
+        if (c + 2 < n_chunks) {
+          const int jn = j ^ 1;
+          if (c >= 2) ACPF_CUDA(cudaStreamWaitEvent(L.cs_in, L.ev_out[jn], 0));
+          mark(c + 2, 0, L.cs_in);
+          acpf_status r = h2d(c + 2, L.cs_in);
+          if (r != ACPF_OK) return r;
+          ACPF_CUDA(cudaEventRecord(L.ev_in[jn], L.cs_in));
+        }
+        // results out on the output copy stream
+        ACPF_CUDA(cudaStreamWaitEvent(L.cs_out, L.ev_done[j], 0));
+        acpf_status r = d2h(c, L.cs_out);
+        if (r != ACPF_OK) return r;
+        ACPF_CUDA(cudaEventRecord(L.ev_out[j], L.cs_out));
+        mark(c, 3, L.cs_out);
       }
-      ACPF_CUDA(cudaEventRecord(p->lanes[k].ev_end, s));
-      ACPF_CUDA(cudaStreamSynchronize(s));
+      ACPF_CUDA(cudaStreamWaitEvent(L.st, L.ev_out[0], 0));
+      ACPF_CUDA(cudaStreamWaitEvent(L.st, L.ev_out[1], 0));
+      ACPF_CUDA(cudaEventRecord(L.ev_end, L.st));
+      ACPF_CUDA(cudaStreamSynchronize(L.st));
       return ACPF_OK;
     };
     lrc[k] = body();
@@ -822,6 +878,15 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
       set_error(lerr[k]);
       return lrc[k];
     }
+  if (trace) {
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      float t[4] = {-1, -1, -1, -1};
+      for (int i = c >= 2 ? 0 : 1; i < 4; ++i) cudaEventElapsedTime(&t[i], p->ev0, tev[4 * c + i]);
+      std::fprintf(stderr, "lane %d chunk %lld (%lld scenarios): h2d@%.1f solve %.1f-%.1f d2h-end %.1f ms\n",
+                   (int)(c & 1), (long long)c, (long long)(cbeg[c + 1] - cbeg[c]), t[0], t[1], t[2], t[3]);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   float ms = 0.0f, ms1 = 0.0f;
   ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->lanes[0].ev_end));
   if (n_chunks > 1) ACPF_CUDA(cudaEventElapsedTime(&ms1, p->ev0, p->lanes[1].ev_end));
@@ -994,6 +1059,13 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
       L.graphs.release();
       if (L.graphs.capture) cudaStreamDestroy(L.graphs.capture);
       if (L.st) cudaStreamDestroy(L.st);
+      if (L.cs_in) cudaStreamDestroy(L.cs_in);
+      if (L.cs_out) cudaStreamDestroy(L.cs_out);
+      for (int i = 0; i < 2; ++i) {
+        if (L.ev_in[i]) cudaEventDestroy(L.ev_in[i]);
+        if (L.ev_done[i]) cudaEventDestroy(L.ev_done[i]);
+        if (L.ev_out[i]) cudaEventDestroy(L.ev_out[i]);
+      }
       if (L.ev_h2d) cudaEventDestroy(L.ev_h2d);
       if (L.ev_end) cudaEventDestroy(L.ev_end);
       if (L.host_active) cudaFreeHost(L.host_active);
