@@ -154,7 +154,13 @@ acpf_status acpf_nr_plan_structure(acpf_nr_plan_t plan, int32_t* perm_out, int64
  * ACPF_HOST_PTRS: the batch is copied in chunks solved on two concurrent
  * lanes (streams); the call drives the second lane from an internal host
  * thread that is joined before it returns (ACPF_NR_PIPELINE=1: one stream
- * plus a copy stream, 0: serial chunks).                                    */
+ * plus a copy stream, 0: serial chunks); results are complete on return.
+ * ACPF_DEVICE_PTRS: the solve is enqueued on cuda_stream and the call returns
+ * without waiting (stream-ordered, like a CUDA library call): synchronise the
+ * stream (or call acpf_nr_last_timing) before reading the results on the
+ * host; consecutive device-pointer solves of one plan must use one stream.
+ * The Newton loop runs on the device (one CUDA graph with conditional nodes
+ * per solve; ACPF_NR_DEVLOOP=0 steps it from the host).                      */
 acpf_status acpf_nr_solve(acpf_nr_plan_t plan, int64_t batch, const double* p_spec,
                           const double* q_spec, double tol_mismatch, int32_t max_newton,
                           double* theta_out, double* vmag_out, uint8_t* converged,
@@ -198,7 +204,9 @@ acpf_status acpf_zbus_plan_create(int32_t device, int32_t n, int32_t n_l, const 
  *   floor_slot: for ACPF_ZB_FLOOR, which check failed first, in the
  *   reference's order: k (wye k), n_wye+k (delta k, phase p),
  *   n_wye+n_delta+k (delta k, phase q), n_wye+2*n_delta+k (delta k, p-q);
- *   -1 otherwise. Any output pointer except v_out may be NULL.          */
+ *   -1 otherwise. Any output pointer except v_out may be NULL.
+ * ACPF_DEVICE_PTRS: enqueued on cuda_stream, returns without waiting (as
+ * acpf_nr_solve); ACPF_HOST_PTRS: results complete on return.            */
 acpf_status acpf_zbus_solve(acpf_zbus_plan_t plan, int64_t batch, const double* s_wye,
                             const double* s_delta, double tol, int32_t max_iter, double* v_out,
                             uint8_t* converged, int32_t* iterations, double* final_delta,

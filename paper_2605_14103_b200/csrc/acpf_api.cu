@@ -137,6 +137,10 @@ struct acpf_nr_plan {
   double last_ms = 0.0;
   int last_launches = 0;
   NrLane lanes[2];                      // concurrent chunk solvers (host-pointer path)
+  // device-pointer solves return without a host sync: their per-chunk events
+  // and host-counted launches are resolved by acpf_nr_last_timing
+  std::vector<cudaEvent_t> tev;
+  int pending_chunks = 0, pending_launches = 0;
 };
 
 struct acpf_zbus_plan {
@@ -155,6 +159,7 @@ struct acpf_zbus_plan {
   size_t stage_bytes = 0;
   void* stage_base = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool pending = false;  // last solve was a device-pointer (asynchronous) one
   double last_ms = 0.0;
   int last_launches = 0;
 };
@@ -958,10 +963,22 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   }
   float total_ms = 0.0f;
   int launches = 0;
-  for (int64_t s0 = 0; s0 < batch; s0 += chunk) {
+  int64_t ci = 0;  // chunk index
+  if (dev_ptrs) {
+    // asynchronous w.r.t. the host (like any stream-ordered CUDA library
+    // call): the device launch counter restarts for this solve
+    ACPF_CUDA(cudaMemsetAsync(p->ws.kstep + 1, 0, sizeof(int), st));
+    p->pending_chunks = 0;
+  }
+  for (int64_t s0 = 0; s0 < batch; s0 += chunk, ++ci) {
     const int64_t nb = std::min(chunk, batch - s0);
     NrBatchIO io{};
     io.batch = nb;
+    while (p->tev.size() < (size_t)(2 * ci + 2)) {
+      cudaEvent_t e;
+      ACPF_CUDA(cudaEventCreate(&e));
+      p->tev.push_back(e);
+    }
     if (dev_ptrs) {
       io.p_spec = p_spec ? p_spec + s0 * d.n_theta : nullptr;
       io.q_spec = q_spec ? q_spec + s0 * d.n_q : nullptr;
@@ -1001,13 +1018,14 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
       io.status = stt;
       io.converged = cv;
     }
-    ACPF_CUDA(cudaEventRecord(p->ev0, st));
+    ACPF_CUDA(cudaEventRecord(p->tev[2 * ci], st));
     int nl = 0;
     NrWorkspace wsb = p->ws;  // capacity may exceed this chunk: index by the chunk's groups
     wsb.groups = (nb + kGroup - 1) / kGroup;
     ACPF_CUDA(launch_nr_newton(d, p->hs, wsb, io, tol_mismatch, max_newton, st, &nl, nr_graphs(p)));
-    ACPF_CUDA(cudaEventRecord(p->ev1, st));
+    ACPF_CUDA(cudaEventRecord(p->tev[2 * ci + 1], st));
     launches += nl;
+    if (dev_ptrs) continue;
     if (!dev_ptrs) {
       ACPF_CUDA(cudaMemcpyAsync(theta_out + s0 * d.n_bus, io.theta_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
       ACPF_CUDA(cudaMemcpyAsync(vmag_out + s0 * d.n_bus, io.vmag_out, nb * d.n_bus * 8, cudaMemcpyDeviceToHost, st));
@@ -1018,10 +1036,15 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
       if (status) ACPF_CUDA(cudaMemcpyAsync(status + s0, io.status, nb * 4, cudaMemcpyDeviceToHost, st));
       if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, io.converged, nb, cudaMemcpyDeviceToHost, st));
     }
-    ACPF_CUDA(cudaEventSynchronize(p->ev1));
+    ACPF_CUDA(cudaEventSynchronize(p->tev[2 * ci + 1]));
     float ms = 0.0f;
-    ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    ACPF_CUDA(cudaEventElapsedTime(&ms, p->tev[2 * ci], p->tev[2 * ci + 1]));
     total_ms += ms;
+  }
+  if (dev_ptrs) {  // resolved lazily by acpf_nr_last_timing
+    p->pending_chunks = (int)ci;
+    p->pending_launches = launches;
+    return ACPF_OK;
   }
   ACPF_CUDA(cudaStreamSynchronize(st));
   p->last_ms = total_ms;
@@ -1034,6 +1057,19 @@ acpf_status acpf_nr_last_timing(acpf_nr_plan_t p, double* kernel_ms, int32_t* la
     set_error("acpf_nr_last_timing: null plan");
     return ACPF_EINVAL;
   }
+  if (p->pending_chunks > 0) {  // the last solve was a device-pointer (asynchronous) one
+    DeviceGuard dg(p->device);
+    float total = 0.0f;
+    for (int c = 0; c < p->pending_chunks; ++c) {
+      float ms = 0.0f;
+      ACPF_CUDA(cudaEventSynchronize(p->tev[2 * c + 1]));
+      ACPF_CUDA(cudaEventElapsedTime(&ms, p->tev[2 * c], p->tev[2 * c + 1]));
+      total += ms;
+    }
+    p->last_ms = total;
+    p->last_launches = p->pending_launches + nr_take_device_launches(p->ws);
+    p->pending_chunks = 0;
+  }
   if (kernel_ms) *kernel_ms = p->last_ms;
   if (launches) *launches = p->last_launches;
   return ACPF_OK;
@@ -1045,6 +1081,7 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
     DeviceGuard dg(p->device);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    for (cudaEvent_t e : p->tev) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
       if (p->ev_h2d[k]) cudaEventDestroy(p->ev_h2d[k]);
       if (p->ev_kend[k]) cudaEventDestroy(p->ev_kend[k]);
@@ -1362,6 +1399,11 @@ acpf_status acpf_zbus_solve(acpf_zbus_plan_t p, int64_t batch, const double* s_w
     ACPF_CUDA(launch_zbus(d, io, tol, max_iter, false, nullptr, &nl, st));
     ACPF_CUDA(cudaEventRecord(p->ev1, st));
     launches += nl;
+    if (dev_ptrs) {  // one launch, asynchronous: resolved by acpf_zbus_last_timing
+      p->pending = true;
+      p->last_launches = launches;
+      return ACPF_OK;
+    }
     if (!dev_ptrs) {
       ACPF_CUDA(cudaMemcpyAsync(v_out + 2 * s0 * d.n, io.v_out, nb * d.n * 16, cudaMemcpyDeviceToHost, st));
       if (converged) ACPF_CUDA(cudaMemcpyAsync(converged + s0, io.converged, nb, cudaMemcpyDeviceToHost, st));
@@ -1386,6 +1428,14 @@ acpf_status acpf_zbus_last_timing(acpf_zbus_plan_t p, double* kernel_ms, int32_t
   if (!p) {
     set_error("acpf_zbus_last_timing: null plan");
     return ACPF_EINVAL;
+  }
+  if (p->pending) {
+    DeviceGuard dg(p->device);
+    float ms = 0.0f;
+    ACPF_CUDA(cudaEventSynchronize(p->ev1));
+    ACPF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->last_ms = ms;
+    p->pending = false;
   }
   if (kernel_ms) *kernel_ms = p->last_ms;
   if (launches) *launches = p->last_launches;

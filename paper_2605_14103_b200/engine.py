@@ -152,8 +152,13 @@ def _is_device(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
 
-def _stream_ptr(stream) -> int | None:
+def _stream_ptr(stream, like=None) -> int | None:
+    """cudaStream_t for a call; device tensors default to torch's current
+    stream (device-pointer solves are stream-ordered and asynchronous)."""
     if stream is None:
+        if like is not None and _is_device(like):
+            import torch
+            return int(torch.cuda.current_stream(like.device).cuda_stream) or None
         return None
     return int(getattr(stream, "cuda_stream", stream))
 
@@ -291,7 +296,7 @@ class NrPlan:
             self._h, b, _ptr(p_spec), _ptr(q_spec), float(tol), int(max_newton),
             _ptr(out["theta"]), _ptr(out["vmag"]), _ptr(out["converged"]),
             _ptr(out["iterations"]), _ptr(out["final_mismatch_inf"]), _ptr(out["status"]),
-            flags, _stream_ptr(stream)))
+            flags, _stream_ptr(stream, p_spec)))
         return out
 
     def alloc_outputs(self, b: int, like=None) -> dict:
@@ -486,7 +491,7 @@ class ZbusPlan:
             _ptr(s_delta) if self.n_delta else None, float(tol), int(max_iter), _ptr(out["v"]),
             _ptr(out["converged"]), _ptr(out["iterations"]), _ptr(out["final_delta"]),
             _ptr(out["residual_inf"]), _ptr(out["status"]), _ptr(out["floor_slot"]), flags,
-            _stream_ptr(stream)))
+            _stream_ptr(stream, s_wye)))
         return out
 
     def last_timing(self) -> tuple:

@@ -17,7 +17,7 @@ plan = m.plan()
 pt, qt = plan.scenarios(base, 10010, 0, B, 0.2, device=0)
 out = plan.alloc_outputs(B, like=pt)
 st = torch.cuda.current_stream()
-for k in range(8):
+for k in range(int(sys.argv[2]) if len(sys.argv) > 2 else 8):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     h0 = time.perf_counter()
