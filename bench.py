@@ -325,7 +325,29 @@ def nr_api(args, model, hp, hq, dev):
                            "solver-allocated page-locked result tables out"}
 
 
-def zb_workload(args, dev, stream, local, case, seed, start, count, e2e=True, roof=True):
+def zb_api(args, model, hsw, hsd, dev):
+    """distribution.batch_zbus_solve on the array-backed scenario list
+    make_scenarios returns, results as FixedPointResult records over
+    page-locked tables (results.ZbusResults)."""
+    import paper_2605_14103_b200 as pf
+    from paper_2605_14103_b200 import shard
+    from paper_2605_14103_b200.results import DistributionScenarios
+
+    scen = DistributionScenarios(hsw, hsd)
+    box = {}
+
+    def step():
+        box["r"] = pf.batch_zbus_solve(model, scen)
+
+    t = time_host(step, args.steps, 2, dev)
+    t = shard.max_over_ranks(t, dev)
+    conv = shard.sum_over_ranks(int(box["r"].converged().sum()), dev)
+    return {"value": conv * args.steps / t, "unit": "converged flows/s",
+            "call": "batch_zbus_solve(model, make_scenarios-style DistributionScenarios) -> ZbusResults",
+            "host_memory": "page-locked scenario tables in, solver-allocated page-locked result tables out"}
+
+
+def zb_workload(args, dev, stream, local, case, seed, start, count, e2e=True, roof=True, api=False):
     import torch
     from paper_2605_14103_b200 import engine, peaks, roofline, shard
 
@@ -379,6 +401,8 @@ def zb_workload(args, dev, stream, local, case, seed, start, count, e2e=True, ro
             r["e2e"] = {"value": ce * args.steps / tze, "unit": "converged flows/s",
                         "h2d_bytes_per_step": int(hsw.nbytes + hsd.nbytes) * shard.dist_env()[2],
                         "d2h_bytes_per_step": int(sum(v.nbytes for v in hz.values())) * shard.dist_env()[2]}
+            if api:
+                r["api"] = zb_api(args, zmodel, hsw, hsd, dev)
             del hsw, hsd, hz
         else:
             r["e2e"] = None
@@ -405,7 +429,7 @@ def run_ours(args, rank, local, world):
         nr_rows = (rank * args.nr_batch, args.nr_batch)
         zb_rows = (rank * args.zb_batch, args.zb_batch)
     res = {"nr": nr_workload(args, dev, stream, local, NR_CASE, NR_SEED, *nr_rows, api=not args.global_batch),
-           "zb": zb_workload(args, dev, stream, local, ZB_CASE, ZB_SEED, *zb_rows)}
+           "zb": zb_workload(args, dev, stream, local, ZB_CASE, ZB_SEED, *zb_rows, api=not args.global_batch)}
     if not args.global_batch and not args.no_extra_configs:
         # BASELINE configs[0] (IEEE 14-bus NR x 1024) and configs[1] (IEEE13 Z-Bus x 4096)
         c1 = nr_workload(args, dev, stream, local, "case14", 1010, rank * 1024, 1024, roof=False)
@@ -616,7 +640,7 @@ def main():
                              "(BASELINE configs[3])"),
                 "value": zb["value"], "unit": "converged flows/s",
                 "ms_per_step": zb["t"] / args.steps * 1e3, "roofline": zb["roofline"],
-                "e2e": zb["e2e"], "gpu_launches": zb["launches"], "clocks": zb["clocks"],
+                "e2e": zb["e2e"], "api": zb.get("api"), "gpu_launches": zb["launches"], "clocks": zb["clocks"],
                 "iterations": zb["iterations"], "cpu_baseline": cpu[1] if cpu else None},
         }
         if nr.get("api"):

@@ -25,7 +25,7 @@ from paper_2605_14103_b200.transmission import results_from_arrays
 
 pytestmark = pytest.mark.gpu
 
-TX = {"case14": "case14", "case118": "case118", "gb2224": "gb2224"}
+TX = {"case14": "case14", "case118": "case118", "case1354": "case1354pegase", "gb2224": "gb2224"}
 
 
 def _split(g, prefix):
@@ -64,7 +64,11 @@ def test_nr_failure_branches(tag, golden):
             # fnorm of the last check; at a converged exit both are below tol
             if r.converged:
                 assert r.final_mismatch_inf <= float(d["tol"][s]), lab
-            elif "collapsed" not in str(d["diagnostic"][s]):
+            elif lab.startswith(("max_newton", "tol")):
+                # (a stalled heavy-load trajectory, e.g. case1354 x2 running to
+                # max_newton without collapsing, compares flags, iterations and
+                # diagnostics only: after 20 non-contracting steps the iterates
+                # of the exact and the inexact step are no longer comparable)
                 # an unconverged iterate: the reference's GMRES step is inexact
                 # (relative tolerance 1e-8, sparse.py:219-338), the engine's LU
                 # step exact, so ||F|| of iterate k differs at ~1e-6 relative
@@ -106,7 +110,8 @@ def _zb_sets(g):
 
 
 @pytest.mark.parametrize("key", ["wye_sweep1", "wye_sweep5", "delta_phase", "delta_phase_mid", "delta_line",
-                                 "mixed_floor", "max_iter5", "tol1e-6", "eulv_max_iter5"])
+                                 "mixed_floor", "max_iter5", "tol1e-6", "eulv_max_iter5", "ieee123_floor",
+                                 "ieee123_max_iter3"])
 def test_zbus_failure_branches(key, golden):
     g = golden("fail_zb")
     assert key in _zb_sets(g)

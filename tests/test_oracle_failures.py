@@ -14,7 +14,7 @@ from oracle import zbus as ozb
 from paper_2605_14103_b200.engine import zbus_floor_message
 from paper_2605_14103_b200.fixtures import load_transmission
 
-TX = {"case14": "case14", "case118": "case118", "gb2224": "gb2224"}
+TX = {"case14": "case14", "case118": "case118", "case1354": "case1354pegase", "gb2224": "gb2224"}
 
 
 def _split(g, prefix):
@@ -27,7 +27,7 @@ def test_oracle_nr_failures(tag, golden):
     m = pf.build_transmission_model(load_transmission(TX[tag]))
     st = pf.flat_start(m.net, m.part)
     case = onr.NrCase(m.y.csr, m.part.theta_block, m.part.q_block, st.theta, st.vmag)
-    rows = range(d["tol"].size) if tag != "gb2224" else range(0, d["tol"].size, 3)
+    rows = range(d["tol"].size) if tag not in ("gb2224", "case1354") else range(0, d["tol"].size, 3)
     for s in rows:
         lab = str(d["label"][s])
         with np.errstate(all="ignore"):
@@ -44,7 +44,7 @@ def test_oracle_nr_failures(tag, golden):
 
 
 @pytest.mark.parametrize("key", ["wye_sweep1", "wye_sweep5", "delta_phase", "delta_phase_mid", "delta_line",
-                                 "mixed_floor", "max_iter5", "tol1e-6"])
+                                 "mixed_floor", "max_iter5", "tol1e-6", "ieee123_floor", "ieee123_max_iter3"])
 def test_oracle_zbus_failures(key, golden):
     d = _split(golden("fail_zb"), key)
     model = pf.build_zbus_model(pf.parse_distribution_json(str(d["network"])), voltage_floor=float(d["floor"]))

@@ -20,8 +20,8 @@ Z-Bus `_zbus_loop` (distribution.py:653-687), tests/golden/fail_zb.npz
   * VoltageFloorError on a wye phase at sweep 1 (v = v0) and at sweep 5
     (v = previous iterate), on a delta phase, and on a delta line-to-line
     voltage (label "p-q"), distribution.py:583-606, :662-672
-  * a mixed batch: seeded scenarios under a floor that stops some of them at
-    different sweeps while the rest converge
+  * mixed batches: seeded scenarios under a floor that stops some of them at
+    different sweeps while the rest converge (IEEE13, IEEE123)
   * `max_iter` exits (max_iter = 5), and a looser tolerance (1e-6)
   * the per-sweep sum-of-magnitudes deltas of every scenario (recorded by
     wrapping ZBusModel.z_apply without changing its result) for the stop-rule
@@ -54,7 +54,7 @@ def _text(name: str) -> str:
 def _nr_cases(ac):
     out = {}
     for tag, fname, seed, count in [("case14", "case14.m", 1010, 8), ("case118", "case118.m", 1010, 16),
-                                    ("gb2224", "gb2224.m", 10010, 4)]:
+                                    ("case1354", "case1354pegase.m", 1010, 4), ("gb2224", "gb2224.m", 10010, 4)]:
         net = ac.parse_matpower_case(_text(fname))
         model = ac.build_transmission_model(net)
         part = model.part
@@ -67,7 +67,10 @@ def _nr_cases(ac):
         for mx in (1, 2):
             rows += [(s.p_spec, s.q_spec, 1e-8, mx, f"max_newton={mx}") for s in seeded]
         rows += [(s.p_spec, s.q_spec, 1e-4, 20, "tol=1e-4") for s in seeded]
-        if tag != "gb2224":
+        if tag == "case1354":
+            for sc in (2, 4, 8, 30):
+                rows.append((sc * b.p_spec, sc * b.q_spec, 1e-8, 20, f"base x{sc}"))
+        elif tag != "gb2224":
             for val, lab in ((np.nan, "nan"), (np.inf, "+inf"), (-np.inf, "-inf")):
                 p = b.p_spec.copy()
                 p[len(p) // 2] = val
@@ -187,6 +190,17 @@ def _zb_cases(ac, dm):
         solve_set("mixed_floor", ieee13, 0.905, seeded, 1e-9, 100, ["seeded, floor 0.905"] * 256)
         solve_set("max_iter5", ieee13, 1e-6, seeded[:64], 1e-9, 5, ["max_iter=5"] * 64)
         solve_set("tol1e-6", ieee13, 1e-6, seeded[:64], 1e-6, 100, ["tol=1e-6"] * 64)
+        # IEEE123: a floor that stops part of a seeded batch, and max_iter
+        i123 = _text("ieee123.json")
+        m123 = ac.build_zbus_model(ac.parse_distribution_json(i123))
+        b123 = ac.distribution_base(m123)
+        mu = ac.generate_load_multipliers(
+            ac.ScenarioSpec(count=64, seed=5050, spread=0.2, target="distribution"), b123.n_elements)
+        s123 = [ac.apply_multipliers(b123, mu[i]) for i in range(64)]
+        base_sol = ac.zbus_iterate(m123)
+        fl = float(np.quantile(np.abs(base_sol.v), 0.02))  # below a few load voltages of some scenarios
+        solve_set("ieee123_floor", i123, fl, s123, 1e-9, 100, ["seeded, floor at the 2% |v| quantile"] * 64)
+        solve_set("ieee123_max_iter3", i123, 1e-6, s123[:16], 1e-9, 3, ["max_iter=3"] * 16)
         eu = ac.build_zbus_model(ac.parse_distribution_json(nets["eulv"]))
         eb = ac.distribution_base(eu)
         em = ac.generate_load_multipliers(
