@@ -167,6 +167,19 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t plan, int64_t batch, const double* p_sp
                           int32_t* iterations, double* final_mismatch_inf, int32_t* status,
                           uint32_t flags, void* cuda_stream);
 
+/* acpf_nr_solve from a given start state instead of the plan's flat start
+ * (reference newton_solve(..., start=PolarState), transmission.py:306-330):
+ * theta_start, vmag_start [batch][n_bus] (host or device per flags, like the
+ * other batch buffers). The first Newton step is then factored per scenario
+ * (the shared flat-start LU does not apply); slack and PV entries keep the
+ * start's values, as in the reference's PolarState.with_packed (:70-78). */
+acpf_status acpf_nr_solve_start(acpf_nr_plan_t plan, int64_t batch, const double* p_spec,
+                                const double* q_spec, const double* theta_start,
+                                const double* vmag_start, double tol_mismatch, int32_t max_newton,
+                                double* theta_out, double* vmag_out, uint8_t* converged,
+                                int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                                uint32_t flags, void* cuda_stream);
+
 /* Time (ms) of the last acpf_nr_solve, measured with CUDA events, and the
  * number of kernel launches it made. Device pointers (and the host-pointer
  * serial / copy-stream pipelines, ACPF_NR_PIPELINE=0/1): the device time of

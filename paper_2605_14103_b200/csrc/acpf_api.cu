@@ -901,16 +901,45 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   return ACPF_OK;
 }
 
+static acpf_status nr_solve_impl(acpf_nr_plan_t p, int64_t batch, const double* p_spec, const double* q_spec,
+                                 const double* theta_start, const double* vmag_start, double tol_mismatch,
+                                 int32_t max_newton, double* theta_out, double* vmag_out, uint8_t* converged,
+                                 int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                                 uint32_t flags, void* cuda_stream);
+
 acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
                           const double* q_spec, double tol_mismatch, int32_t max_newton,
                           double* theta_out, double* vmag_out, uint8_t* converged,
                           int32_t* iterations, double* final_mismatch_inf, int32_t* status,
                           uint32_t flags, void* cuda_stream) {
+  return nr_solve_impl(p, batch, p_spec, q_spec, nullptr, nullptr, tol_mismatch, max_newton, theta_out, vmag_out,
+                       converged, iterations, final_mismatch_inf, status, flags, cuda_stream);
+}
+
+acpf_status acpf_nr_solve_start(acpf_nr_plan_t p, int64_t batch, const double* p_spec, const double* q_spec,
+                                const double* theta_start, const double* vmag_start, double tol_mismatch,
+                                int32_t max_newton, double* theta_out, double* vmag_out, uint8_t* converged,
+                                int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                                uint32_t flags, void* cuda_stream) {
+  if (!theta_start || !vmag_start) {
+    set_error("acpf_nr_solve_start: theta_start and vmag_start are required");
+    return ACPF_EINVAL;
+  }
+  return nr_solve_impl(p, batch, p_spec, q_spec, theta_start, vmag_start, tol_mismatch, max_newton, theta_out,
+                       vmag_out, converged, iterations, final_mismatch_inf, status, flags, cuda_stream);
+}
+
+static acpf_status nr_solve_impl(acpf_nr_plan_t p, int64_t batch, const double* p_spec, const double* q_spec,
+                                 const double* theta_start, const double* vmag_start, double tol_mismatch,
+                                 int32_t max_newton, double* theta_out, double* vmag_out, uint8_t* converged,
+                                 int32_t* iterations, double* final_mismatch_inf, int32_t* status,
+                                 uint32_t flags, void* cuda_stream) {
   if (!p || batch < 0 || !theta_out || !vmag_out || max_newton < 1 || !(tol_mismatch > 0) ||
       (p->dm.n_theta && !p_spec) || (p->dm.n_q && !q_spec) || flags > 1u) {
     set_error("acpf_nr_solve: invalid argument");
     return ACPF_EINVAL;
   }
+  const bool warm = theta_start != nullptr;
   if (batch == 0) return ACPF_OK;
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -943,7 +972,7 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
   acpf_status rc = nr_ensure_workspace(p, groups);
   if (rc != ACPF_OK) return rc;
 
-  if (!dev_ptrs && pipeline == 2) {
+  if (!dev_ptrs && pipeline == 2 && !warm) {
     rc = nr_solve_lanes(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
                         converged, iterations, final_mismatch_inf, status, st);
     if (rc != kLaneFallback) return rc;
@@ -951,14 +980,14 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
                          converged, iterations, final_mismatch_inf, status, st);
   }
-  if (!dev_ptrs && pipeline == 1)
+  if (!dev_ptrs && pipeline == 1 && !warm)
     return nr_solve_host(p, batch, chunk, p_spec, q_spec, tol_mismatch, max_newton, theta_out, vmag_out,
                          converged, iterations, final_mismatch_inf, status, st);
   // per-scenario byte sizes
-  const size_t in_b = (size_t)(d.n_theta + d.n_q) * 8;
+  const size_t in_b = (size_t)(d.n_theta + d.n_q) * 8 + (warm ? (size_t)d.n_bus * 16 : 0);
   const size_t out_b = (size_t)d.n_bus * 16 + 1 + 4 + 8 + 4;
   if (!dev_ptrs) {
-    rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, (size_t)chunk * (in_b + out_b) + 256);
+    rc = ensure_stage(p->stage, p->stage_bytes, p->stage_base, (size_t)chunk * (in_b + out_b) + 512);
     if (rc != ACPF_OK) return rc;
   }
   float total_ms = 0.0f;
@@ -982,6 +1011,10 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
     if (dev_ptrs) {
       io.p_spec = p_spec ? p_spec + s0 * d.n_theta : nullptr;
       io.q_spec = q_spec ? q_spec + s0 * d.n_q : nullptr;
+      if (warm) {
+        io.theta_start = theta_start + s0 * d.n_bus;
+        io.vmag_start = vmag_start + s0 * d.n_bus;
+      }
       io.theta_out = theta_out + s0 * d.n_bus;
       io.vmag_out = vmag_out + s0 * d.n_bus;
       io.converged = converged ? converged + s0 : nullptr;
@@ -1005,6 +1038,17 @@ acpf_status acpf_nr_solve(acpf_nr_plan_t p, int64_t batch, const double* p_spec,
       int32_t* stt = (int32_t*)b;
       b += (size_t)chunk * 4;
       uint8_t* cv = (uint8_t*)b;
+      b += (size_t)chunk;
+      if (warm) {  // start state staged after the outputs (16-byte aligned)
+        b = (char*)(((uintptr_t)b + 15) & ~(uintptr_t)15);
+        double* ths = (double*)b;
+        b += (size_t)chunk * d.n_bus * 8;
+        double* vms = (double*)b;
+        ACPF_CUDA(cudaMemcpyAsync(ths, theta_start + s0 * d.n_bus, nb * d.n_bus * 8, cudaMemcpyHostToDevice, st));
+        ACPF_CUDA(cudaMemcpyAsync(vms, vmag_start + s0 * d.n_bus, nb * d.n_bus * 8, cudaMemcpyHostToDevice, st));
+        io.theta_start = ths;
+        io.vmag_start = vms;
+      }
       if (d.n_theta)
         ACPF_CUDA(cudaMemcpyAsync(ps, p_spec + s0 * d.n_theta, nb * d.n_theta * 8, cudaMemcpyHostToDevice, st));
       if (d.n_q)

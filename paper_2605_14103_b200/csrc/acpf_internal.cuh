@@ -98,6 +98,7 @@ struct NrGraphCache {
   double tol = 0.0;
   int max_newton = -1;
   const double* arena = nullptr;
+  bool warm = false;  // head/body captured for a warm start (no shared step 0)
   // whole solves with the Newton loop on the device (conditional nodes),
   // one per (chunk size, tolerances, workspace, io pointers) seen recently
   struct Solve {
@@ -106,7 +107,7 @@ struct NrGraphCache {
     double tol = 0.0;
     int max_newton = -1;
     const double* arena = nullptr;
-    const void* io[4] = {nullptr, nullptr, nullptr, nullptr};
+    const void* io[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     uint64_t used = 0;
   };
   static constexpr int kSolves = 4;
@@ -125,6 +126,10 @@ struct NrBatchIO {
   double* fnorm;
   int32_t* status;
   int64_t batch;  // scenarios in this chunk
+  // warm start (acpf_nr_solve_start): [batch][n_bus] start state, or null for
+  // the plan's flat start (transmission.py:306-330 `start=`)
+  const double* theta_start = nullptr;
+  const double* vmag_start = nullptr;
 };
 
 // dynamic smem of a factor launch (pipeline variant, longest L part of its rows)

@@ -243,9 +243,10 @@ __global__ void nr_init_kernel(NrDeviceModel m, NrWorkspace w, NrBatchIO io) {
   const int64_t s = g * kGroup + sc;
   const bool valid = s < io.batch;
   const GroupBase gb = group_base(m, w, g, sc);
+  const bool warm = io.theta_start != nullptr && valid;
   for (int i = r; i < m.n_bus; i += 4) {
-    SL(gb.s, m.off_th + i) = m.theta_init[i];
-    SL(gb.s, m.off_vm + i) = m.vmag_init[i];
+    SL(gb.s, m.off_th + i) = warm ? io.theta_start[s * m.n_bus + i] : m.theta_init[i];
+    SL(gb.s, m.off_vm + i) = warm ? io.vmag_start[s * m.n_bus + i] : m.vmag_init[i];
     const int p = m.bus_row[i];
     if (p >= 0) {
       const int tp = m.tpos[i], qi = m.qidx[i];
@@ -1207,9 +1208,16 @@ void NrGraphCache::release() {
   arena = nullptr;
 }
 
-cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w,
+cudaError_t launch_nr_newton(const NrDeviceModel& m_in, const NrHostSchedule& hs, const NrWorkspace& w,
                              const NrBatchIO& io, double tol, int max_newton, cudaStream_t stream,
                              int* launches, NrGraphCache* graphs) {
+  // a warm start leaves the flat start: step 0 factors per scenario and the
+  // step-0 mismatch gathers phasors like every other step
+  NrDeviceModel m = m_in;
+  if (io.theta_start) {
+    m.sh_vals = nullptr;
+    m.sh_s0 = nullptr;
+  }
   const int v = hs.variant;
   if (v == 3) {  // mixed: the 4x4 factor kernel is launched too
     cudaError_t e2 = cudaFuncSetAttribute(nr_factor_kernel<V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1280,11 +1288,11 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
     return !(v && v[0] == '0');
   }();
   if (graphs && devloop) {
-    const void* key[4] = {io.p_spec, io.q_spec, io.theta_out, io.iterations};
+    const void* key[5] = {io.p_spec, io.q_spec, io.theta_out, io.iterations, io.theta_start};
     NrGraphCache::Solve* slot = nullptr;
     for (auto& e : graphs->solves) {
       bool hit = e.exec && e.batch == io.batch && e.tol == tol && e.max_newton == max_newton && e.arena == w.arena;
-      for (int i = 0; i < 4; ++i) hit = hit && e.io[i] == key[i];
+      for (int i = 0; i < 5; ++i) hit = hit && e.io[i] == key[i];
       if (hit) slot = &e;
     }
     if (!slot) {
@@ -1384,7 +1392,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
         slot->tol = tol;
         slot->max_newton = max_newton;
         slot->arena = w.arena;
-        for (int i = 0; i < 4; ++i) slot->io[i] = key[i];
+        for (int i = 0; i < 5; ++i) slot->io[i] = key[i];
       } else {
         if (slot->exec) cudaGraphExecDestroy(slot->exec);
         *slot = NrGraphCache::Solve{};
@@ -1399,7 +1407,8 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
   }
   bool use_graphs = graphs != nullptr;
   if (use_graphs && (graphs->groups != groups || graphs->batch != io.batch || graphs->tol != tol ||
-                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head)) {
+                     graphs->max_newton != max_newton || graphs->arena != w.arena || !graphs->head ||
+                     graphs->warm != (io.theta_start != nullptr))) {
     graphs->release();
     if (!graphs->capture && cudaStreamCreateWithFlags(&graphs->capture, cudaStreamNonBlocking) != cudaSuccess)
       use_graphs = false;
@@ -1420,6 +1429,7 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m, const NrHostSchedule& hs, c
       graphs->tol = tol;
       graphs->max_newton = max_newton;
       graphs->arena = w.arena;
+      graphs->warm = io.theta_start != nullptr;
     } else {
       graphs->release();
       cudaGetLastError();

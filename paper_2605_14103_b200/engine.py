@@ -30,7 +30,7 @@ EXPORTED = (
     "acpf_last_error", "acpf_abi_version", "acpf_device_count",
     "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
     "acpf_nr_plan_structure",
-    "acpf_nr_solve", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
+    "acpf_nr_solve", "acpf_nr_solve_start", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
     "acpf_zbus_plan_destroy", "acpf_philox_multipliers", "acpf_nr_scenarios",
     "acpf_zbus_scenarios", "acpf_nr_plan_set_branches", "acpf_nr_certify",
@@ -93,6 +93,7 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_nr_plan_info_get": (I32, [P, P]),
         "acpf_nr_plan_structure": (I32, [P, P, P]),
         "acpf_nr_solve": (I32, [P, I64, P, P, D, I32, P, P, P, P, P, P, U32, P]),
+        "acpf_nr_solve_start": (I32, [P, I64, P, P, P, P, D, I32, P, P, P, P, P, P, U32, P]),
         "acpf_nr_last_timing": (I32, [P, P, P]),
         "acpf_nr_plan_destroy": (I32, [P]),
         "acpf_zbus_plan_create": (I32, [I32, I32, I32, P, P, P, I32, P, I32, P, P, D, P]),
@@ -284,19 +285,25 @@ class NrPlan:
         return perm, rp
 
     def solve(self, p_spec, q_spec, tol: float, max_newton: int, out: dict | None = None,
-              stream=None) -> dict:
+              stream=None, theta_start=None, vmag_start=None) -> dict:
         """Solve a stacked batch. numpy in -> numpy out (host staging inside
-        the library); CUDA tensors in -> CUDA tensors out (device pointers)."""
+        the library); CUDA tensors in -> CUDA tensors out (device pointers).
+        ``theta_start``/``vmag_start`` ([batch][n_bus]): start state per
+        scenario instead of the flat start (acpf_nr_solve_start)."""
         dev = _is_device(p_spec)
         b = int(p_spec.shape[0])
         if out is None:
             out = self.alloc_outputs(b, like=p_spec if dev else None)
         flags = ACPF_DEVICE_PTRS if dev else ACPF_HOST_PTRS
-        _check(_lib.acpf_nr_solve(
-            self._h, b, _ptr(p_spec), _ptr(q_spec), float(tol), int(max_newton),
-            _ptr(out["theta"]), _ptr(out["vmag"]), _ptr(out["converged"]),
-            _ptr(out["iterations"]), _ptr(out["final_mismatch_inf"]), _ptr(out["status"]),
-            flags, _stream_ptr(stream, p_spec)))
+        outs = (_ptr(out["theta"]), _ptr(out["vmag"]), _ptr(out["converged"]), _ptr(out["iterations"]),
+                _ptr(out["final_mismatch_inf"]), _ptr(out["status"]))
+        if theta_start is None:
+            _check(_lib.acpf_nr_solve(self._h, b, _ptr(p_spec), _ptr(q_spec), float(tol), int(max_newton),
+                                      *outs, flags, _stream_ptr(stream, p_spec)))
+        else:
+            _check(_lib.acpf_nr_solve_start(self._h, b, _ptr(p_spec), _ptr(q_spec), _ptr(theta_start),
+                                            _ptr(vmag_start), float(tol), int(max_newton), *outs, flags,
+                                            _stream_ptr(stream, p_spec)))
         return out
 
     def alloc_outputs(self, b: int, like=None) -> dict:

@@ -218,11 +218,13 @@ def _stack(model: TransmissionModel, scenarios):
 
 
 def _check_options(opts: NewtonOptions | None, start) -> NewtonOptions:
+    """Reference newton_solve (transmission.py:319-324): a start state is used
+    as given; without one, flat_start=False is an error."""
     opts = opts or NewtonOptions()
-    if start is not None:
-        raise NotImplementedError("the GPU engine solves from the flat start only")
-    if not opts.flat_start:
+    if start is None and not opts.flat_start:
         raise ValueError("flat_start=False requires an explicit start state")
+    if start is not None and opts.step == "gmres":
+        raise NotImplementedError("the GPU GMRES ablation solves from the flat start only")
     return opts
 
 
@@ -259,7 +261,7 @@ _FAILED_ROW = {"converged": 0, "iterations": 0, "final_mismatch_inf": np.inf, "s
 
 
 def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = None,
-                       device: int | None = None, devices=None):
+                       device: int | None = None, devices=None, starts=None):
     """Solve a list of scenarios on the GPU; order preserved.
 
     Each record equals ``newton_solve(model, scenario, opts)`` of the
@@ -270,10 +272,12 @@ def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = Non
     ``device`` picks a single GPU. A malformed scenario becomes a failed
     record (NaN state, diagnostic = the error) instead of failing the batch,
     as the reference's batch driver isolates it (batch.py:237-239).
+    ``starts``: a PolarState per scenario (or one for all) to start from
+    instead of the flat start (reference ``start=``, transmission.py:306-330).
     """
     from .results import NewtonResults, scatter_rows, solve_sharded
     model = _as_model(net_or_model)
-    opts = _check_options(opts, None)
+    opts = _check_options(opts, starts)
     if len(scenarios) == 0:
         return NewtonResults({k: np.empty((0,) if k not in ("theta", "vmag") else (0, len(model.net.buses)))
                               for k in _FAILED_ROW})
@@ -288,8 +292,24 @@ def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = Non
         out["gmres_diag_k"] = np.zeros(b, dtype=np.int32)
         out["gmres_diag_relres"] = np.zeros(b)
 
+    th0 = vm0 = None
+    if starts is not None:
+        from . import hostmem
+        st_list = [starts] * len(scenarios) if isinstance(starts, PolarState) else list(starts)
+        if len(st_list) != len(scenarios):
+            raise ValueError("starts must be one PolarState or one per scenario")
+        n = len(model.net.buses)
+        th0, vm0 = hostmem.empty((b, n)), hostmem.empty((b, n))
+        for j, k in enumerate(idx):
+            th0[j] = np.asarray(st_list[k].theta, dtype=np.float64)
+            vm0[j] = np.asarray(st_list[k].vmag, dtype=np.float64)
+
     def shard(slot, dev, lo, hi, view):
         plan = model.plan(dev, slot)
+        if th0 is not None:
+            plan.solve(p[lo:hi], q[lo:hi], opts.tol_mismatch, opts.max_newton, out=view,
+                       theta_start=th0[lo:hi], vmag_start=vm0[lo:hi])
+            return
         if gm:
             if getattr(plan, "_fd_eps", None) != opts.epsilon:
                 plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, opts.epsilon)
@@ -306,12 +326,15 @@ def batch_newton_solve(net_or_model, scenarios, opts: NewtonOptions | None = Non
 
 def newton_solve(net_or_model, scenario: TransmissionScenario | None = None,
                  opts: NewtonOptions | None = None, start: PolarState | None = None) -> NewtonResult:
-    """Reference :306-330 (flat start), computed on the GPU."""
+    """Reference :306-330 (flat start, or ``start``), computed on the GPU."""
     model = _as_model(net_or_model)
     opts = _check_options(opts, start)
     if scenario is None:
         scenario = base_scenario(model.net, model.part)
-    return batch_newton_solve(model, [scenario], opts)[0]
+    r = batch_newton_solve(model, [scenario], opts, starts=None if start is None else [start])
+    if r.errors:
+        raise ValueError(r.errors[0].split(": ", 1)[-1])
+    return r[0]
 
 
 class GpuNewtonSolver:

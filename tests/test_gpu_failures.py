@@ -39,7 +39,7 @@ def _solve_nr(model, d):
     keys = sorted({(float(t), int(m)) for t, m in zip(d["tol"], d["max_newton"])})
     rows = [None] * n
     for tol, mx in keys:
-        idx = np.flatnonzero((d["tol"] == tol) & (d["max_newton"] == mx))
+        idx = np.flatnonzero((d["tol"] == tol) & (d["max_newton"] == mx) & ~d["has_start"])
         o = model.plan().solve(np.ascontiguousarray(d["p_spec"][idx]), np.ascontiguousarray(d["q_spec"][idx]),
                                tol, mx)
         res = results_from_arrays(o)
@@ -56,6 +56,8 @@ def test_nr_failure_branches(tag, golden):
     res = _solve_nr(model, d)["res"]
     for s, r in enumerate(res):
         lab = str(d["label"][s])
+        if d["has_start"][s]:
+            continue  # warm starts: test_nr_warm_start
         assert r.converged == bool(d["converged"][s]), lab
         assert r.iterations == int(d["iterations"][s]), lab
         assert (r.diagnostic or "") == str(d["diagnostic"][s]), lab
@@ -137,3 +139,34 @@ def test_zbus_failure_branches(key, golden):
             assert r.residual_inf <= 1e-6, s
         else:
             assert r.residual_inf == rr, s
+
+
+@pytest.mark.parametrize("tag", list(TX))
+def test_nr_warm_start(tag, golden):
+    """newton_solve(..., start=PolarState) / flat_start=False (reference
+    transmission.py:306-330) through acpf_nr_solve_start: host buffers via the
+    Python API, device buffers via the plan; flags, iterations and states."""
+    d = _split(golden("fail_nr"), tag)
+    rows = np.flatnonzero(d["has_start"])
+    model = pf.build_transmission_model(load_transmission(TX[tag]))
+    scen = [pf.TransmissionScenario(d["p_spec"][s], d["q_spec"][s]) for s in rows]
+    starts = [pf.PolarState(d["theta0"][s], d["vmag0"][s]) for s in rows]
+    res = tm.batch_newton_solve(model, scen, tm.NewtonOptions(flat_start=False), starts=starts)
+    for s, r in zip(rows, res):
+        assert r.converged == bool(d["converged"][s]) and r.iterations == int(d["iterations"][s]), s
+        assert np.abs(r.state.theta - d["theta"][s]).max() <= 1e-8
+        assert np.abs(r.state.vmag - d["vmag"][s]).max() <= 1e-8
+    one = pf.newton_solve(model, scen[0], start=starts[0])
+    assert one.iterations == int(d["iterations"][rows[0]])
+    torch = pytest.importorskip("torch")
+    cuda = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    out = model.plan().solve(cuda(d["p_spec"][rows]), cuda(d["q_spec"][rows]), 1e-8, 20,
+                             theta_start=cuda(d["theta0"][rows]), vmag_start=cuda(d["vmag0"][rows]))
+    np.testing.assert_array_equal(out["iterations"].cpu().numpy(), d["iterations"][rows])
+    assert np.abs(out["vmag"].cpu().numpy() - d["vmag"][rows]).max() <= 1e-8
+    # the flat start after a warm one (graph caches keyed on the start mode)
+    flat = model.plan().solve(np.ascontiguousarray(d["p_spec"][rows]), np.ascontiguousarray(d["q_spec"][rows]),
+                              1e-8, 20)
+    assert flat["converged"].all()
+    with pytest.raises(ValueError):
+        pf.newton_solve(model, scen[0], tm.NewtonOptions(flat_start=False))

@@ -30,14 +30,17 @@ def test_oracle_nr_failures(tag, golden):
     rows = range(d["tol"].size) if tag not in ("gb2224", "case1354") else range(0, d["tol"].size, 3)
     for s in rows:
         lab = str(d["label"][s])
+        cs = case
+        if "has_start" in d and d["has_start"][s]:  # warm start (transmission.py:306-330)
+            cs = onr.NrCase(m.y.csr, m.part.theta_block, m.part.q_block, d["theta0"][s], d["vmag0"][s])
         with np.errstate(all="ignore"):
-            o = onr.newton(case, d["p_spec"][s], d["q_spec"][s], tol=float(d["tol"][s]),
+            o = onr.newton(cs, d["p_spec"][s], d["q_spec"][s], tol=float(d["tol"][s]),
                            max_newton=int(d["max_newton"][s]))
         assert o.converged == bool(d["converged"][s]), lab
         assert o.iterations == int(d["iterations"][s]), lab
         assert (o.diagnostic or "") == str(d["diagnostic"][s]), lab
         np.testing.assert_equal(np.isnan(o.final_mismatch_inf), np.isnan(d["fnorm"][s]))
-        if np.isfinite(d["fnorm"][s]) and lab.startswith(("max_newton", "tol")):
+        if np.isfinite(d["fnorm"][s]) and lab.startswith(("max_newton", "tol", "warm")):
             assert o.final_mismatch_inf == pytest.approx(float(d["fnorm"][s]), rel=1e-8), lab
             assert np.abs(o.theta - d["theta"][s]).max() <= 1e-10, lab
             assert np.abs(o.vmag - d["vmag"][s]).max() <= 1e-10, lab

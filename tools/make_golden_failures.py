@@ -16,6 +16,8 @@ NR `_newton_loop` (transmission.py:333-380), tests/golden/fail_nr.npz
   * heavy loads (x2 .. x30 of the base case): slow convergence (5, 7
     iterations) and V <= 0 collapses at iterations 1 .. 10, :355-357
   * an extreme injection (1e150) that collapses at iteration 1
+  * warm starts (`start=`, flat_start=False; :306-330): from the base case's
+    solution and from a perturbed flat start
 Z-Bus `_zbus_loop` (distribution.py:653-687), tests/golden/fail_zb.npz
   * VoltageFloorError on a wye phase at sweep 1 (v = v0) and at sweep 5
     (v = previous iterate), on a delta phase, and on a delta line-to-line
@@ -83,10 +85,25 @@ def _nr_cases(ac):
             p = b.p_spec.copy()
             p[0] = 1e150
             rows.append((p, b.q_spec, 1e-8, 20, "p_spec[0] = 1e150"))
+        # warm starts (transmission.py:306-330 `start=`): from the base case's
+        # solution, and from a perturbed flat start, with flat_start=False
+        flat = ac.flat_start(net, part)
+        bsol = ac.newton_solve(model, b).state
+        rng = np.random.default_rng(77)
+        pert = ac.PolarState(flat.theta + rng.normal(scale=0.02, size=flat.theta.size),
+                             flat.vmag * (1 + rng.normal(scale=0.01, size=flat.vmag.size)))
+        starts = [None] * len(rows)
+        for s in seeded[:4]:
+            rows.append((s.p_spec, s.q_spec, 1e-8, 20, "warm: base solution"))
+            starts.append(bsol)
+            rows.append((s.p_spec, s.q_spec, 1e-8, 20, "warm: perturbed flat start"))
+            starts.append(pert)
         res = []
-        for p, q, tol, mx, _ in rows:
-            opts = ac.NewtonOptions(tol_mismatch=tol, max_newton=mx)
-            res.append(ac.newton_solve(model, ac.TransmissionScenario(p, q), opts))
+        for (p, q, tol, mx, _), st in zip(rows, starts):
+            opts = ac.NewtonOptions(tol_mismatch=tol, max_newton=mx, flat_start=st is None)
+            res.append(ac.newton_solve(model, ac.TransmissionScenario(p, q), opts, start=st))
+        th0 = np.stack([(flat if st is None else st).theta for st in starts])
+        vm0 = np.stack([(flat if st is None else st).vmag for st in starts])
         out[tag] = dict(
             p_spec=np.stack([r[0] for r in rows]), q_spec=np.stack([r[1] for r in rows]),
             tol=np.array([r[2] for r in rows]), max_newton=np.array([r[3] for r in rows], dtype=np.int32),
@@ -94,7 +111,8 @@ def _nr_cases(ac):
             converged=np.array([r.converged for r in res]), iterations=np.array([r.iterations for r in res]),
             fnorm=np.array([r.final_mismatch_inf for r in res]),
             diagnostic=np.array([r.diagnostic or "" for r in res]),
-            theta=np.stack([r.state.theta for r in res]), vmag=np.stack([r.state.vmag for r in res]))
+            theta=np.stack([r.state.theta for r in res]), vmag=np.stack([r.state.vmag for r in res]),
+            has_start=np.array([st is not None for st in starts]), theta0=th0, vmag0=vm0)
         print(tag, [(r[4], x.converged, x.iterations, x.diagnostic) for r, x in zip(rows, res)
                     if not r[4].startswith(("max_newton", "tol"))])
     return out
