@@ -30,6 +30,8 @@
 
 #include "acpf_internal.cuh"
 
+#include <cstdlib>
+
 namespace acpf {
 
 namespace {
@@ -49,6 +51,19 @@ constexpr int kRowGroups = 8 / kRowWarps;
 constexpr int kColWarps = ACPF_ZB_COL_WARPS;
 constexpr int kThreads = kRowWarps * kColWarps * 32;
 constexpr int kMaxKsPerStage = 16;  // k-steps (of 4) per Z stage
+// Row-block classes: the per-column sums of every pass are formed per class
+// (row blocks c, c + V, c + 2V, ... for c = 0..V-1, each in order) and the V
+// class partials are then added in class order. A batch too small to fill
+// the GPU with tiles (fewer tiles than resident clusters) runs each tile on a
+// thread-block cluster of V CTAs, CTA c streaming class c's row blocks and
+// the partials combined through distributed shared memory; larger batches run
+// one CTA per tile that walks the classes one after the other. Both give the
+// same bits, so results stay independent of the batch size, and a small
+// batch's sweeps take ~1/V of the time.
+#ifndef ACPF_ZB_VIRT
+#define ACPF_ZB_VIRT 4
+#endif
+constexpr int kZbVirt = ACPF_ZB_VIRT;
 constexpr int kZbBuf = 2;            // Z stage buffers (TMA ring; 4 x half-K stages measured 2% slower)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -95,6 +110,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+template <int CL>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  if (CL == 1) return 0;
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+// cluster-wide barrier with release/acquire semantics (orders the global v
+// writes of one CTA before the other CTAs' next injection reads)
+template <int CL>
+__device__ __forceinline__ void cluster_sync_all() {
+  if (CL == 1) {
+    __syncthreads();
+    return;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// a double in CTA `rank`'s shared memory at the address of `p` in this CTA
+__device__ __forceinline__ double ld_dsmem(const double* p, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
+
 // reference-style complex quotient s / v (scaled, no overflow for |v| ~ 1)
 __device__ __forceinline__ double2 cdiv(double2 s, double2 v) {
   if (fabs(v.x) >= fabs(v.y)) {
@@ -128,19 +171,33 @@ struct ZbTileState {
   double* red;     // [kRowWarps][NT]
   int* run;        // [NT] 1 = running (writes allowed in an iterate pass)
   int* cert;       // [NT] 1 = needs the certificate pass
+  double* part;    // [kZbVirt][NT] per-class column partials of a pass
 };
 
 // One sweep over all Z stages for the current tile.
-template <int NT, int MODE>
+template <int NT, int MODE, int CL>
 __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t tile_col0,
                         double* zs, const double* isf, uint64_t* bars, uint32_t& phase_bits,
-                        ZbTileState st) {
+                        ZbTileState st, int crank) {
   constexpr int CGW = Smem<NT>::kCgWarp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rp = warp % kRowWarps, ch = warp / kRowWarps;
   const int ksteps = m.kpad >> 2;
   const int n_kc = (ksteps + kMaxKsPerStage - 1) / kMaxKsPerStage;
-  const int n_stage = m.n_rb * n_kc;
+  // this CTA's row-block classes: its rank's (cluster of kZbVirt) or all of
+  // them in order (one CTA per tile); class c = row blocks c, c + V, ...
+  const int c_begin = CL == 1 ? 0 : crank, c_end = CL == 1 ? kZbVirt : crank + 1;
+  auto nrb = [&](int c) { return m.n_rb > c ? (m.n_rb - c + kZbVirt - 1) / kZbVirt : 0; };
+  int n_stage = 0;
+  for (int c = c_begin; c < c_end; ++c) n_stage += nrb(c) * n_kc;
+  // stage -> (class, row block, k chunk)
+  auto decode = [&](int sidx, int& cls, int& rb, int& kc) {
+    int c = c_begin, base = 0;
+    while (base + nrb(c) * n_kc <= sidx) base += nrb(c++) * n_kc;
+    cls = c;
+    rb = c + kZbVirt * ((sidx - base) / n_kc);
+    kc = (sidx - base) % n_kc;
+  };
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
 
   // Each stage is two row halves (rows 0-31 / 32-63 of the row block), each
@@ -155,7 +212,8 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   uint64_t* const fullb = bars + half * kZbBuf;                // [kZbBuf] of this half
   uint64_t* const emptyb = bars + 2 * kZbBuf + half * kZbBuf;  // [kZbBuf] of this half
   auto issue = [&](int sidx) {
-    const int rb = sidx / n_kc, kc = sidx % n_kc;
+    int cls_, rb, kc;
+    decode(sidx, cls_, rb, kc);
     const int ks0 = kc * kMaxKsPerStage;
     const int nks = min(kMaxKsPerStage, ksteps - ks0);
     const double* src = m.zfrag + (((size_t)rb * 2 + half) * ksteps + ks0) * 256;
@@ -196,8 +254,27 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
   double acc[CGW][2];
 #pragma unroll
   for (int b = 0; b < CGW; ++b) acc[b][0] = acc[b][1] = 0.0;
+  // per-pass column reduction of the lane partials of one class: 8 row lanes
+  // (fixed butterfly), then the kRowWarps row warps in fixed order
+  // (the lane butterfly here, per warp; the row warps at the end of the pass)
+  auto flush = [&](int cls) {
+#pragma unroll
+    for (int b = 0; b < CGW; ++b)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double x = acc[b][j];
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          const double o = __shfl_xor_sync(0xffffffffu, x, off);
+          x = (MODE == kCert) ? nanmax(x, o) : x + o;
+        }
+        if (lane < 4) st.red[(cls * kRowWarps + rp) * NT + (ch * CGW + b) * 8 + 2 * lane + j] = x;
+        acc[b][j] = 0.0;
+      }
+  };
   for (int sidx = 0; sidx < n_stage; ++sidx) {
-    const int rb = sidx / n_kc, kc = sidx % n_kc;
+    int cls, rb, kc;
+    decode(sidx, cls, rb, kc);
     const int buf = sidx % kZbBuf;
     if (kc == 0) {
 #pragma unroll
@@ -305,6 +382,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
         }
       }
     }
+    if (kc == n_kc - 1 && rb + kZbVirt >= m.n_rb) flush(cls);  // the class's last row block
   }
   // the empty-barrier phases of the stages whose refill was not needed
   // (the last kZbBuf) still advance: keep thread 0's parity bits in sync
@@ -315,27 +393,25 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
       phase_bits ^= (1u << (kZbBuf + buf));
     }
   }
-  // ---- per-pass column reduction: 8 row lanes (fixed butterfly), then the
-  // kRowWarps row warps in fixed order
-#pragma unroll
-  for (int b = 0; b < CGW; ++b)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      double x = acc[b][j];
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, x, off);
-        x = (MODE == kCert) ? nanmax(x, o) : x + o;
-      }
-      if (lane < 4) st.red[rp * NT + (ch * CGW + b) * 8 + 2 * lane + j] = x;
-    }
+  // per class: the kRowWarps row warps in fixed order (classes without row
+  // blocks contribute 0); then this CTA's column sums: the classes in order
+  // (one CTA per tile) or its own class (cluster)
   __syncthreads();
   if (tid < NT) {
-    const double* r = st.red;
-    double x = r[tid];
+    for (int c = c_begin; c < c_end; ++c) {
+      double x = 0.0;
+      if (nrb(c) > 0) {
+        const double* r = st.red + (size_t)c * kRowWarps * NT;
+        x = r[tid];
 #pragma unroll
-    for (int w = 1; w < kRowWarps; ++w) x = (MODE == kCert) ? nanmax(x, r[w * NT + tid]) : x + r[w * NT + tid];
-    st.colsum[tid] = (MODE == kCert) ? nanmax(st.colsum[tid], x) : st.colsum[tid] + x;
+        for (int w = 1; w < kRowWarps; ++w) x = (MODE == kCert) ? nanmax(x, r[w * NT + tid]) : x + r[w * NT + tid];
+      }
+      st.part[c * NT + tid] = x;
+    }
+    double x = st.part[c_begin * NT + tid];
+    for (int c = c_begin + 1; c < c_end; ++c)
+      x = (MODE == kCert) ? nanmax(x, st.part[c * NT + tid]) : x + st.part[c * NT + tid];
+    st.colsum[tid] = x;
   }
   __syncthreads();
 }
@@ -351,7 +427,7 @@ __device__ int zb_injection(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t
   }
   auto vat = [&](int lcol) -> double2 {
     const int row = m.l_row[lcol];
-    return from_v0 ? m.v0[row] : io.v_out[scen * m.n + row];
+    return from_v0 ? m.v0[row] : __ldcg(io.v_out + scen * m.n + row);
   };
   // floor checks in the reference order (distribution.py:583-606)
   for (int k = 0; k < m.n_wye; ++k) {
@@ -418,7 +494,7 @@ __device__ void zb_injection_cta(const ZbDeviceModel& m, const ZbBatchIO& io, in
     const int col = idx / nl, lc = idx - col * nl;
     if (!want[col]) continue;
     const int row = m.l_row[lc];
-    vl[idx] = from_v0 ? m.v0[row] : io.v_out[(col0 + col) * m.n + row];
+    vl[idx] = from_v0 ? m.v0[row] : __ldcg(io.v_out + (col0 + col) * m.n + row);
   }
   __syncthreads();
   for (int idx = tid; idx < NT * nld; idx += kThreads) {
@@ -472,7 +548,28 @@ __device__ void zb_injection_cta(const ZbDeviceModel& m, const ZbBatchIO& io, in
   }
 }
 
-template <int NT>
+// Combine the cluster's per-CTA column partials (sum, or NaN-propagating max
+// for the certificate) in rank order; every CTA ends with the same totals.
+template <int NT, int CL, bool MAX>
+__device__ __forceinline__ void zb_cluster_combine(double* colsum) {
+  if (CL == 1) return;      // colsum already holds the totals
+  cluster_sync_all<CL>();   // every CTA's partial is in its colsum
+  const int tid = threadIdx.x;
+  double x = 0.0;
+  if (tid < NT) {
+    x = ld_dsmem(colsum + tid, 0);
+#pragma unroll
+    for (int r = 1; r < CL; ++r) {
+      const double y = ld_dsmem(colsum + tid, (uint32_t)r);
+      x = MAX ? nanmax(x, y) : x + y;
+    }
+  }
+  cluster_sync_all<CL>();  // all remote reads done before colsum is overwritten
+  if (tid < NT) colsum[tid] = x;
+  __syncthreads();
+}
+
+template <int NT, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     zbus_kernel(ZbDeviceModel m, ZbBatchIO io, double tol, int max_iter, int mag0_mode,
                 double* mag0_out) {
@@ -483,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* isf = zs + kZbBuf * stage_doubles;
   double* colsum = isf + (size_t)ksteps * NT * 8;
   double* red = colsum + NT;
-  double* mag = red + kRowWarps * NT;
+  double* mag = red + kZbVirt * kRowWarps * NT;
   double* delta = mag + NT;
   double* resid = delta + NT;
   int* run = reinterpret_cast<int*>(resid + NT);
@@ -492,8 +589,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* iters = stat + NT;
   int* fslot = iters + NT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(fslot + NT + (NT & 1));
+  double* part = reinterpret_cast<double*>(bars + 4 * kZbBuf);  // [kZbVirt][NT]
 
   const int tid = threadIdx.x;
+  const int crank = (int)cluster_rank<CL>();
   if (tid == 0) {
     for (int b = 0; b < 2 * kZbBuf; ++b) {
       mbar_init(bars + b, 1);                              // half-stage full (TMA transaction count)
@@ -503,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   uint32_t phase_bits = 0;
-  ZbTileState st{colsum, red, run, cert};
+  ZbTileState st{colsum, red, run, cert, part};
   // the CTA-wide injection needs [NT][n_l] voltages + [NT][loads] currents of
   // scratch in the (then idle) Z stage buffers
   const bool par_inj = (size_t)NT * (m.n_l + m.n_wye + m.n_delta) * 2 <= kZbBuf * (size_t)stage_doubles;
@@ -512,13 +611,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = tid; k < ksteps * NT * 8; k += kThreads) isf[k] = 0.0;
     if (tid < NT) colsum[tid] = 0.0, run[tid] = 0;
     __syncthreads();
-    zb_pass<NT, kMag0>(m, io, 0, zs, isf, bars, phase_bits, st);
-    if (tid == 0) *mag0_out = colsum[0];
+    zb_pass<NT, kMag0, CL>(m, io, 0, zs, isf, bars, phase_bits, st, crank);
+    zb_cluster_combine<NT, CL, false>(colsum);
+    if (tid == 0 && crank == 0) *mag0_out = colsum[0];
     return;
   }
 
   const int64_t n_tiles = (io.batch + NT - 1) / NT;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  for (int64_t tile = cid; tile < n_tiles; tile += ncl) {
     const int64_t col0 = tile * NT;
     const int64_t scen = col0 + tid;
     if (tid < NT) {
@@ -548,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             iters[tid] = k;
             fslot[tid] = fs;
             resid[tid] = __longlong_as_double(0x7ff0000000000000LL);
-            if (k == 1)
+            if (k == 1 && crank == 0)
               for (int r = 0; r < m.n; ++r) io.v_out[scen * m.n + r] = m.v0[r];
           }
         }
@@ -561,7 +662,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int any = __syncthreads_or(tid < NT && run[tid]);
       if (!any) break;
-      zb_pass<NT, kIterate>(m, io, col0, zs, isf, bars, phase_bits, st);
+      zb_pass<NT, kIterate, CL>(m, io, col0, zs, isf, bars, phase_bits, st, crank);
+      zb_cluster_combine<NT, CL, false>(colsum);
       if (tid < NT && run[tid]) {
         const double s = colsum[tid];
         const double d = fabs(s - mag[tid]);
@@ -606,10 +708,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int anyc = __syncthreads_or(tid < NT && cert[tid]);
     if (anyc) {
-      zb_pass<NT, kCert>(m, io, col0, zs, isf, bars, phase_bits, st);
+      zb_pass<NT, kCert, CL>(m, io, col0, zs, isf, bars, phase_bits, st, crank);
+      zb_cluster_combine<NT, CL, true>(colsum);
       if (tid < NT && cert[tid]) resid[tid] = colsum[tid];
     }
-    if (tid < NT && scen < io.batch) {
+    if (tid < NT && scen < io.batch && crank == 0) {
       if (io.converged) io.converged[scen] = stat[tid] == ACPF_ZB_CONVERGED;
       if (io.iterations) io.iterations[scen] = iters[tid];
       if (io.final_delta) io.final_delta[scen] = delta[tid];
@@ -625,25 +728,89 @@ template <int NT>
 size_t zbus_smem_bytes(int kpad) {
   const int ksteps = kpad >> 2;
   const int stage_doubles = (ksteps < kMaxKsPerStage ? ksteps : kMaxKsPerStage) * 512;
-  size_t d = kZbBuf * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kRowWarps * NT + 3 * NT;
+  size_t d = kZbBuf * (size_t)stage_doubles + (size_t)ksteps * NT * 8 + NT + kZbVirt * kRowWarps * NT + 3 * NT;
   size_t bytes = d * 8 + (5 * NT + 2) * 4 + 32 * kZbBuf + 16;
-  return bytes;
+  return bytes + (size_t)kZbVirt * NT * 8;  // per-class partials (after the barriers)
+}
+
+template <int NT, int CL>
+cudaError_t launch_ntc(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter, bool mag0_mode,
+                       double* mag0_out, cudaStream_t stream, int clusters, size_t smem) {
+  if (CL == 1) {
+    zbus_kernel<NT, 1><<<clusters, kThreads, smem, stream>>>(m, io, tol, max_iter, mag0_mode ? 1 : 0, mag0_out);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(clusters * CL), 1, 1);
+  return cudaLaunchKernelEx(&cfg, zbus_kernel<NT, CL>, m, io, tol, max_iter, mag0_mode ? 1 : 0, mag0_out);
+}
+
+// clusters of CL CTAs that can be resident at once (clusters live inside a GPC)
+template <int NT, int CL>
+int resident_clusters(size_t smem, int sms) {
+  static int cached = 0;
+  if (cached > 0) return cached;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(sms / CL * CL), 1, 1);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, zbus_kernel<NT, CL>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 0;  // no cluster launch possible: one CTA per tile
+  }
+  cached = n > 0 ? n : -1;
+  return n;
 }
 
 template <int NT>
 cudaError_t launch_nt(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, int max_iter,
                       bool mag0_mode, double* mag0_out, cudaStream_t stream) {
   const size_t smem = zbus_smem_bytes<NT>(m.kpad);
-  cudaError_t err = cudaFuncSetAttribute(zbus_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t err = cudaFuncSetAttribute(zbus_kernel<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(zbus_kernel<NT, kZbVirt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(zbus_kernel<NT, kZbVirt>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   if (err != cudaSuccess) return err;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = mag0_mode ? 1 : (io.batch + NT - 1) / NT;
+  // small batches: one cluster per tile (ACPF_ZB_CLUSTER=0 disables);
+  // otherwise one CTA per tile (same bits)
+  static const bool allow = [] {
+    const char* v = std::getenv("ACPF_ZB_CLUSTER");
+    return !(v && v[0] == '0');
+  }();
+  // (only when every CTA of the cluster has row blocks to stream)
+  const int rc = (allow && !mag0_mode && kZbVirt > 1 && m.n_rb >= 2 * kZbVirt)
+                     ? resident_clusters<NT, kZbVirt>(smem, sms) : 0;
+  // a tile takes ~1/kZbVirt of the time on a cluster: worth it while the
+  // tiles fit in up to kZbVirt - 1 waves of clusters
+  if (rc > 0 && tiles <= (int64_t)(kZbVirt - 1) * rc)
+    return launch_ntc<NT, kZbVirt>(m, io, tol, max_iter, mag0_mode, mag0_out, stream,
+                                   (int)(tiles < rc ? tiles : rc), smem);
   const int grid = (int)(tiles < sms ? tiles : sms);
-  zbus_kernel<NT><<<grid, kThreads, smem, stream>>>(m, io, tol, max_iter, mag0_mode ? 1 : 0, mag0_out);
-  return cudaGetLastError();
+  return launch_ntc<NT, 1>(m, io, tol, max_iter, mag0_mode, mag0_out, stream, grid, smem);
 }
 
 }  // namespace
