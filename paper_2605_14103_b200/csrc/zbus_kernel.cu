@@ -758,8 +758,10 @@ cudaError_t launch_ntc(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, 
 // clusters of CL CTAs that can be resident at once (clusters live inside a GPC)
 template <int NT, int CL>
 int resident_clusters(size_t smem, int sms) {
+  static size_t cached_smem = 0;  // the answer depends on the feeder's shared memory
   static int cached = 0;
-  if (cached > 0) return cached;
+  if (cached != 0 && cached_smem == smem) return cached > 0 ? cached : 0;
+  cached_smem = smem;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
