@@ -913,7 +913,7 @@ constexpr int kTYCol = kTRows;    // the right-hand side column
 constexpr int kTTiles = kTRows / 8 + 1;
 constexpr int kTLd = 148;         // U row stride: 148 = 4 (mod 16), conflict-free B fragments (4 rows x 8 cols)
 constexpr int kTPcLd = 12;        // panel-column stride: conflict-free A fragments (8 rows x 4 cols)
-constexpr size_t kTailSmem = ((size_t)kTRows * kTLd + (size_t)kTRows * kTPcLd + 16 + 2 * kTRows) * 8 + 16;
+constexpr size_t kTailSmem = ((size_t)kTRows * kTLd + (size_t)kTRows * kTPcLd + 16 * 16 + 2 * kTRows) * 8 + 16;
 
 __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -921,13 +921,126 @@ __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double 
       : "d"(a), "d"(b));
 }
 
+// Panel-specialised pieces of nr_tail_kernel: with the panel index a template
+// constant every accumulator tile index is static, so the tile loops carry no
+// predicates or warp syncs and the B-fragment loads can be scheduled ahead of
+// the DMMAs (the runtime-indexed form ran the update phase at 1/5 of the DMMA
+// pipe rate). Tiles past the matrix are zero and stay zero.
+// (d) for panel P: C -= L^(strip, panel) U^(panel, tiles right of it). The
+// next panel's owner updates its diagonal tile first and publishes it (look-
+// ahead: warp 0 factors it while the other warps are still updating).
+template <int P>
+__device__ __forceinline__ void tail_update(double (&C)[kTTiles][2], const double* Pc, double* U, int crow,
+                                            int ccol, int lane, bool owner, volatile int* ready) {
+  const double a0 = -Pc[crow * kTPcLd + (lane & 3)], a1 = -Pc[crow * kTPcLd + 4 + (lane & 3)];
+  const double* const ub0 = U + (8 * P + (lane & 3)) * kTLd + (lane >> 2);
+  const double* const ub1 = ub0 + 4 * kTLd;
+  if (P + 1 < kTTiles && owner) {
+    dmma_t(C[P + 1][0], C[P + 1][1], a0, ub0[8 * (P + 1)]);
+    dmma_t(C[P + 1][0], C[P + 1][1], a1, ub1[8 * (P + 1)]);
+    *reinterpret_cast<double2*>(U + crow * kTLd + 8 * (P + 1) + ccol) = make_double2(C[P + 1][0], C[P + 1][1]);
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *ready = P + 1;
+  }
+  const int jd = owner ? P + 2 : P + 1;  // first tile still to update
+  double b[kTTiles];
+#pragma unroll
+  for (int j = P + 1; j < kTTiles; ++j) b[j] = ub0[8 * j];
+#pragma unroll
+  for (int j = P + 1; j < kTTiles; ++j)
+    if (j >= jd) dmma_t(C[j][0], C[j][1], a0, b[j]);
+#pragma unroll
+  for (int j = P + 1; j < kTTiles; ++j) b[j] = ub1[8 * j];
+#pragma unroll
+  for (int j = P + 1; j < kTTiles; ++j)
+    if (j >= jd) dmma_t(C[j][0], C[j][1], a1, b[j]);
+}
+
+// (a) for panel P: the panel column -> Pc; the owner's strip right of its
+// (already factored) diagonal tile -> U
+template <int P>
+__device__ __forceinline__ void tail_store_panel(const double (&C)[kTTiles][2], double* Pc, double* U, int crow,
+                                                 int ccol, bool owner) {
+  *reinterpret_cast<double2*>(Pc + crow * kTPcLd + ccol) = make_double2(C[P][0], C[P][1]);
+  if (owner) {
+#pragma unroll
+    for (int j = P + 1; j < kTTiles; ++j)
+      *reinterpret_cast<double2*>(U + crow * kTLd + 8 * j + ccol) = make_double2(C[j][0], C[j][1]);
+  }
+}
+
+// (b) the 8 x 8 diagonal block of a panel (4 x 4 blocks of 2 x 2) in shared
+// memory, 4 block steps by one warp: pivot inverses D_k^-1 -> dinv, U^ blocks
+// right of each pivot, update of the blocks below; leaves L^11 (lower), D
+// (diagonal, raw) and U^11 (upper) in place. r0: first scalar row of the panel.
+__device__ __forceinline__ void tail_diag_block(double* Dg, double* dinv, int lane, int r0, int n2, int* zflag) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double a00 = Dg[(2 * k) * kTLd + 2 * k], a01 = Dg[(2 * k) * kTLd + 2 * k + 1];
+    const double a10 = Dg[(2 * k + 1) * kTLd + 2 * k], a11 = Dg[(2 * k + 1) * kTLd + 2 * k + 1];
+    const double det = a00 * a11 - a01 * a10;
+    const double rd = 1.0 / det;
+    const double i00 = a11 * rd, i01 = -a01 * rd, i10 = -a10 * rd, i11 = a00 * rd;
+    if (lane == 0) {
+      dinv[4 * k] = i00;
+      dinv[4 * k + 1] = i01;
+      dinv[4 * k + 2] = i10;
+      dinv[4 * k + 3] = i11;
+      if (det == 0.0 && r0 + 2 * k < n2) *zflag = 1;
+    }
+    // U^ blocks (k, mb), mb = k+1..3: lanes 0 .. 4(3-k)-1, one entry each
+    const int nu = 4 * (3 - k);
+    double u = 0.0;
+    int ui = 0, uc = 0;
+    if (lane < nu) {
+      ui = (lane & 3) >> 1;
+      uc = 2 * (k + 1 + (lane >> 2)) + (lane & 1);
+      const double f0 = Dg[(2 * k) * kTLd + uc], f1 = Dg[(2 * k + 1) * kTLd + uc];
+      u = ui ? i10 * f0 + i11 * f1 : i00 * f0 + i01 * f1;
+    }
+    __syncwarp();
+    if (lane < nu) Dg[(2 * k + ui) * kTLd + uc] = u;
+    __syncwarp();
+    // trailing entries of the block: F(ri, ci) -= L^(ri, 2k..) U^(2k.., ci)
+    const int nr = 6 - 2 * k;
+    for (int e = lane; e < nr * nr; e += 32) {
+      const int ri = 2 * k + 2 + e / nr, ci = 2 * k + 2 + e % nr;
+      Dg[ri * kTLd + ci] -= Dg[ri * kTLd + 2 * k] * Dg[(2 * k) * kTLd + ci] +
+                            Dg[ri * kTLd + 2 * k + 1] * Dg[(2 * k + 1) * kTLd + ci];
+    }
+    __syncwarp();
+  }
+}
+
+#define ACPF_TAIL_PANEL_SWITCH(p, CALL) \
+  switch (p) {                          \
+    case 0: CALL(0); break;             \
+    case 1: CALL(1); break;             \
+    case 2: CALL(2); break;             \
+    case 3: CALL(3); break;             \
+    case 4: CALL(4); break;             \
+    case 5: CALL(5); break;             \
+    case 6: CALL(6); break;             \
+    case 7: CALL(7); break;             \
+    case 8: CALL(8); break;             \
+    case 9: CALL(9); break;             \
+    case 10: CALL(10); break;           \
+    case 11: CALL(11); break;           \
+    case 12: CALL(12); break;           \
+    case 13: CALL(13); break;           \
+    case 14: CALL(14); break;           \
+    default: CALL(15); break;           \
+  }
+
 __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, NrWorkspace w) {
   extern __shared__ __align__(16) double tsm[];
   double* const U = tsm;                  // [kTRows][kTLd]
   double* const Pc = U + kTRows * kTLd;   // [kTRows][kTPcLd]
-  double* const Dv = Pc + kTRows * kTPcLd;  // [4][2x2] pivot inverses of the current panel
-  double* const xs = Dv + 16;             // [kTRows] solution
+  double* const Dv = Pc + kTRows * kTPcLd;  // [16 panels][4][2x2] pivot inverses
+  double* const xs = Dv + 16 * 16;        // [kTRows] solution
   int* const zflag = reinterpret_cast<int*>(xs + 2 * kTRows);
+  volatile int* const ready = zflag + 1;  // last panel whose diagonal tile is in U (look-ahead)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t s = blockIdx.x;
   const int64_t g = s / kGroup;
@@ -957,7 +1070,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, N
     U[(2 * i) * kTLd + kTYCol] = y.x;
     U[(2 * i + 1) * kTLd + kTYCol] = y.y;
   }
-  if (tid == 0) *zflag = 0;
+  if (tid == 0) *zflag = 0, *ready = 0;
   __syncthreads();
   const int crow = 8 * wid + (lane >> 2), ccol = 2 * (lane & 3);
   double C[kTTiles][2];
@@ -967,64 +1080,20 @@ __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, N
     C[j][0] = v.x;
     C[j][1] = v.y;
   }
+  if (wid == 0) tail_diag_block(U, Dv, lane, 0, n2, zflag);  // panel 0's diagonal block
   __syncthreads();
 
   for (int p = 0; p < np; ++p) {
     const int r0 = 8 * p;
     // (a) panel column -> Pc (rows >= r0); panel rows -> U
     if (wid >= p && wid < np) {
-#pragma unroll
-      for (int j = 0; j < kTTiles - 1; ++j)
-        if (j == p) *reinterpret_cast<double2*>(Pc + crow * kTPcLd + ccol) = make_double2(C[j][0], C[j][1]);
-    }
-    if (wid == p) {
-#pragma unroll
-      for (int j = 0; j < kTTiles; ++j)
-        if (j >= p && (j < np || j == kTTiles - 1))
-          *reinterpret_cast<double2*>(U + crow * kTLd + 8 * j + ccol) = make_double2(C[j][0], C[j][1]);
+#define ACPF_TAIL_STORE(P) tail_store_panel<P>(C, Pc, U, crow, ccol, wid == p)
+      ACPF_TAIL_PANEL_SWITCH(p, ACPF_TAIL_STORE)
+#undef ACPF_TAIL_STORE
     }
     __syncthreads();
-    // (b) the 8 x 8 diagonal block, 4 block steps (warp 0)
-    double* const Dg = U + r0 * kTLd + r0;
-    if (wid == 0) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double a00 = Dg[(2 * k) * kTLd + 2 * k], a01 = Dg[(2 * k) * kTLd + 2 * k + 1];
-        const double a10 = Dg[(2 * k + 1) * kTLd + 2 * k], a11 = Dg[(2 * k + 1) * kTLd + 2 * k + 1];
-        const double det = a00 * a11 - a01 * a10;
-        const double rd = 1.0 / det;
-        const double i00 = a11 * rd, i01 = -a01 * rd, i10 = -a10 * rd, i11 = a00 * rd;
-        if (lane == 0) {
-          Dv[4 * k] = i00;
-          Dv[4 * k + 1] = i01;
-          Dv[4 * k + 2] = i10;
-          Dv[4 * k + 3] = i11;
-          if (det == 0.0 && r0 + 2 * k < n2) *zflag = 1;
-        }
-        // U^ blocks (k, mb), mb = k+1..3: lanes 0 .. 4(3-k)-1, one entry each
-        const int nu = 4 * (3 - k);
-        double u = 0.0;
-        int ui = 0, uc = 0;
-        if (lane < nu) {
-          ui = (lane & 3) >> 1;
-          uc = 2 * (k + 1 + (lane >> 2)) + (lane & 1);
-          const double f0 = Dg[(2 * k) * kTLd + uc], f1 = Dg[(2 * k + 1) * kTLd + uc];
-          u = ui ? i10 * f0 + i11 * f1 : i00 * f0 + i01 * f1;
-        }
-        __syncwarp();
-        if (lane < nu) Dg[(2 * k + ui) * kTLd + uc] = u;
-        __syncwarp();
-        // trailing entries of the block: F(ri, ci) -= L^(ri, 2k..) U^(2k.., ci)
-        const int nr = 6 - 2 * k;
-        for (int e = lane; e < nr * nr; e += 32) {
-          const int ri = 2 * k + 2 + e / nr, ci = 2 * k + 2 + e % nr;
-          Dg[ri * kTLd + ci] -= Dg[ri * kTLd + 2 * k] * Dg[(2 * k) * kTLd + ci] +
-                                Dg[ri * kTLd + 2 * k + 1] * Dg[(2 * k + 1) * kTLd + ci];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
+    double* const Dg = U + r0 * kTLd + r0;  // L^11 | D | U^11 of the panel (factored ahead)
+    const double* const Dvp = Dv + 16 * p;
     // (c) panel rows right of the panel (thread per column, incl. y) and the
     //     L^ blocks of the rows below (thread per row)
     {
@@ -1043,8 +1112,8 @@ __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, N
                 Dg[(2 * k + 1) * kTLd + 2 * mb] * x[2 * mb] + Dg[(2 * k + 1) * kTLd + 2 * mb + 1] * x[2 * mb + 1];
           }
           const double a = x[2 * k], b = x[2 * k + 1];
-          x[2 * k] = Dv[4 * k] * a + Dv[4 * k + 1] * b;
-          x[2 * k + 1] = Dv[4 * k + 2] * a + Dv[4 * k + 3] * b;
+          x[2 * k] = Dvp[4 * k] * a + Dvp[4 * k + 1] * b;
+          x[2 * k + 1] = Dvp[4 * k + 2] * a + Dvp[4 * k + 3] * b;
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) Dg[r * kTLd + (c - r0)] = x[r];
@@ -1071,14 +1140,14 @@ __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, N
     __syncthreads();
     // (d) C -= L^(strip, panel) U^(panel, tiles right of the panel) on the DMMA pipe
     if (wid > p && wid < np) {
-#pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2) {
-        const double a = -Pc[crow * kTPcLd + 4 * s2 + (lane & 3)];
-        const double* const ub = U + (r0 + 4 * s2 + (lane & 3)) * kTLd + (lane >> 2);
-#pragma unroll
-        for (int j = 0; j < kTTiles; ++j)
-          if (j > p && (j < np || j == kTTiles - 1)) dmma_t(C[j][0], C[j][1], a, ub[8 * j]);
+#define ACPF_TAIL_UPDATE(P) tail_update<P>(C, Pc, U, crow, ccol, lane, wid == p + 1, ready)
+      ACPF_TAIL_PANEL_SWITCH(p, ACPF_TAIL_UPDATE)
+#undef ACPF_TAIL_UPDATE
+    } else if (wid == 0 && p + 1 < np) {
+      while (*ready < p + 1) {
       }
+      __threadfence_block();
+      tail_diag_block(U + (r0 + 8) * kTLd + r0 + 8, Dv + 16 * (p + 1), lane, r0 + 8, n2, zflag);
     }
   }
   __syncthreads();
