@@ -108,7 +108,8 @@ typedef struct acpf_nr_plan_info {
  *   perm          fill-reducing ordering of the n_theta block rows (one
  *                 2x2 block per non-slack bus): perm[k] = index into
  *                 theta_block of the bus eliminated k-th; NULL for the
- *                 built-in minimum-degree ordering. Rows are then
+ *                 built-in minimum-fill ordering (acpf_nr_ordering with
+ *                 ACPF_ORDER_MIN_FILL). Rows are then
  *                 level-sorted (a topological order of the elimination tree,
  *                 same fill).                                              */
 acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_rowptr,
@@ -117,6 +118,21 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
                                 const int32_t* q_block, const double* theta_init,
                                 const double* vmag_init, const int32_t* perm,
                                 acpf_nr_plan_t* out);
+
+/* Host-only (no device): a fill-reducing elimination order of the n_theta
+ * block rows for acpf_nr_plan_create's `perm` (replaces the SciPy/SuperLU
+ * MMD ordering a NumPy host would take; the reference factors dense,
+ * sparse.py:159-176). Greedy on the 2x2-block bus graph, lowest index
+ * breaking ties:
+ *   ACPF_ORDER_MIN_DEGREE  fewest remaining neighbours;
+ *   ACPF_ORDER_MIN_FILL    fewest fill edges, then degree (fewer block
+ *                          updates, hence a shorter factor gather stream).
+ * perm_out: len n_theta, perm_out[k] = index into theta_block.             */
+#define ACPF_ORDER_MIN_DEGREE 1
+#define ACPF_ORDER_MIN_FILL 2
+acpf_status acpf_nr_ordering(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
+                             int32_t n_theta, const int32_t* theta_block, int32_t kind,
+                             int32_t* perm_out);
 
 /* Host-only symbolic analysis (no device needed): fills the structural
  * fields of `info` (workspace_bytes_per_group included) for the same inputs

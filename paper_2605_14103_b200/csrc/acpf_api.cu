@@ -371,6 +371,24 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
   return ACPF_OK;
 }
 
+acpf_status acpf_nr_ordering(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col, int32_t n_theta,
+                             const int32_t* theta_block, int32_t kind, int32_t* perm_out) {
+  if (n_bus <= 0 || !y_rowptr || !y_col || n_theta <= 0 || !theta_block || !perm_out ||
+      (kind != ACPF_ORDER_MIN_DEGREE && kind != ACPF_ORDER_MIN_FILL)) {
+    set_error("acpf_nr_ordering: invalid argument");
+    return ACPF_EINVAL;
+  }
+  try {
+    NrSymbolic s;
+    build_nr_symbolic(s, n_bus, y_rowptr, y_col, n_theta, theta_block, 0, nullptr, nullptr, kind);
+    std::memcpy(perm_out, s.perm.data(), (size_t)n_theta * sizeof(int32_t));
+  } catch (const std::exception& ex) {
+    set_error(std::string("ordering: ") + ex.what());
+    return ACPF_EINVAL;
+  }
+  return ACPF_OK;
+}
+
 acpf_status acpf_nr_analyze(int32_t n_bus, const int32_t* y_rowptr, const int32_t* y_col,
                             int32_t n_theta, const int32_t* theta_block, int32_t n_q,
                             const int32_t* q_block, const int32_t* perm, acpf_nr_plan_info* info) {

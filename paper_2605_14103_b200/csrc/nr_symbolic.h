@@ -109,8 +109,11 @@ bool nr_flat_start_factor(const NrSymbolic& s, const NrSchedule& o, int n_bus, c
 // Level-sorted topological reordering of an elimination order (same fill).
 std::vector<int32_t> level_sorted_perm(const NrSymbolic& s);
 
+// perm_in: elimination order (perm[k] = unknown eliminated k-th), or null to
+// choose one: ordering 1 minimum degree, 2 minimum fill (kNrOrderMinFill)
+constexpr int kNrOrderMinDegree = 1, kNrOrderMinFill = 2;
 void build_nr_symbolic(NrSymbolic& s, int n_bus, const int32_t* y_rowptr, const int32_t* y_col,
                        int n_theta, const int32_t* theta_block, int n_q, const int32_t* q_block,
-                       const int32_t* perm_in);
+                       const int32_t* perm_in, int ordering = kNrOrderMinFill);
 
 }  // namespace acpf

@@ -28,7 +28,7 @@ ZB_CONVERGED, ZB_MAX_ITER, ZB_FLOOR = range(3)
 
 EXPORTED = (
     "acpf_last_error", "acpf_abi_version", "acpf_device_count",
-    "acpf_nr_plan_create", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
+    "acpf_nr_plan_create", "acpf_nr_ordering", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
     "acpf_nr_plan_structure",
     "acpf_nr_solve", "acpf_nr_solve_start", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
@@ -88,6 +88,7 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_abi_version": (I32, []),
         "acpf_device_count": (I32, []),
         "acpf_nr_plan_create": (I32, [I32, I32, P, P, P, P, I32, P, I32, P, P, P, P, P]),
+        "acpf_nr_ordering": (I32, [I32, P, P, I32, P, I32, P]),
         "acpf_nr_analyze": (I32, [I32, P, P, I32, P, I32, P, P, P]),
         "acpf_nr_flat_start_solve": (I32, [I32, P, P, P, P, I32, P, I32, P, P, P, P, P, P]),
         "acpf_nr_plan_info_get": (I32, [P, P]),
@@ -162,6 +163,24 @@ def _stream_ptr(stream, like=None) -> int | None:
             return int(torch.cuda.current_stream(like.device).cuda_stream) or None
         return None
     return int(getattr(stream, "cuda_stream", stream))
+
+
+ORDER_MIN_DEGREE, ORDER_MIN_FILL = 1, 2  # include/acpf.h ACPF_ORDER_*
+
+
+def nr_ordering(y_csr, theta_block, kind: int = ORDER_MIN_FILL) -> np.ndarray:
+    """Native fill-reducing elimination order of the 2x2 bus blocks
+    (acpf_nr_ordering, host only): perm[k] = theta-block index of the bus
+    eliminated k-th."""
+    lib = load_library()
+    y = y_csr.tocsr()
+    y.sort_indices()
+    rowptr = np.ascontiguousarray(y.indptr, dtype=np.int32)
+    col = np.ascontiguousarray(y.indices, dtype=np.int32)
+    tb = np.ascontiguousarray(theta_block, dtype=np.int32)
+    out = np.empty(tb.size, dtype=np.int32)
+    _check(lib.acpf_nr_ordering(y.shape[0], _ptr(rowptr), _ptr(col), tb.size, _ptr(tb), int(kind), _ptr(out)))
+    return out
 
 
 def nr_analyze(y_csr, theta_block, q_block, perm=None) -> dict:

@@ -111,7 +111,7 @@ class TransmissionModel:
     net: TransmissionNetwork
     y: AdmittanceMatrix
     part: BusPartition
-    ordering: str = "mmd"
+    ordering: str = "minfill"
     _plans: dict = field(default_factory=dict, repr=False)
 
     def plan(self, device: int = 0, slot: int = 0):
@@ -122,12 +122,9 @@ class TransmissionModel:
         p = self._plans.get(key)
         if p is None:
             st = flat_start(self.net, self.part)
-            if self.ordering == "mmd":
-                perm = self._plans.get("_perm")
-                if perm is None:
-                    perm = self._plans["_perm"] = jacobian_ordering(self)
-            else:
-                perm = None
+            perm = self._plans.get("_perm")
+            if perm is None:
+                perm = self._plans["_perm"] = jacobian_ordering(self)
             p = engine.NrPlan(self.y.csr, self.part.theta_block, self.part.q_block, st.theta,
                               st.vmag, device=device, perm=perm)
             self._plans[key] = p
@@ -135,11 +132,12 @@ class TransmissionModel:
 
 
 def build_transmission_model(net: TransmissionNetwork, epsilon: float = 1e-6,
-                             ordering: str = "mmd") -> TransmissionModel:
-    """Y-bus + partition (reference :146-160). ``ordering``: 'mmd' (SuperLU's
-    MMD on A^T+A, the survey's pinned structure) or 'md' (built-in C++
-    minimum degree)."""
-    if ordering not in ("mmd", "md"):
+                             ordering: str = "minfill") -> TransmissionModel:
+    """Y-bus + partition (reference :146-160). ``ordering`` of the sparse LU:
+    'minfill' (native minimum fill, the default: fewest block updates),
+    'md' (native minimum degree) or 'mmd' (SuperLU's MMD on A^T+A, the
+    structure SURVEY.md pins the roofline's nnz_LU to)."""
+    if ordering not in ("minfill", "md", "mmd"):
         raise ValueError(f"unknown ordering {ordering!r}")
     return TransmissionModel(net=net, y=build_ybus(net), part=partition_buses(net),
                              ordering=ordering)
@@ -180,13 +178,19 @@ def bus_pattern(model: TransmissionModel):
 
 
 def jacobian_ordering(model: TransmissionModel) -> np.ndarray:
-    """MMD(A^T + A) ordering of the non-slack bus graph (host, once).
+    """Fill-reducing ordering of the non-slack bus graph (host, once).
 
     The engine factors the Jacobian as a matrix of 2x2 bus blocks
-    [theta_i, V_i], so the fill-reducing ordering is computed on buses. Only
-    the permutation is taken from SuperLU; the factorisation runs on the
-    device. perm[k] = theta-block position of the bus eliminated k-th.
+    [theta_i, V_i], so the ordering is computed on buses: the native greedy
+    minimum fill / minimum degree of libacpf (acpf_nr_ordering), or, for
+    ``ordering='mmd'``, SuperLU's MMD(A^T + A) permutation (only the
+    permutation is taken from SuperLU; the factorisation runs on the device).
+    perm[k] = theta-block position of the bus eliminated k-th.
     """
+    if model.ordering in ("minfill", "md"):
+        from . import engine
+        kind = engine.ORDER_MIN_FILL if model.ordering == "minfill" else engine.ORDER_MIN_DEGREE
+        return engine.nr_ordering(model.y.csr, model.part.theta_block, kind)
     import scipy.sparse as sp
     import scipy.sparse.linalg as spl
     j = bus_pattern(model)

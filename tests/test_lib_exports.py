@@ -45,16 +45,28 @@ def test_abi_version_and_errors():
     assert lib.acpf_zbus_plan_destroy(None) == 0
 
 
-@pytest.mark.parametrize("case,expect", [("gb2224", 24273), ("case118", 807)])
-def test_symbolic_analysis_host_only(case, expect):
-    m = pf.build_transmission_model(load_transmission(case))
+@pytest.mark.parametrize("case,expect,minfill", [("gb2224", 24273, (23165, 109233)),
+                                                  ("case118", 807, (807, 1551))])
+def test_symbolic_analysis_host_only(case, expect, minfill):
+    m = pf.build_transmission_model(load_transmission(case), ordering="mmd")
     perm = tx.jacobian_ordering(m)
     info = engine.nr_analyze(m.y.csr, m.part.theta_block, m.part.q_block, perm)
-    # 2x2-block factor over the non-slack buses
+    # 2x2-block factor over the non-slack buses; MMD: the SURVEY-pinned size
     assert info["n_j"] == m.part.n_theta
     assert info["nnz_lu"] == expect
+    # the default (native minimum fill): no more fill, fewer block updates
+    mf = pf.build_transmission_model(load_transmission(case))
+    pmf = tx.jacobian_ordering(mf)
+    assert sorted(pmf.tolist()) == list(range(m.part.n_theta))
+    imf = engine.nr_analyze(mf.y.csr, mf.part.theta_block, mf.part.q_block, pmf)
+    assert (imf["nnz_lu"], imf["n_pairs"]) == minfill
+    assert imf["n_pairs"] <= info["n_pairs"] * 1.01
     built_in = engine.nr_analyze(m.y.csr, m.part.theta_block, m.part.q_block, None)
-    assert built_in["nnz_lu"] < 1.05 * expect
+    assert built_in["nnz_lu"] == imf["nnz_lu"]
+    md = engine.nr_ordering(m.y.csr, m.part.theta_block, engine.ORDER_MIN_DEGREE)
+    assert engine.nr_analyze(m.y.csr, m.part.theta_block, m.part.q_block, md)["nnz_lu"] < 1.05 * expect
+    with pytest.raises(engine.EngineError):
+        engine.nr_ordering(m.y.csr, m.part.theta_block, 7)
     with pytest.raises(engine.EngineError):
         engine.nr_analyze(m.y.csr, m.part.theta_block, m.part.q_block, np.zeros_like(perm))
 

@@ -11,7 +11,8 @@ from paper_2605_14103_b200.fixtures import load_transmission  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 net = load_transmission('gb2224')
-m = pf.build_transmission_model(net)
+import os
+m = pf.build_transmission_model(net, ordering=os.environ.get('ACPF_PROBE_ORDER', 'minfill'))
 base = pf.transmission_base(net, m.part)
 plan = m.plan()
 pt, qt = plan.scenarios(base, 10010, 0, B, 0.2, device=0)
