@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
          "-I", str(ROOT / "include"), "-Xptxas", "-v"]
-LIBS = ["-lcusolver", "-lcublas"]
+LIBS = ["-lcusolver"]
 
 
 def sources() -> list:

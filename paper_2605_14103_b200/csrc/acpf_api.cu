@@ -5,7 +5,6 @@
 // chunking when the batch would not fit the device workspace, staging host
 // buffers through device memory when ACPF_HOST_PTRS is given.
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -132,7 +131,6 @@ struct acpf_nr_plan {
   DevArena cert_arena;
   GmModel gm{};                         // acpf_nr_plan_set_fd (binv1 null: not set)
   DevArena gm_arena;
-  void* cublas = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
@@ -1150,7 +1148,6 @@ acpf_status acpf_nr_plan_destroy(acpf_nr_plan_t p) {
       if (p->ev_d2h[k]) cudaEventDestroy(p->ev_d2h[k]);
     }
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
-    if (p->cublas) cublasDestroy((cublasHandle_t)p->cublas);
     p->graphs.release();
     if (p->graphs.capture) cudaStreamDestroy(p->graphs.capture);
     if (p->host_active) cudaFreeHost(p->host_active);
@@ -1954,14 +1951,6 @@ acpf_status acpf_nr_plan_set_fd(acpf_nr_plan_t p, const double* bprime_inv, cons
   up(const_cast<int32_t**>(&g.g_col), g_col, (size_t)gnnz);
   up(const_cast<double**>(&g.g_val), g_val, (size_t)gnnz);
   ACPF_CUDA(e);
-  if (!p->cublas) {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
-      set_error("acpf_nr_plan_set_fd: cublasCreate failed");
-      return ACPF_ECUDA;
-    }
-    p->cublas = h;
-  }
   p->gm = g;
   return ACPF_OK;
 }
@@ -1985,7 +1974,6 @@ acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t p, int64_t batch, const double* p
   if (batch == 0) return ACPF_OK;
   DeviceGuard dg(p->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  cublasSetStream((cublasHandle_t)p->cublas, st);
   const GmModel& m = p->gm;
   const int mm = std::min<int>(restart, std::max(1, m.nj));  // m = min(restart, n) (sparse.py:262)
   const int bc = (int)std::min<int64_t>(batch, std::max<int64_t>(32, env_int("ACPF_GMRES_CHUNK", 4096)));
@@ -2096,7 +2084,7 @@ acpf_status acpf_nr_solve_gmres(acpf_nr_plan_t p, int64_t batch, const double* p
       w.q_spec = sq;
     }
     if (err == cudaSuccess)
-      err = gmres_newton(m, w, p->cublas, nb, tol_mismatch, max_newton, gmres_tol, mm, max_outer, precond == 1, st);
+      err = gmres_newton(m, w, nb, tol_mismatch, max_newton, gmres_tol, mm, max_outer, precond == 1, st);
     auto o = [&](auto* user, auto* stage, int64_t per) { return dev_ptrs ? (user ? user + s0 * per : nullptr) : (user ? stage : nullptr); };
     if (err == cudaSuccess)
       err = gmres_output(m, w, nb, max_newton, o(theta_out, sth, (int64_t)nbus), o(vmag_out, svm, (int64_t)nbus),

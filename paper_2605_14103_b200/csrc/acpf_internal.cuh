@@ -302,7 +302,7 @@ struct GmWork {
 };
 
 size_t gmres_work_doubles(const GmModel& m, int bc, int restart);
-cudaError_t gmres_newton(const GmModel& m, GmWork& w, void* cublas, int64_t nb, double tol, int max_newton,
+cudaError_t gmres_newton(const GmModel& m, GmWork& w, int64_t nb, double tol, int max_newton,
                          double gtol, int restart, int max_outer, bool fd, cudaStream_t st);
 cudaError_t gmres_output(const GmModel& m, const GmWork& w, int64_t nb, int max_newton, double* theta_out,
                          double* vmag_out, uint8_t* converged, int32_t* iterations, double* fnorm,

@@ -13,15 +13,16 @@
 // Batched form: every vector is [rows][Bc] with the Bc scenarios of a chunk
 // fastest, so per-row work is coalesced across scenarios and the two dense
 // preconditioner solves of all scenarios are two GEMMs against the explicit
-// inverses of the shared FD matrices (cuBLAS DGEMM). Each scenario runs its
+// inverses of the shared FD matrices, on the FP64 tensor cores (fd_gemm_kernel,
+// DMMA). Each scenario runs its
 // own GMRES (own Krylov basis, Hessenberg, Givens rotations, own iteration
 // count and convergence), masked in lockstep kernels; dot products are
 // fixed-order two-phase reductions, so results do not depend on the batch.
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -39,6 +40,142 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 unsigned blocks_for(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
+
+// ---- FD solves: C[M][N] = A[M][K] B[K][N] (row-major, FP64) on DMMA ----
+// A = (B' + eps I)^-1 or (B'' + eps I)^-1 (shared by every scenario), B the
+// chunk's scaled residuals [rows][Bc]. CTA tile BM x BN, K steps of 16
+// through a 3-stage cp.async ring; warps of WM x WN mma.m8n8k4 accumulator
+// tiles. Small CTAs (64 x 64, 4 warps of 32 x 32) so that several are
+// resident per SM: their independent DMMA streams keep the FP64 tensor pipe
+// busy and the grid splits into many short waves. Shared rows are padded
+// (A BK+4, B BN+4 doubles) so the fragment loads of a half-warp hit 16
+// distinct 8-byte bank pairs. Edges are zero-filled (cp.async src-size 0),
+// so any M, N, K and unaligned leading dimensions work. Each output element
+// is one fixed-order sum, independent of the batch and of the grid.
+constexpr int kGBK = 16, kGStages = 3;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 8 : 0)
+               : "memory");
+}
+
+template <int BM, int BN, int WM, int WN>
+struct GemmCfg {
+  static constexpr int kWarpsN = BN / (8 * WN);
+  static constexpr int kThreads = 32 * (BM / (8 * WM)) * kWarpsN;
+  static constexpr int kLdA = kGBK + 4, kLdB = BN + 4;
+  static constexpr int kStageA = BM * kLdA, kStageB = kGBK * kLdB;
+  static constexpr size_t kSmem = (size_t)kGStages * (kStageA + kStageB) * sizeof(double);
+};
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN>::kThreads, GemmCfg<BM, BN, WM, WN>::kThreads <= 128 ? 4 : 1)
+    fd_gemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda, const double* __restrict__ B,
+                   int ldb, double* __restrict__ C, int ldc) {
+  using G = GemmCfg<BM, BN, WM, WN>;
+  constexpr int T = G::kThreads;
+  extern __shared__ __align__(16) double gsm[];
+  double* const As = gsm;
+  double* const Bs = gsm + kGStages * G::kStageA;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / G::kWarpsN, wn = warp % G::kWarpsN;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (K + kGBK - 1) / kGBK;
+  auto load = [&](int stage, int kt) {
+    const int k0 = kt * kGBK;
+    double* const as = As + stage * G::kStageA;
+    double* const bs = Bs + stage * G::kStageB;
+#pragma unroll
+    for (int i = 0; i < BM * kGBK / T; ++i) {
+      const int e = tid + T * i, r = e / kGBK, c = e % kGBK;
+      const bool ok = m0 + r < M && k0 + c < K;
+      cp_async8(as + r * G::kLdA + c, ok ? A + (size_t)(m0 + r) * lda + k0 + c : A, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < kGBK * BN / T; ++i) {
+      const int e = tid + T * i, r = e / BN, c = e % BN;
+      const bool ok = k0 + r < K && n0 + c < N;
+      cp_async8(bs + r * G::kLdB + c, ok ? B + (size_t)(k0 + r) * ldb + n0 + c : B, ok);
+    }
+  };
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < kGStages - 1; ++s) {
+    if (s < nk) load(s, s);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  const int ar = wm * 8 * WM + (lane >> 2), ac = lane & 3;      // A fragment: row, k
+  const int br = lane & 3, bcol = wn * 8 * WN + (lane >> 2);   // B fragment: k, column
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kGStages - 2) : "memory");
+    __syncthreads();
+    if (kt + kGStages - 1 < nk) load((kt + kGStages - 1) % kGStages, kt + kGStages - 1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const double* const as = As + (kt % kGStages) * G::kStageA;
+    const double* const bs = Bs + (kt % kGStages) * G::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < kGBK; kk += 4) {
+      double a[WM], b[WN];
+#pragma unroll
+      for (int i = 0; i < WM; ++i) a[i] = as[(ar + 8 * i) * G::kLdA + kk + ac];
+#pragma unroll
+      for (int j = 0; j < WN; ++j) b[j] = bs[(kk + br) * G::kLdB + bcol + 8 * j];
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+              : "d"(a[i]), "d"(b[j]));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  const int cr = m0 + wm * 8 * WM + (lane >> 2), cc = n0 + wn * 8 * WN + 2 * (lane & 3);
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    const int r = cr + 8 * i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < WN; ++j) {
+      const int c = cc + 8 * j;
+      double* const dst = C + (size_t)r * ldc + c;
+      if (c + 1 < N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < N) dst[0] = acc[i][j][0];
+        if (c + 1 < N) dst[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN>
+cudaError_t fd_gemm_launch(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C,
+                           int ldc, cudaStream_t st) {
+  using G = GemmCfg<BM, BN, WM, WN>;
+  static cudaError_t attr = cudaFuncSetAttribute(fd_gemm_kernel<BM, BN, WM, WN>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
+  if (attr != cudaSuccess) return attr;
+  const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  fd_gemm_kernel<BM, BN, WM, WN><<<grid, G::kThreads, G::kSmem, st>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  return cudaGetLastError();
+}
+
+// ACPF_FD_GEMM_TILE: 0 (default) 64 x 64 CTAs of 4 warps; 1 128 x 128 of 8 warps
+cudaError_t fd_gemm(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                    cudaStream_t st) {
+  static const int tile = [] {
+    const char* v = std::getenv("ACPF_FD_GEMM_TILE");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (tile == 1) return fd_gemm_launch<128, 128, 8, 4>(M, N, K, A, lda, B, ldb, C, ldc, st);
+  return fd_gemm_launch<64, 64, 4, 4>(M, N, K, A, lda, B, ldb, C, ldc, st);
+}
 
 // ---- state: u = V e^{j th}, phase = e^{j th}, I = Y u; mismatch F packed
 // [th block: P - p_spec; q block: Q - q_spec]; ||F||inf and flags per scenario
@@ -432,9 +569,8 @@ cudaError_t gmres_output(const GmModel& m, const GmWork& w, int64_t nb, int max_
 
 // The whole GMRES-Newton solve of one chunk (host loop; one 4-byte D2H per
 // Newton step and per GMRES iteration for the active counts).
-cudaError_t gmres_newton(const GmModel& m, GmWork& w, void* cublas, int64_t nb, double tol, int max_newton,
+cudaError_t gmres_newton(const GmModel& m, GmWork& w, int64_t nb, double tol, int max_newton,
                          double gtol, int restart, int max_outer, bool fd, cudaStream_t st) {
-  cublasHandle_t hb = (cublasHandle_t)cublas;
   const int bc = w.bc, nj = m.nj, mm = restart;
   const int64_t nbus_b = (int64_t)m.n_bus * bc, nj_b = (int64_t)nj * bc;
   const int nchunk = (nj + kDotChunk - 1) / kDotChunk;
@@ -457,20 +593,15 @@ cudaError_t gmres_newton(const GmModel& m, GmWork& w, void* cublas, int64_t nb, 
       gm_copy<<<blocks_for(nj_b), kT, 0, st>>>(nj_b, in, out);
       return cudaGetLastError();
     }
-    const double one = 1.0, zero = 0.0;
     gm_scale_th<<<blocks_for((int64_t)m.n_theta * bc), kT, 0, st>>>(m, w, in, w.t2, mask);
-    // column-major view: [rows][Bc] is a Bc x rows matrix; Z = T Binv^T
-    if (m.n_theta &&
-        cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, bc, m.n_theta, m.n_theta, &one, w.t2, bc, m.binv1, m.n_theta,
-                    &zero, out, bc) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
-    if (m.n_q) {
+    // z_th[n_theta][Bc] = B'^-1 t, z_q = B''^-1 ((r_q - G z_th) / V_q)
+    cudaError_t r = cudaSuccess;
+    if (m.n_theta) r = fd_gemm(m.n_theta, bc, m.n_theta, m.binv1, m.n_theta, w.t2, bc, out, bc, st);
+    if (r == cudaSuccess && m.n_q) {
       gm_couple_q<<<blocks_for((int64_t)m.n_q * bc), kT, 0, st>>>(m, w, in, out, w.t2, mask);
-      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, bc, m.n_q, m.n_q, &one, w.t2, bc, m.binv2, m.n_q, &zero,
-                      out + (size_t)m.n_theta * bc, bc) != CUBLAS_STATUS_SUCCESS)
-        return cudaErrorUnknown;
+      r = fd_gemm(m.n_q, bc, m.n_q, m.binv2, m.n_q, w.t2, bc, out + (size_t)m.n_theta * bc, bc, st);
     }
-    return cudaGetLastError();
+    return r == cudaSuccess ? cudaGetLastError() : r;
   };
   auto op = [&](const double* v, double* out, const int* mask) {
     gm_jvp_du<<<blocks_for(nbus_b), kT, 0, st>>>(m, w, v, mask);

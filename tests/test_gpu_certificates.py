@@ -1,4 +1,10 @@
-"""On-device certificates vs the host restatements.
+"""On-device certificates vs the reference and the host.
+
+Reference anchor: tests/golden/cert.npz (tools/make_golden_certs.py) holds
+the real reference's mismatch, branch_flows, calc_injections and
+kirchhoff_residual at fixed converged and perturbed states; the device
+certificates are evaluated at exactly those states
+(test_*_certificates_match_reference).
 
 NR: acpf_nr_certify's ||F||inf, slack power balance and branch loss against
 the host `mismatch` / `branch_flows` (reference transmission.py:202-215,
@@ -18,6 +24,39 @@ from paper_2605_14103_b200 import transmission as tm
 from paper_2605_14103_b200.fixtures import load_distribution, load_transmission
 
 pytestmark = pytest.mark.gpu
+
+
+def _split(g, prefix):
+    return {k.split("__", 1)[1]: v for k, v in g.items() if k.startswith(prefix + "__")}
+
+
+@pytest.mark.parametrize("name", ["case118", "gb2224"])
+def test_nr_certificates_match_reference(name, golden):
+    d = _split(golden("cert"), f"nr_{name}")
+    model = pf.build_transmission_model(load_transmission(name))
+    plan = model.plan()
+    plan.set_branches(model.net)
+    p, q = np.ascontiguousarray(d["p_spec"]), np.ascontiguousarray(d["q_spec"])
+    cert = plan.certify(np.ascontiguousarray(d["theta"]), np.ascontiguousarray(d["vmag"]), p, q)
+    # sums of O(|Y| |u|^2) terms in a different order: rounding-level agreement
+    np.testing.assert_allclose(cert["mismatch_inf"], d["mismatch_inf"], rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(cert["branch_loss"], d["branch_loss"], rtol=1e-11, atol=1e-12)
+    ref_balance = d["p_slack"] - ((d["branch_loss"] + d["shunt_loss"]) - p.sum(axis=1))
+    np.testing.assert_allclose(cert["slack_balance"], ref_balance, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["ieee13", "ieee123", "eulv"])
+def test_zbus_kirchhoff_matches_reference(name, golden):
+    d = _split(golden("cert"), f"zb_{name}")
+    model = pf.build_zbus_model(load_distribution(name))
+    plan = engine.zbus_plan_for(model)
+    plan.set_network(model)
+    kcl = plan.kirchhoff(np.ascontiguousarray(d["v"]), np.ascontiguousarray(d["s_wye"]),
+                         np.ascontiguousarray(d["s_delta"]))
+    # converged states sit at rounding noise (~1e-11, sums of O(|Y| |v|)
+    # terms in another order); the perturbed ones are O(1e-3..1e2)
+    np.testing.assert_allclose(kcl, d["kirchhoff"], rtol=1e-10, atol=1e-10)
+    assert (d["kirchhoff"][d["v"].shape[0] // 2:] > 1e-6).all()
 
 
 @pytest.mark.parametrize("name", ["case118", "gb2224"])
