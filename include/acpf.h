@@ -119,6 +119,34 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
                                 const double* vmag_init, const int32_t* perm,
                                 acpf_nr_plan_t* out);
 
+/* Host-only (no device): native model build, bit-identical
+ * to the reference's NumPy/SciPy assembly: CSR with sorted columns, exact
+ * 0+0j entries absent, duplicates summed in the reference's order. Call
+ * with capacity 0 (arrays may be NULL) to get *nnz, then again with
+ * capacity >= *nnz and rowptr[n+1], col/re/im[capacity].
+ *
+ * acpf_ybus_build: pi-model Ybus (network.py:450-496). Per branch k (bus
+ * INDICES from_idx/to_idx, in_service 0/1): series 1/(r + jx), charging
+ * b_ch, tap ratio and shift (rad); stamps (f,f) (y + j b/2)/tap^2,
+ * (t,t) y + j b/2, (f,t) -y/conj(a), (t,f) -y/a, a = tap e^{j shift}; then
+ * bus shunts gs + j bs. Zero parts are +0.0 (the reference's G + jB).
+ * ACPF_EINVAL for an in-service branch with r = x = 0 or tap = 0.           */
+acpf_status acpf_ybus_build(int32_t n_bus, int32_t n_branch, const int32_t* from_idx, const int32_t* to_idx,
+                            const double* r, const double* x, const double* b_ch, const double* tap,
+                            const double* shift, const uint8_t* in_service, const double* gs, const double* bs,
+                            int64_t capacity, int32_t* rowptr, int32_t* col, double* re, double* im,
+                            int64_t* nnz);
+
+/* acpf_y3_build: node-phase Y of a three-phase feeder (distribution.py:
+ * 356-391) from its primitive blocks in stamp order (per line y_ff, y_ft,
+ * y_tf, y_tt, then the shunts). Block b is k x k, k = block_ptr[b+1] -
+ * block_ptr[b]; its row node-phases are idx[2 block_ptr[b] ..][0..k), its
+ * column node-phases the next k; its values row-major complex (re, im
+ * interleaved) consecutively in val.                                        */
+acpf_status acpf_y3_build(int32_t n, int32_t n_blocks, const int32_t* block_ptr, const int32_t* idx,
+                          const double* val, int64_t capacity, int32_t* rowptr, int32_t* col, double* re,
+                          double* im, int64_t* nnz);
+
 /* Host-only (no device): a fill-reducing elimination order of the n_theta
  * block rows for acpf_nr_plan_create's `perm` (replaces the SciPy/SuperLU
  * MMD ordering a NumPy host would take; the reference factors dense,

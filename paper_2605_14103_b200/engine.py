@@ -28,7 +28,7 @@ ZB_CONVERGED, ZB_MAX_ITER, ZB_FLOOR = range(3)
 
 EXPORTED = (
     "acpf_last_error", "acpf_abi_version", "acpf_device_count",
-    "acpf_nr_plan_create", "acpf_nr_ordering", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
+    "acpf_nr_plan_create", "acpf_ybus_build", "acpf_y3_build", "acpf_nr_ordering", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
     "acpf_nr_plan_structure",
     "acpf_nr_solve", "acpf_nr_solve_start", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
@@ -89,6 +89,8 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_device_count": (I32, []),
         "acpf_nr_plan_create": (I32, [I32, I32, P, P, P, P, I32, P, I32, P, P, P, P, P]),
         "acpf_nr_ordering": (I32, [I32, P, P, I32, P, I32, P]),
+        "acpf_ybus_build": (I32, [I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P]),
+        "acpf_y3_build": (I32, [I32, I32, P, P, P, I64, P, P, P, P, P]),
         "acpf_nr_analyze": (I32, [I32, P, P, I32, P, I32, P, P, P]),
         "acpf_nr_flat_start_solve": (I32, [I32, P, P, P, P, I32, P, I32, P, P, P, P, P, P]),
         "acpf_nr_plan_info_get": (I32, [P, P]),
@@ -163,6 +165,54 @@ def _stream_ptr(stream, like=None) -> int | None:
             return int(torch.cuda.current_stream(like.device).cuda_stream) or None
         return None
     return int(getattr(stream, "cuda_stream", stream))
+
+
+def _csr_two_pass(call, n: int):
+    """Run a host-only CSR builder twice: size query, then fill."""
+    import scipy.sparse as sp
+    nnz = C.c_int64(0)
+    _check(call(0, None, None, None, None, C.byref(nnz)))
+    k = nnz.value
+    rp = np.empty(n + 1, dtype=np.int32)
+    col = np.empty(max(k, 1), dtype=np.int32)
+    re = np.empty(max(k, 1), dtype=np.float64)
+    im = np.empty(max(k, 1), dtype=np.float64)
+    _check(call(k, _ptr(rp), _ptr(col), _ptr(re), _ptr(im), C.byref(nnz)))
+    val = np.empty(k, dtype=np.complex128)
+    val.real, val.imag = re[:k], im[:k]
+    y = sp.csr_matrix((val, col[:k].copy(), rp), shape=(n, n))
+    y.has_sorted_indices = True
+    return y
+
+
+def ybus_build(n_bus: int, f, t, r, x, b_ch, tap, shift, in_service, gs, bs):
+    """Native pi-model Ybus (acpf_ybus_build, host only) -> complex CSR."""
+    lib = load_library()
+    a32 = lambda v: np.ascontiguousarray(v, dtype=np.int32)  # noqa: E731
+    f64 = lambda v: np.ascontiguousarray(v, dtype=np.float64)  # noqa: E731
+    f, t = a32(f), a32(t)
+    r, x, b_ch, tap, shift, gs, bs = map(f64, (r, x, b_ch, tap, shift, gs, bs))
+    on = np.ascontiguousarray(in_service, dtype=np.uint8)
+    return _csr_two_pass(lambda cap, rp, col, re, im, nz: lib.acpf_ybus_build(
+        n_bus, f.size, _ptr(f), _ptr(t), _ptr(r), _ptr(x), _ptr(b_ch), _ptr(tap), _ptr(shift), _ptr(on),
+        _ptr(gs), _ptr(bs), cap, rp, col, re, im, nz), n_bus)
+
+
+def y3_build(n: int, blocks):
+    """Native three-phase node-phase Y (acpf_y3_build, host only) from
+    (block k x k complex, row node-phases, column node-phases) in stamp order."""
+    lib = load_library()
+    blocks = list(blocks)
+    sizes = [len(r) for _, r, _ in blocks]
+    ptr = np.zeros(len(blocks) + 1, dtype=np.int32)
+    ptr[1:] = np.cumsum(sizes)
+    idx = np.ascontiguousarray(np.concatenate([np.concatenate([r, c]) for _, r, c in blocks])
+                               if blocks else np.zeros(0), dtype=np.int32)
+    val = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.complex128).ravel() for b, _, _ in blocks])
+                               if blocks else np.zeros(0, dtype=np.complex128)).view(np.float64)
+    return _csr_two_pass(lambda cap, rp, col, re, im, nz: lib.acpf_y3_build(
+        n, len(blocks), _ptr(ptr), _ptr(idx) if idx.size else None, _ptr(val) if val.size else None,
+        cap, rp, col, re, im, nz), n)
 
 
 ORDER_MIN_DEGREE, ORDER_MIN_FILL = 1, 2  # include/acpf.h ACPF_ORDER_*
