@@ -119,6 +119,39 @@ acpf_status acpf_nr_plan_create(int32_t device, int32_t n_bus, const int32_t* y_
                                 const double* vmag_init, const int32_t* perm,
                                 acpf_nr_plan_t* out);
 
+/* Host-only: native report emission, byte-identical to
+ * the reference's json.dumps(doc, indent=1) of the `solve` command's
+ * acpflow-solve-result/1 document (cli.py:141-180, embedding
+ * report_to_dict, batch.py:352-376) and to report_to_csv (batch.py:379-387).
+ * Written to `path` when non-NULL, else into out[capacity] with the byte
+ * count in *length (a first call with capacity 0 sizes the buffer).
+ *   errors[i]        NULL or the record's error text (UTF-8)
+ *   state_a/state_b  [count][n_state]: theta/vmag (kind "tx") or
+ *                    v_re/v_im (kind "dist"); has_solution[i] == 0 (or a
+ *                    NULL state) writes null lists (errored records)
+ *   node_phase_ids   dist only: the reduced node-phase labels            */
+typedef struct {
+  const char* case_name; /* "case": file name of the network             */
+  const char* kind;      /* "tx" | "dist"                                  */
+  int64_t seed;
+  double spread;
+  int64_t batch;
+  int64_t worker_count;
+  double total_wall_time;
+  double throughput;
+} acpf_result_meta;
+
+acpf_status acpf_solve_result_json(const acpf_result_meta* meta, int64_t count, const uint8_t* converged,
+                                   const int32_t* iterations, const double* residual, const double* wall_time,
+                                   const char* const* errors, int32_t n_state, const double* state_a,
+                                   const double* state_b, const uint8_t* has_solution, int32_t n_ids,
+                                   const char* const* node_phase_ids, const char* path, char* out,
+                                   int64_t capacity, int64_t* length);
+
+acpf_status acpf_report_csv(int64_t count, const uint8_t* converged, const int32_t* iterations,
+                            const double* residual, const double* wall_time, const char* const* errors,
+                            const char* path, char* out, int64_t capacity, int64_t* length);
+
 /* Host-only (no device): native model build, bit-identical
  * to the reference's NumPy/SciPy assembly: CSR with sorted columns, exact
  * 0+0j entries absent, duplicates summed in the reference's order. Call

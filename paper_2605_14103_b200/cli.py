@@ -109,33 +109,35 @@ def _solve_device(kind, model, base, seed, count, spread, tol, step="lu", precon
 
 
 def cmd_solve(args) -> int:
+    """`solve`: the device batch, then the acpflow-solve-result/1 document
+    (or the report CSV) written natively from the result arrays
+    (engine.solve_result_json / report_csv; reference cli.py:100-180)."""
+    from .results import NewtonResults, ZbusResults
     path, kind, model, base = _load(args)
     out, wall = _solve_device(kind, model, base, args.seed, args.batch, args.spread, args.tol, args.step,
                               args.precond)
-    results = (tm.results_from_arrays(out) if kind == "tx" else engine.zbus_results(model, out))
-    report = bm.report_from_results(results, wall)
+    res = NewtonResults(out) if kind == "tx" else ZbusResults(model, out)
+    n = len(res)
+    conv, its, resid, diag = res.converged(), res.iterations(), res.residuals(), res.diagnostics()
     if args.verbose:
-        print(f"{report.n_converged}/{len(results)} converged in {wall:.3f}s on the GPU",
-              file=sys.stderr)
+        print(f"{int(conv.sum())}/{n} converged in {wall:.3f}s on the GPU", file=sys.stderr)
+    share = wall / n
     if args.format == "csv":
-        payload = bm.report_to_csv(report)
+        payload = engine.report_csv(conv, its, resid, share, diag, path=args.out)
     else:
+        meta = {"case": Path(path).name, "kind": kind, "seed": args.seed, "spread": args.spread,
+                "batch": args.batch, "worker_count": 1, "total_wall_time": wall,
+                "throughput": n / wall if wall > 0 else float("inf")}
         if kind == "tx":
-            sols = [{"index": i, "theta": list(r.state.theta), "vmag": list(r.state.vmag)}
-                    for i, r in enumerate(results)]
+            a, b, ids = out["theta"], out["vmag"], None
         else:
-            sols = {"node_phase_ids": model.reduced_ids(),
-                    "records": [{"index": i, "v_re": list(r.v.real), "v_im": list(r.v.imag)}
-                                for i, r in enumerate(results)]}
-        payload = json.dumps({"schema": "acpflow-solve-result/1", "case": Path(path).name,
-                              "kind": kind, "seed": args.seed, "spread": args.spread,
-                              "batch": args.batch, "report": bm.report_to_dict(report),
-                              "solutions": sols}, indent=1) + "\n"
-    if args.out:
-        Path(args.out).write_text(payload, encoding="utf-8")
-    else:
+            v = np.asarray(out["v"])
+            a, b, ids = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag), model.reduced_ids()
+        payload = engine.solve_result_json(meta, conv, its, resid, share, diag, a, b,
+                                           node_phase_ids=ids, path=args.out)
+    if not args.out:
         sys.stdout.write(payload)
-    return EXIT_OK if report.n_converged == len(results) else EXIT_NUMERICAL
+    return EXIT_OK if bool(conv.all()) else EXIT_NUMERICAL
 
 
 def cmd_bench(args) -> int:

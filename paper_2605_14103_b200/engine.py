@@ -28,7 +28,7 @@ ZB_CONVERGED, ZB_MAX_ITER, ZB_FLOOR = range(3)
 
 EXPORTED = (
     "acpf_last_error", "acpf_abi_version", "acpf_device_count",
-    "acpf_nr_plan_create", "acpf_ybus_build", "acpf_y3_build", "acpf_nr_ordering", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
+    "acpf_nr_plan_create", "acpf_solve_result_json", "acpf_report_csv", "acpf_ybus_build", "acpf_y3_build", "acpf_nr_ordering", "acpf_nr_analyze", "acpf_nr_flat_start_solve", "acpf_nr_plan_info_get",
     "acpf_nr_plan_structure",
     "acpf_nr_solve", "acpf_nr_solve_start", "acpf_nr_last_timing", "acpf_nr_plan_destroy",
     "acpf_zbus_plan_create", "acpf_zbus_solve", "acpf_zbus_last_timing",
@@ -89,6 +89,9 @@ def load_library(path: str | os.PathLike | None = None):
         "acpf_device_count": (I32, []),
         "acpf_nr_plan_create": (I32, [I32, I32, P, P, P, P, I32, P, I32, P, P, P, P, P]),
         "acpf_nr_ordering": (I32, [I32, P, P, I32, P, I32, P]),
+        "acpf_solve_result_json": (I32, [P, I64, P, P, P, P, P, I32, P, P, P, I32, P, C.c_char_p, P, I64,
+                                          P]),
+        "acpf_report_csv": (I32, [I64, P, P, P, P, P, C.c_char_p, P, I64, P]),
         "acpf_ybus_build": (I32, [I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P]),
         "acpf_y3_build": (I32, [I32, I32, P, P, P, I64, P, P, P, P, P]),
         "acpf_nr_analyze": (I32, [I32, P, P, I32, P, I32, P, P, P]),
@@ -165,6 +168,77 @@ def _stream_ptr(stream, like=None) -> int | None:
             return int(torch.cuda.current_stream(like.device).cuda_stream) or None
         return None
     return int(getattr(stream, "cuda_stream", stream))
+
+
+class ResultMeta(C.Structure):
+    _fields_ = [("case_name", C.c_char_p), ("kind", C.c_char_p), ("seed", C.c_int64), ("spread", C.c_double),
+                ("batch", C.c_int64), ("worker_count", C.c_int64), ("total_wall_time", C.c_double),
+                ("throughput", C.c_double)]
+
+
+def _report_arrays(converged, iterations, residual, wall_time, errors):
+    n = len(converged)
+    conv = np.ascontiguousarray(converged, dtype=np.uint8)
+    its = np.ascontiguousarray(iterations, dtype=np.int32)
+    res = np.ascontiguousarray(residual, dtype=np.float64)
+    wall = np.ascontiguousarray(np.broadcast_to(np.asarray(wall_time, dtype=np.float64), (n,)))
+    errs = None
+    keep = []
+    if errors is not None and any(e is not None for e in errors):
+        errs = (C.c_char_p * n)()
+        for k, e in enumerate(errors):
+            if e is not None:
+                b = str(e).encode("utf-8", "surrogatepass")
+                keep.append(b)
+                errs[k] = b
+    return n, conv, its, res, wall, errs, keep
+
+
+def _text_out(call, path):
+    """path -> written file (returns None); no path -> the text, sized first."""
+    if path is not None:
+        _check(call(str(path).encode(), None, 0, None))
+        return None
+    n = C.c_int64(0)
+    _check(call(None, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(call(None, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value].decode("utf-8")
+
+
+def solve_result_json(meta: dict, converged, iterations, residual, wall_time, errors=None, state_a=None,
+                      state_b=None, has_solution=None, node_phase_ids=None, path=None):
+    """acpflow-solve-result/1 document written natively (acpf_solve_result_json):
+    byte-identical to json.dumps(doc, indent=1) + "\n" of the reference's
+    `solve` (cli.py:141-180). state_a/state_b: [count][n] theta/vmag (tx) or
+    v_re/v_im (dist)."""
+    lib = load_library()
+    n, conv, its, res, wall, errs, keep = _report_arrays(converged, iterations, residual, wall_time, errors)
+    m = ResultMeta(str(meta["case"]).encode(), str(meta["kind"]).encode(), int(meta["seed"]),
+                   float(meta["spread"]), int(meta["batch"]), int(meta.get("worker_count", 1)),
+                   float(meta["total_wall_time"]), float(meta["throughput"]))
+    a = None if state_a is None else np.ascontiguousarray(state_a, dtype=np.float64)
+    b = None if state_b is None else np.ascontiguousarray(state_b, dtype=np.float64)
+    ns = 0 if a is None else (a.shape[1] if a.ndim == 2 else 0)
+    has = None if has_solution is None else np.ascontiguousarray(has_solution, dtype=np.uint8)
+    ids = None
+    if node_phase_ids is not None:
+        enc = [str(x).encode("utf-8") for x in node_phase_ids]
+        keep.extend(enc)
+        ids = (C.c_char_p * max(len(enc), 1))(*enc)
+    n_ids = 0 if node_phase_ids is None else len(node_phase_ids)
+    return _text_out(lambda pth, out, cap, ln: lib.acpf_solve_result_json(
+        C.byref(m), n, _ptr(conv), _ptr(its), _ptr(res), _ptr(wall), errs, ns, _ptr(a), _ptr(b), _ptr(has),
+        n_ids, ids, pth, out, cap, ln), path)
+
+
+def report_csv(converged, iterations, residual, wall_time, errors=None, path=None):
+    """report_to_csv written natively (acpf_report_csv), byte-identical to the
+    reference's batch.py:379-387."""
+    lib = load_library()
+    n, conv, its, res, wall, errs, keep = _report_arrays(converged, iterations, residual, wall_time, errors)
+    return _text_out(lambda pth, out, cap, ln: lib.acpf_report_csv(
+        n, _ptr(conv), _ptr(its), _ptr(res), _ptr(wall), errs, pth, out, cap, ln), path)
 
 
 def _csr_two_pass(call, n: int):

@@ -57,3 +57,22 @@ def test_step_option_validated():
         tm.NewtonOptions(step="cg")
     with pytest.raises(SystemExit):
         cli.build_parser().parse_args(["solve", "--case", "case14", "--step", "cg"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,batch", [("case118", 16), ("ieee13", 32)])
+def test_solve_document_is_python_json(case, batch, tmp_path):
+    """The natively written solve-result document (acpf_solve_result_json)
+    re-serialises to the same bytes under the reference's json.dumps(indent=1)
+    (cli.py:154): every float is repr-exact, the layout is json's."""
+    out = tmp_path / "r.json"
+    assert cli.main(["solve", "--case", case, "--batch", str(batch), "--seed", "1010", "--out", str(out)]) == 0
+    text = out.read_text(encoding="utf-8")
+    doc = json.loads(text)
+    assert json.dumps(doc, indent=1) + "\n" == text
+    assert doc["report"]["aggregate"]["count"] == batch
+    csv = tmp_path / "r.csv"
+    assert cli.main(["solve", "--case", case, "--batch", str(batch), "--seed", "1010", "--format", "csv",
+                     "--out", str(csv)]) == 0
+    rows = csv.read_text().splitlines()
+    assert rows[0] == "index,converged,iterations,residual,error,wall_time" and len(rows) == batch + 1
