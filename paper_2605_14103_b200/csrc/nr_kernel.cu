@@ -1215,8 +1215,9 @@ size_t nr_group_state_bytes() { return kGroup * (8 + 4 + 4 + 4 + 8 + 1) + 4; }
 namespace {
 
 template <class Q>
-void launch_tail_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t units,
+void launch_tail_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t groups,
                        cudaStream_t stream) {
+  const int64_t units = (groups + Q::NG - 1) / Q::NG;
   for (int c = 0; c < hs.n_tail_class; ++c) {  // one launch per row-buffer class, group-major
     const int k0 = hs.tail_class_ptr[c], nt = hs.tail_class_ptr[c + 1] - k0;
     nr_factor_kernel<Q><<<(unsigned)(units * nt), 32, Q::smem_bytes() + (size_t)hs.tail_class_maxl[c] * Q::kSlot,
@@ -1228,11 +1229,12 @@ template <class P>
 void launch_factor_level(const NrDeviceModel& m, const NrHostSchedule& hs, const NrWorkspace& w, int64_t units,
                          int l, cudaStream_t stream) {
   if (l == hs.tail_level) {
+    const int64_t groups = units * P::NG;  // the unit count of the tail's own pipe
     switch (hs.tail_variant) {
-      case 0: launch_tail_level<V0>(m, hs, w, units, stream); break;
-      case 1: launch_tail_level<V1>(m, hs, w, units, stream); break;
-      case 2: launch_tail_level<V2>(m, hs, w, units, stream); break;
-      default: launch_tail_level<V3>(m, hs, w, units, stream); break;
+      case 0: launch_tail_level<V0>(m, hs, w, groups, stream); break;
+      case 1: launch_tail_level<V1>(m, hs, w, groups, stream); break;
+      case 2: launch_tail_level<V2>(m, hs, w, groups, stream); break;
+      default: launch_tail_level<V3>(m, hs, w, groups, stream); break;
     }
     return;
   }
@@ -1309,7 +1311,10 @@ cudaError_t launch_nr_newton(const NrDeviceModel& m_in, const NrHostSchedule& hs
       return cudaFuncSetAttribute(nr_factor_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(Q::smem_bytes() + (size_t)cap * Q::kSlot));
     };
-    e = hs.tail_variant == 0 ? attr(V0{}) : hs.tail_variant == 1 ? attr(V1{}) : hs.tail_variant == 2 ? attr(V2{}) : attr(V3{});
+    e = hs.tail_variant == 0   ? attr(V0{})
+        : hs.tail_variant == 1 ? attr(V1{})
+        : hs.tail_variant == 2 ? attr(V2{})
+                               : attr(V3{});
     if (e != cudaSuccess) return e;
   }
   const int64_t groups = (io.batch + kGroup - 1) / kGroup;
