@@ -6,7 +6,8 @@ import json
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-# profiles/fp64_peak_r1.txt: DMMA m8n8k4 best of three configurations
+# profiles/r2/fp64_peak_r2_clocks.txt: DMMA m8n8k4 best configuration, 5 runs at
+# 1965 MHz (clock record alongside; r1: profiles/fp64_peak_r1.txt, same value)
 FP64_DMMA_TFLOPS = 37.09
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
 
@@ -20,4 +21,4 @@ def hbm_gbs() -> tuple:
 
 
 def fp64_tflops() -> tuple:
-    return FP64_DMMA_TFLOPS, "measured DMMA f64 (profiles/fp64_peak_r1.txt)"
+    return FP64_DMMA_TFLOPS, "measured DMMA f64 at 1965 MHz (profiles/r2/fp64_peak_r2_clocks.txt)"
