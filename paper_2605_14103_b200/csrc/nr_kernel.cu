@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
 #ifndef ACPF_JAC_MINB
 #define ACPF_JAC_MINB 8
 #endif
+#ifndef ACPF_JAC_UNROLL
+#define ACPF_JAC_UNROLL 2
+#endif
 __global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDeviceModel m, NrWorkspace w) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -408,24 +411,47 @@ __global__ void __launch_bounds__(128, ACPF_JAC_MINB) nr_jacobian_kernel(NrDevic
     int dslot = -1;
     double2 dy = make_double2(0.0, 0.0);
     const int a0 = __ldg(m.asm_ptr + i), a1 = __ldg(m.asm_ptr + i + 1);
-    for (int a = a0; a < a1; ++a) {
-      const int slot = __ldg(m.asm_slot + a);
-      const double2 y = __ldg(m.asm_y + a);
-      const int jb = __ldg(m.asm_j + a);
-      const double2 uj = ld2(su, jb);
+    // one assembly entry: I_i accumulation, then the off-diagonal block
+    auto entry = [&](int slot, double2 y, int jb, double2 uj, double vj, int qj) {
       acc.x += y.x * uj.x - y.y * uj.y;
       acc.y += y.x * uj.y + y.y * uj.x;
       if (jb == i) {
         dslot = slot;
         dy = y;
-        continue;
+        return;
       }
-      if (slot < 0) continue;  // slack column
+      if (slot < 0) return;  // slack column
       // u_i conj(y E_j) = u_i conj(y u_j) / V_j (V_j real): no E gather
       const double2 wt = mul_conj(u, cmul(y, uj));
-      const double rv = ACPF_INV_V(uj, jb);
+      const double rv = 1.0 / vj;
       const double2 wv = make_double2(wt.x * rv, wt.y * rv);
-      put(slot, make_double2(wt.y, -wt.x), wv, pq, __ldg(m.qidx + jb) >= 0, false);
+      put(slot, make_double2(wt.y, -wt.x), wv, pq, qj >= 0, false);
+    };
+    // ACPF_JAC_UNROLL entries' gathers (u_j, V_j) in flight before any is
+    // used: the kernel waits on these loads (long_scoreboard); same
+    // arithmetic order as one entry at a time
+    int a = a0;
+    constexpr int U = ACPF_JAC_UNROLL;
+    for (; a + U <= a1; a += U) {
+      int sl[U], jj[U], qq[U];
+      double2 yy[U], uu[U];
+      double vv[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) sl[k] = __ldg(m.asm_slot + a + k), jj[k] = __ldg(m.asm_j + a + k);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        yy[k] = __ldg(m.asm_y + a + k);
+        uu[k] = ld2(su, jj[k]);
+        vv[k] = __ldg(svm + (size_t)jj[k] * kGroup);
+        qq[k] = __ldg(m.qidx + jj[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) entry(sl[k], yy[k], jj[k], uu[k], vv[k], qq[k]);
+    }
+    for (; a < a1; ++a) {
+      const int j0 = __ldg(m.asm_j + a);
+      entry(__ldg(m.asm_slot + a), __ldg(m.asm_y + a), j0, ld2(su, j0), __ldg(svm + (size_t)j0 * kGroup),
+            __ldg(m.qidx + j0));
     }
     if (dslot >= 0) {
       const double rv = ACPF_INV_V(u, i);
