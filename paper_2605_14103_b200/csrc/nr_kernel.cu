@@ -304,6 +304,9 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   if (neg) atomicOr(&w.flags[g * kGroup + sc], 4);
 }
 
+#ifndef ACPF_MIS_UNROLL
+#define ACPF_MIS_UNROLL 2  // 2.87 -> 2.75 ms per launch (4: 2.80; 64 registers: 3.1)
+#endif
 #ifndef ACPF_MIS_MINB
 #define ACPF_MIS_MINB 12  // 40 registers, 48 resident warps/SM: 9.0 -> 8.1 ms per launch (16: spills, 10.0 ms)
 #endif
@@ -334,7 +337,24 @@ __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDevic
     } else {
       double2 acc = make_double2(0.0, 0.0);
       const int e1 = __ldg(m.y_rowptr + i + 1);
-      for (int e = __ldg(m.y_rowptr + i); e < e1; ++e) {
+      int e = __ldg(m.y_rowptr + i);
+#if ACPF_MIS_UNROLL > 1
+      // ACPF_MIS_UNROLL gathers in flight, summed in order (same rounding)
+      for (; e + ACPF_MIS_UNROLL <= e1; e += ACPF_MIS_UNROLL) {
+        int c[ACPF_MIS_UNROLL];
+        double2 y[ACPF_MIS_UNROLL], uj[ACPF_MIS_UNROLL];
+#pragma unroll
+        for (int k = 0; k < ACPF_MIS_UNROLL; ++k) c[k] = __ldg(m.y_col + e + k);
+#pragma unroll
+        for (int k = 0; k < ACPF_MIS_UNROLL; ++k) y[k] = __ldg(m.y_val + e + k), uj[k] = ld2(su, c[k]);
+#pragma unroll
+        for (int k = 0; k < ACPF_MIS_UNROLL; ++k) {
+          acc.x += y[k].x * uj[k].x - y[k].y * uj[k].y;
+          acc.y += y[k].x * uj[k].y + y[k].y * uj[k].x;
+        }
+      }
+#endif
+      for (; e < e1; ++e) {
         const double2 y = __ldg(m.y_val + e);
         const double2 uj = ld2(su, __ldg(m.y_col + e));
         acc.x += y.x * uj.x - y.y * uj.y;
@@ -874,7 +894,18 @@ __global__ void __launch_bounds__(128) nr_shared_step_kernel(NrDeviceModel m, Nr
   for (int p = 0; p < m.n_rows; ++p) {
     const int t0 = __ldg(m.row_slot + p), td = __ldg(m.sh_diag + p);
     double acc = half ? 0.0 : yx[(size_t)p * kBlk + i];
-    for (int t = t0 + half; t < td; t += 2) {
+    // this half's slots t, t + 2 loaded together (the row is a chain of
+    // dependent index -> value loads); the sum keeps its order
+    int t = t0 + half;
+    for (; t + 2 < td; t += 4) {
+      const int c0 = __ldg(m.sh_col + t), c1 = __ldg(m.sh_col + t + 2);
+      const double2 l0 = __ldg(rows + 2 * t + i), l1 = __ldg(rows + 2 * (t + 2) + i);
+      const double2 y0 = *reinterpret_cast<const double2*>(yx + (size_t)c0 * kBlk);
+      const double2 y1 = *reinterpret_cast<const double2*>(yx + (size_t)c1 * kBlk);
+      acc = fma(-l0.y, y0.y, fma(-l0.x, y0.x, acc));
+      acc = fma(-l1.y, y1.y, fma(-l1.x, y1.x, acc));
+    }
+    if (t < td) {
       const int c = __ldg(m.sh_col + t);
       const double2 l = __ldg(rows + 2 * t + i);
       const double2 y = *reinterpret_cast<const double2*>(yx + (size_t)c * kBlk);
@@ -890,7 +921,16 @@ __global__ void __launch_bounds__(128) nr_shared_step_kernel(NrDeviceModel m, Nr
   for (int p = m.n_rows - 1; p >= 0; --p) {
     const int td = __ldg(m.sh_diag + p), t1 = __ldg(m.row_slot + p + 1);
     double part = 0.0;
-    for (int t = td + 1 + half; t < t1; t += 2) {
+    int t = td + 1 + half;
+    for (; t + 2 < t1; t += 4) {
+      const int c0 = __ldg(m.sh_col + t), c1 = __ldg(m.sh_col + t + 2);
+      const double2 u0 = __ldg(rows + 2 * t + i), u1 = __ldg(rows + 2 * (t + 2) + i);
+      const double2 x0 = *reinterpret_cast<const double2*>(yx + (size_t)c0 * kBlk);
+      const double2 x1 = *reinterpret_cast<const double2*>(yx + (size_t)c1 * kBlk);
+      part = fma(u0.y, x0.y, fma(u0.x, x0.x, part));
+      part = fma(u1.y, x1.y, fma(u1.x, x1.x, part));
+    }
+    if (t < t1) {
       const int c = __ldg(m.sh_col + t);
       const double2 u = __ldg(rows + 2 * t + i);
       const double2 x = *reinterpret_cast<const double2*>(yx + (size_t)c * kBlk);
