@@ -604,6 +604,10 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
   int32_t wstore = ts0 + lane < ts1 ? m.slot_store[ts0 + lane] : 0;
   int32_t nstore = ts0 + 32 + lane < ts1 ? m.slot_store[ts0 + 32 + lane] : 0;
   int t = ts0;
+  // control and store words of the slot about to run, fetched one slot ahead
+  // (the shuffle is off the slot's critical path)
+  uint32_t cur_info = __shfl_sync(kFull, winfo, 0);
+  int32_t cur_store = __shfl_sync(kFull, wstore, 0);
   for (int p = p0; p < p1; ++p) {
     const int t0 = t;
     pp.ensure(pp.q);
@@ -616,14 +620,17 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
     ++pp.q;
     double ir0[NG], ir1[NG];  // row i of inv(U_pp), set at the diagonal slot
     for (;; ++t) {
-      if (t - tw == 32) {
+      const uint32_t info = cur_info;
+      const int32_t stv = cur_store;
+      if (t + 1 - tw == 32) {
         tw += 32;
         winfo = ninfo;
         wstore = nstore;
         ninfo = tw + 32 + lane < ts1 ? m.slot_info[tw + 32 + lane] : 0u;
         nstore = tw + 32 + lane < ts1 ? m.slot_store[tw + 32 + lane] : 0;
       }
-      const uint32_t info = __shfl_sync(kFull, winfo, t - tw);
+      cur_info = __shfl_sync(kFull, winfo, (t + 1 - tw) & 31);
+      cur_store = __shfl_sync(kFull, wstore, (t + 1 - tw) & 31);
       const int cnt = (int)(info >> 16);
       double a[NG], a2[NG], a3[NG], a4[NG];
 #pragma unroll
@@ -691,12 +698,12 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
       } else if (info & kSlotTail) {
         // tail row, tail column: A_pt minus the non-tail updates, stored raw
         // for the dense tail factorisation (nr_tail_kernel)
-        const size_t st = (size_t)(uint32_t)__shfl_sync(kFull, wstore, t - tw) * kBlk;
+        const size_t st = (size_t)(uint32_t)stv * kBlk;
 #pragma unroll
         for (int h = 0; h < NG; ++h)
           if ((live >> h) & 1u) luw[h * gstride + st] = a[h];
       } else {
-        const size_t st = (size_t)(uint32_t)__shfl_sync(kFull, wstore, t - tw) * kBlk;
+        const size_t st = (size_t)(uint32_t)stv * kBlk;
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
           if (info & kSlotDiag) {
