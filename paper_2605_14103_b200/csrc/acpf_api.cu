@@ -715,7 +715,9 @@ static acpf_status nr_solve_lanes(acpf_nr_plan* p, int64_t batch, int64_t chunk,
   // two lanes take alternate chunks and end up with equal shares
   std::vector<int64_t> cbeg;
   {
-    const int64_t edge = ((std::min(chunk, batch / 8) + kGroup - 1) / kGroup) * kGroup;
+    // ACPF_NR_EDGE_DIV: edge chunk = B / div (10: 314-315 ms on the device timeline at 65,536 vs 322-325 for 8)
+    static const int64_t edge_div = std::max<int64_t>(2, env_int("ACPF_NR_EDGE_DIV", 10));
+    const int64_t edge = ((std::min(chunk, batch / edge_div) + kGroup - 1) / kGroup) * kGroup;
     if (batch > 2 * chunk || edge < 1024 || env_int("ACPF_NR_EDGE_CHUNKS", 1) == 0) {
       for (int64_t s0 = 0; s0 < batch; s0 += chunk) cbeg.push_back(s0);
     } else {  // [edge, (B - 2 edge) / 2, (B - 2 edge) / 2, edge]
