@@ -158,8 +158,9 @@ template <int BM, int BN, int WM, int WN>
 cudaError_t fd_gemm_launch(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C,
                            int ldc, cudaStream_t st) {
   using G = GemmCfg<BM, BN, WM, WN>;
-  static cudaError_t attr = cudaFuncSetAttribute(fd_gemm_kernel<BM, BN, WM, WN>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
+  // per call, not cached: the attribute belongs to the current device's context
+  const cudaError_t attr = cudaFuncSetAttribute(fd_gemm_kernel<BM, BN, WM, WN>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
   if (attr != cudaSuccess) return attr;
   const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
   fd_gemm_kernel<BM, BN, WM, WN><<<grid, G::kThreads, G::kSmem, st>>>(M, N, K, A, lda, B, ldb, C, ldc);

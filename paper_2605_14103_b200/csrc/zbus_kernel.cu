@@ -31,6 +31,9 @@
 #include "acpf_internal.cuh"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace acpf {
 
@@ -758,10 +761,17 @@ cudaError_t launch_ntc(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, 
 // clusters of CL CTAs that can be resident at once (clusters live inside a GPC)
 template <int NT, int CL>
 int resident_clusters(size_t smem, int sms) {
-  static size_t cached_smem = 0;  // the answer depends on the feeder's shared memory
-  static int cached = 0;
-  if (cached != 0 && cached_smem == smem) return cached > 0 ? cached : 0;
-  cached_smem = smem;
+  // cached per (device, shared memory of the feeder); plans on several
+  // devices are driven from concurrent host threads
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto it = cache.find({dev, smem});
+    if (it != cache.end()) return it->second;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
@@ -778,7 +788,8 @@ int resident_clusters(size_t smem, int sms) {
     cudaGetLastError();
     n = 0;  // no cluster launch possible: one CTA per tile
   }
-  cached = n > 0 ? n : -1;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{dev, smem}] = n;
   return n;
 }
 
