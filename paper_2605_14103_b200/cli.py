@@ -122,8 +122,19 @@ def cmd_solve(args) -> int:
     if args.verbose:
         print(f"{int(conv.sum())}/{n} converged in {wall:.3f}s on the GPU", file=sys.stderr)
     share = wall / n
+    # no --out: the native writer streams to stdout (the document of a large
+    # batch never exists as one Python string)
+    target = args.out
+    if target is None:
+        try:  # a real descriptor (not an in-process redirect such as a test's capture)
+            fd = sys.stdout.fileno()
+        except (AttributeError, OSError, ValueError):
+            fd = None
+        if fd is not None and Path(f"/dev/fd/{fd}").exists():
+            sys.stdout.flush()
+            target = f"/dev/fd/{fd}"
     if args.format == "csv":
-        payload = engine.report_csv(conv, its, resid, share, diag, path=args.out)
+        payload = engine.report_csv(conv, its, resid, share, diag, path=target)
     else:
         meta = {"case": Path(path).name, "kind": kind, "seed": args.seed, "spread": args.spread,
                 "batch": args.batch, "worker_count": 1, "total_wall_time": wall,
@@ -134,8 +145,8 @@ def cmd_solve(args) -> int:
             v = np.asarray(out["v"])
             a, b, ids = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag), model.reduced_ids()
         payload = engine.solve_result_json(meta, conv, its, resid, share, diag, a, b,
-                                           node_phase_ids=ids, path=args.out)
-    if not args.out:
+                                           node_phase_ids=ids, path=target)
+    if payload is not None:
         sys.stdout.write(payload)
     return EXIT_OK if bool(conv.all()) else EXIT_NUMERICAL
 
