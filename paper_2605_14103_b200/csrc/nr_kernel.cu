@@ -980,12 +980,17 @@ __global__ void __launch_bounds__(128) nr_shared_step_kernel(NrDeviceModel m, Nr
 //   (d) every warp below the panel updates its accumulators with two DMMAs
 //       per column tile: C -= L^(rows, panel) U^(panel, columns).
 // Pivot blocks are checked for exact zero like the sparse kernel (flag 8).
-constexpr int kTW = 16;           // warps: one 8-row strip each
+constexpr int kTW = 2 * kTailMaxRows / 8;  // warps: one 8-row strip each
 constexpr int kTRows = 2 * kTailMaxRows;  // 128 scalar rows
 constexpr int kTYCol = kTRows;    // the right-hand side column
 constexpr int kTTiles = kTRows / 8 + 1;
-constexpr int kTLd = 148;         // U row stride: 148 = 4 (mod 16), conflict-free B fragments (4 rows x 8 cols)
+// U row stride >= 8 kTTiles, = 4 (mod 16): conflict-free B fragments (4 rows x 8 cols)
+constexpr int kTLd = ((8 * (2 * kTailMaxRows / 8 + 1) + 11) / 16) * 16 + 4;
 constexpr int kTPcLd = 12;        // panel-column stride: conflict-free A fragments (8 rows x 4 cols)
+// (c): threads [0, kTColThreads) solve the panel row's columns (at most
+// kTRows - 8 plus y), the rest the rows below the panel (at most kTRows - 8)
+constexpr int kTColThreads = ((kTRows - 7 + 31) / 32) * 32;
+static_assert(kTW * 32 - kTColThreads >= kTRows - 8, "dense tail: too few threads for the panel solves");
 constexpr size_t kTailSmem = ((size_t)kTRows * kTLd + (size_t)kTRows * kTPcLd + 16 * 16 + 2 * kTRows) * 8 + 16;
 
 __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double b) {
@@ -1086,27 +1091,28 @@ __device__ __forceinline__ void tail_diag_block(double* Dg, double* dinv, int la
   }
 }
 
-#define ACPF_TAIL_PANEL_SWITCH(p, CALL) \
-  switch (p) {                          \
-    case 0: CALL(0); break;             \
-    case 1: CALL(1); break;             \
-    case 2: CALL(2); break;             \
-    case 3: CALL(3); break;             \
-    case 4: CALL(4); break;             \
-    case 5: CALL(5); break;             \
-    case 6: CALL(6); break;             \
-    case 7: CALL(7); break;             \
-    case 8: CALL(8); break;             \
-    case 9: CALL(9); break;             \
-    case 10: CALL(10); break;           \
-    case 11: CALL(11); break;           \
-    case 12: CALL(12); break;           \
-    case 13: CALL(13); break;           \
-    case 14: CALL(14); break;           \
-    default: CALL(15); break;           \
+// panel index -> template constant (panels 0 .. kTW-1; a panel past the tail's
+// tiles maps to the last one and never runs)
+#define ACPF_TAIL_PANEL_CASE(P, CALL) \
+  case P:                              \
+    CALL((P < kTW ? P : kTW - 1));     \
+    break;
+#define ACPF_TAIL_PANEL_SWITCH(p, CALL)                                                           \
+  switch (p) {                                                                                    \
+    ACPF_TAIL_PANEL_CASE(0, CALL) ACPF_TAIL_PANEL_CASE(1, CALL) ACPF_TAIL_PANEL_CASE(2, CALL)     \
+    ACPF_TAIL_PANEL_CASE(3, CALL) ACPF_TAIL_PANEL_CASE(4, CALL) ACPF_TAIL_PANEL_CASE(5, CALL)     \
+    ACPF_TAIL_PANEL_CASE(6, CALL) ACPF_TAIL_PANEL_CASE(7, CALL) ACPF_TAIL_PANEL_CASE(8, CALL)     \
+    ACPF_TAIL_PANEL_CASE(9, CALL) ACPF_TAIL_PANEL_CASE(10, CALL) ACPF_TAIL_PANEL_CASE(11, CALL)   \
+    ACPF_TAIL_PANEL_CASE(12, CALL) ACPF_TAIL_PANEL_CASE(13, CALL) ACPF_TAIL_PANEL_CASE(14, CALL)  \
+    default:                                                                                      \
+      CALL((15 < kTW ? 15 : kTW - 1));                                                            \
+      break;                                                                                      \
   }
 
-__global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, NrWorkspace w) {
+#ifndef ACPF_TAIL_MINB
+#define ACPF_TAIL_MINB (kTailMaxRows <= 48 ? 2 : 1)  // CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(kTW * 32, ACPF_TAIL_MINB) nr_tail_kernel(NrDeviceModel m, NrWorkspace w) {
   extern __shared__ __align__(16) double tsm[];
   double* const U = tsm;                  // [kTRows][kTLd]
   double* const Pc = U + kTRows * kTLd;   // [kTRows][kTPcLd]
@@ -1191,7 +1197,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) nr_tail_kernel(NrDeviceModel m, N
 #pragma unroll
         for (int r = 0; r < 8; ++r) Dg[r * kTLd + (c - r0)] = x[r];
       }
-      const int t = tid - 256;
+      const int t = tid - kTColThreads;
       if (t >= 0 && t < ncol) {
         double* const row = Pc + (r0 + 8 + t) * kTPcLd;
         double x[8];

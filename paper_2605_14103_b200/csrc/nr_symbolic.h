@@ -92,7 +92,15 @@ constexpr uint32_t kSlotRowEnd = 1u << 6;
 constexpr uint32_t kSlotL = 1u << 8;
 constexpr uint32_t kSlotFill = 1u << 9;
 constexpr uint32_t kSlotTail = 1u << 10;  // tail-column slot of a tail row: store the partial value raw
-constexpr int kTailMaxRows = 64;          // 2 x 64 scalar rows: one DMMA strip of 8 rows per warp
+#ifndef ACPF_TAIL_ROWS
+#define ACPF_TAIL_ROWS 44
+#endif
+// 2 x kTailMaxRows scalar rows: one DMMA strip of 8 rows per warp. 44 (11 warps,
+// 80 registers) lets two CTAs share an SM and overlap their latency-bound panel
+// chains; 64 (16 warps) filled the register file with one scenario. gb2224 x
+// 65,536: 64 -> 287.1 ms per solve, 48 -> 277.3, 44 -> 275.5, 40 -> 275.5,
+// 36 -> 279.7, 32 -> 279.0 (one run, profiles/r2/nr_tail_kernel_phases.txt)
+constexpr int kTailMaxRows = ACPF_TAIL_ROWS;
 
 // s: NrSymbolic built on the non-slack buses (n_theta = #non-slack, n_q = 0)
 void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32_t* y_col,
