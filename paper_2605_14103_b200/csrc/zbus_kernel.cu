@@ -43,17 +43,24 @@ namespace {
 #define ACPF_ZB_ROW_WARPS 8
 #endif
 // warps = kRowWarps (row slices of a 64-row block, kRowGroups 8-row DMMA groups
-// each) x kColWarps column slices; 32 warps (8 per SM sub-partition) let one
-// warp's epilogue overlap the DMMA stream of the others (measured: 8 warps
-// 1.58M, 16 warps 1.66M, 32 warps 1.72M EULV/s)
+// each) x kColWarps column slices. Round 1 measured 8 / 16 / 32 warps at
+// 1.58M / 1.66M / 1.72M EULV/s with 64-wide tiles; with 32-wide tiles 16 warps
+// (kColWarps = 2, each warp two 8-column DMMA tiles, 122 registers) is the
+// fastest shape at every batch size (round 2)
 constexpr int kRowWarps = ACPF_ZB_ROW_WARPS;
 constexpr int kRowGroups = 8 / kRowWarps;
 #ifndef ACPF_ZB_COL_WARPS
-#define ACPF_ZB_COL_WARPS 4
+#define ACPF_ZB_COL_WARPS 2  // 16 warps with 32-wide tiles (below): 141.4 -> 139.0 ms at 262,144, 3.00 -> 2.67 ms at 4,096
 #endif
 constexpr int kColWarps = ACPF_ZB_COL_WARPS;
 constexpr int kThreads = kRowWarps * kColWarps * 32;
-constexpr int kMaxKsPerStage = 16;  // k-steps (of 4) per Z stage
+#ifndef ACPF_ZB_STAGE_KS
+#define ACPF_ZB_STAGE_KS 16
+#endif
+constexpr int kMaxKsPerStage = ACPF_ZB_STAGE_KS;  // k-steps (of 4) per Z stage
+#ifndef ACPF_ZB_MINB
+#define ACPF_ZB_MINB 1  // CTAs per SM (persistent grid = ACPF_ZB_MINB x SMs)
+#endif
 // Row-block classes: the per-column sums of every pass are formed per class
 // (row blocks c, c + V, c + 2V, ... for c = 0..V-1, each in order) and the V
 // class partials are then added in class order. A batch too small to fill
@@ -573,7 +580,7 @@ __device__ __forceinline__ void zb_cluster_combine(double* colsum) {
 }
 
 template <int NT, int CL>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, ACPF_ZB_MINB)
     zbus_kernel(ZbDeviceModel m, ZbBatchIO io, double tol, int max_iter, int mag0_mode,
                 double* mag0_out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -822,7 +829,8 @@ cudaError_t launch_nt(const ZbDeviceModel& m, const ZbBatchIO& io, double tol, i
   if (rc > 0 && tiles <= (int64_t)(kZbVirt - 1) * rc)
     return launch_ntc<NT, kZbVirt>(m, io, tol, max_iter, mag0_mode, mag0_out, stream,
                                    (int)(tiles < rc ? tiles : rc), smem);
-  const int grid = (int)(tiles < sms ? tiles : sms);
+  const int64_t slots = (int64_t)sms * ACPF_ZB_MINB;
+  const int grid = (int)(tiles < slots ? tiles : slots);
   return launch_ntc<NT, 1>(m, io, tol, max_iter, mag0_mode, mag0_out, stream, grid, smem);
 }
 
@@ -859,7 +867,14 @@ cudaError_t launch_zbus(const ZbDeviceModel& m, const ZbBatchIO& io, double tol,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool small = !mag0_mode && (io.batch + 63) / 64 < sms;
-  if (m.kpad <= 64 && !small) return launch_nt<64>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
+  // ACPF_ZB_NT64=1: 64-wide tiles for large batches (the round-1 shape, with
+  // 32 warps: ACPF_ZB_COL_WARPS=4); 32-wide tiles on 16 warps measured faster
+  // at every batch size (122 registers, no spills; 64-wide at 16 warps spills)
+  static const bool nt64 = [] {
+    const char* v = std::getenv("ACPF_ZB_NT64");
+    return v && v[0] == '1';
+  }();
+  if (nt64 && m.kpad <= 64 && !small) return launch_nt<64>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
   return launch_nt<32>(m, io, tol, max_iter, mag0_mode, mag0_out, stream);
 }
 
