@@ -385,7 +385,7 @@ def zb_workload(args, dev, stream, local, case, seed, start, count, e2e=True, ro
         r["roofline"] = {"bound": "tensor", "achieved": zflops / zk / 1e12, "peak": fp, "unit": "TFLOP/s",
                          "frac": zflops / zk / 1e12 / fp,
                          "traffic": traffic_from_profiles("zbus_kernel", count),
-                         "kernel": "zbus_kernel<64>", "algorithmic_flops_per_launch": zflops,
+                         "kernel": "zbus_kernel<32> (16 warps)", "algorithmic_flops_per_launch": zflops,
                          "avg_launch_ms": zk * 1e3, "peak_source": fp_src,
                          "complex_product": "3-multiply (Zr(Ir+Ii), (Zr+Zi)Ii, (Zi-Zr)Ir)",
                          "dmma_executed_tflops": zexec / zk / 1e12, "dmma_executed_frac": zexec / zk / 1e12 / fp}
