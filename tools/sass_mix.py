@@ -16,7 +16,7 @@ KEYS = ["DMMA", "UBLKCP", "UTMALDG", "UTCHMMA", "LDGSTS", "SYNCS", "DFMA", "DMUL
         "LDS", "STS", "LDG", "STG", "SHFL", "BAR", "ATOMG", "RED"]
 HOT = ["zbus_kernel", "nr_factor_kernel", "nr_back_kernel", "nr_mismatch_kernel", "nr_jacobian_kernel",
        "nr_shared_step_kernel", "nr_phasor_kernel", "nr_tail_kernel", "nr_cond_kernel", "nr_scenarios",
-       "zb_scenarios", "nr_cert", "zb_kcl"]
+       "zb_scenarios", "nr_cert", "zb_kcl", "fd_gemm_kernel"]
 
 
 def main():
