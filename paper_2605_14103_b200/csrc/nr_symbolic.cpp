@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <stdexcept>
@@ -524,7 +525,20 @@ void build_nr_schedule(const NrSymbolic& s, const int32_t* y_rowptr, const int32
     std::vector<int> nl(nr, 0);
     for (int p = n0; p < nr; ++p)
       for (int64_t t = s.rowptr[p]; t < s.diag[p]; ++t) nl[p] += s.col[t] < n0 ? 1 : 0;
-    const int bounds[] = {16, 32, 48, 64, 1 << 30};
+    // row-buffer class bounds (L blocks); ACPF_NR_TAIL_CLASSES="b1,b2,..." overrides
+    std::vector<int> bounds = {16, 32, 48, 64};
+    if (const char* env = std::getenv("ACPF_NR_TAIL_CLASSES")) {
+      bounds.clear();
+      for (const char* c = env; *c;) {
+        char* end = nullptr;
+        const long v = std::strtol(c, &end, 10);
+        if (end == c) break;
+        if (v > 0) bounds.push_back((int)v);
+        c = (*end == ',') ? end + 1 : end;
+      }
+      std::sort(bounds.begin(), bounds.end());
+    }
+    bounds.push_back(1 << 30);
     int lo = -1;
     for (int hi : bounds) {
       int mx = 0;
