@@ -308,7 +308,7 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
 #define ACPF_MIS_UNROLL 2  // 2.87 -> 2.75 ms per launch (4: 2.80; 64 registers: 3.1)
 #endif
 #ifndef ACPF_MIS_MINB
-#define ACPF_MIS_MINB 12  // 40 registers, 48 resident warps/SM: 9.0 -> 8.1 ms per launch (16: spills, 10.0 ms)
+#define ACPF_MIS_MINB 16  // 32 registers, 64 resident warps/SM: 2.76 -> 2.52 ms per launch with the two-deep gathers (round 1, one-deep: 12 beat 16)
 #endif
 __global__ void __launch_bounds__(128, ACPF_MIS_MINB) nr_mismatch_kernel(NrDeviceModel m, NrWorkspace w) {
   const int lane = threadIdx.x & 31, r = lane >> 3, sc = lane & 7;
