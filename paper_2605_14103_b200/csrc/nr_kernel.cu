@@ -282,25 +282,47 @@ __global__ void nr_phasor_kernel(NrDeviceModel m, NrWorkspace w) {
   const bool upd = k > 0 && w.active[g * kGroup + sc];
   bool neg = false;
   if (k == 0 && m.sh_s0) return;  // flat start: S_i shared (nr_mismatch_kernel), V > 0 checked on the host
-  for (int i = i0 + r; i < i1; i += 4) {
-    double t = SL(gb.s, m.off_th + i), v = SL(gb.s, m.off_vm + i);
+  // one bus: loads (state, correction) separated from the update so that two
+  // buses' loads are in flight together (same arithmetic)
+  struct Bus {
+    double t, v, dt, dv;
+    int p;
+    bool q;
+  };
+  auto load = [&](int i) {
+    Bus b{SL(gb.s, m.off_th + i), SL(gb.s, m.off_vm + i), 0.0, 0.0, -1, false};
     if (upd) {
-      const int p = m.bus_row[i];
-      if (p >= 0) {
-        t = t + BL(gb.b, m.off_yx + p, 0);
-        SL(gb.s, m.off_th + i) = t;
-        if (m.qidx[i] >= 0) {
-          v = v + BL(gb.b, m.off_yx + p, 1);
-          SL(gb.s, m.off_vm + i) = v;
-        }
+      b.p = m.bus_row[i];
+      if (b.p >= 0) {
+        b.q = m.qidx[i] >= 0;
+        b.dt = BL(gb.b, m.off_yx + b.p, 0);
+        if (b.q) b.dv = BL(gb.b, m.off_yx + b.p, 1);
+      }
+    }
+    return b;
+  };
+  auto finish = [&](int i, Bus b) {
+    if (b.p >= 0) {
+      b.t = b.t + b.dt;
+      SL(gb.s, m.off_th + i) = b.t;
+      if (b.q) {
+        b.v = b.v + b.dv;
+        SL(gb.s, m.off_vm + i) = b.v;
       }
     }
     double sn, cs;
-    sincos(t, &sn, &cs);
-    SL(gb.s, m.off_u + 2 * i) = v * cs;
-    SL(gb.s, m.off_u + 2 * i + 1) = v * sn;
-    neg |= v <= 0.0;
+    sincos(b.t, &sn, &cs);
+    SL(gb.s, m.off_u + 2 * i) = b.v * cs;
+    SL(gb.s, m.off_u + 2 * i + 1) = b.v * sn;
+    neg |= b.v <= 0.0;
+  };
+  int i = i0 + r;
+  for (; i + 4 < i1; i += 8) {
+    const Bus b0 = load(i), b1 = load(i + 4);
+    finish(i, b0);
+    finish(i + 4, b1);
   }
+  if (i < i1) finish(i, load(i));
   if (neg) atomicOr(&w.flags[g * kGroup + sc], 4);
 }
 
