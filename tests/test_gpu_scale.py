@@ -1,7 +1,7 @@
 """Parity at scale against the REAL reference (tools/make_golden_scale.py).
 
-4,096 GBnetwork scenarios (seed 10010) and 16,384 EULV scenarios (seed
-10011), generated on the device (bitwise the reference generator) and solved
+4,096 scenarios each of GBnetwork, case1354pegase and case118 (seed 10010) and
+16,384 each of EULV, IEEE123 and IEEE13 (seed 10011), generated on the device (bitwise the reference generator) and solved
 through the C-ABI: flags equal the reference's for every scenario, iteration
 counts equal except for stop-rule ties (tests/tiebands.py: reported, and only
 allowed where the reference's own decision value is within 1e-3 tol of tol),
@@ -21,11 +21,18 @@ from tiebands import check_iterations
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def gb():
-    net = load_transmission("gb2224")
+NR_CASES = {"gb2224": "gb2224", "case1354": "case1354pegase", "case118": "case118"}
+
+
+def _tx(name):
+    net = load_transmission(NR_CASES[name])
     model = pf.build_transmission_model(net)
     return model, pf.transmission_base(net, model.part)
+
+
+@pytest.fixture(scope="module")
+def gb():
+    return _tx("gb2224")
 
 
 def _nr_check(g, out, name):
@@ -44,13 +51,14 @@ def _nr_check(g, out, name):
     assert np.abs(vm[k] - g["vmag"][sel]).max() <= 1e-8
 
 
-def test_nr_4096_reference_scenarios(gb, golden):
-    g = golden("scale_nr_gb2224")
-    model, base = gb
+@pytest.mark.parametrize("name", list(NR_CASES))
+def test_nr_4096_reference_scenarios(name, golden):
+    g = golden(f"scale_nr_{name}")
+    model, base = _tx(name)
     plan = model.plan()
     p, q = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve(p, q, 1e-8, 20)
-    _nr_check(g, out, "NR gb2224 (LU step)")
+    _nr_check(g, out, f"NR {name} (LU step)")
     assert (out["final_mismatch_inf"] <= 1e-8).all()
 
 
@@ -65,15 +73,16 @@ def test_nr_gmres_step_4096_reference_scenarios(gb, golden):
     np.testing.assert_array_equal(out["gmres_steps"].sum(1), g["gmres_total"])
 
 
-def test_zbus_16384_reference_scenarios(golden):
-    g = golden("scale_zb_eulv")
-    model = pf.build_zbus_model(load_distribution("eulv"))
+@pytest.mark.parametrize("name", ["eulv", "ieee123", "ieee13"])
+def test_zbus_16384_reference_scenarios(name, golden):
+    g = golden(f"scale_zb_{name}")
+    model = pf.build_zbus_model(load_distribution(name))
     base = pf.distribution_base(model)
     plan = engine.zbus_plan_for(model)
     sw, sd = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve(sw, sd, 1e-9, 100)
     np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
-    ties = check_iterations("Z-Bus eulv", g["iterations"], out["iterations"], g["sweep_delta"], 1e-9, first=1)
+    ties = check_iterations(f"Z-Bus {name}", g["iterations"], out["iterations"], g["sweep_delta"], 1e-9, first=1)
     ok = np.setdiff1d(np.arange(g["iterations"].size), ties)
     va = np.abs(out["v"])
     assert np.abs(va.sum(1) - g["vabs_sum"])[ok].max() <= 1e-8 * va.shape[1]

@@ -5,6 +5,7 @@ iteration counts under its stop rules (distribution.py:674-679,
 transmission.py:353)."""
 
 import numpy as np
+import pytest
 
 from tiebands import BAND, classify, margins
 
@@ -21,8 +22,9 @@ def test_classify_separates_ties_from_real_mismatches():
     assert margins(ref, dec, tol) < BAND
 
 
-def test_scale_golden_zbus_decisions_reproduce_iterations(golden):
-    g = golden("scale_zb_eulv")
+@pytest.mark.parametrize("name", ["eulv", "ieee123", "ieee13"])
+def test_scale_golden_zbus_decisions_reproduce_iterations(name, golden):
+    g = golden(f"scale_zb_{name}")
     d, its = g["sweep_delta"], g["iterations"]
     tol = 1e-9
     for s in range(its.size):
@@ -33,8 +35,9 @@ def test_scale_golden_zbus_decisions_reproduce_iterations(golden):
     assert margins(its, d, tol) > 0
 
 
-def test_scale_golden_nr_decisions_reproduce_iterations(golden):
-    g = golden("scale_nr_gb2224")
+@pytest.mark.parametrize("name", ["gb2224", "case1354", "case118"])
+def test_scale_golden_nr_decisions_reproduce_iterations(name, golden):
+    g = golden(f"scale_nr_{name}")
     f, its = g["step_fnorm"], g["iterations"]
     for s in range(its.size):
         k = int(its[s])
