@@ -62,14 +62,15 @@ def test_nr_4096_reference_scenarios(name, golden):
     assert (out["final_mismatch_inf"] <= 1e-8).all()
 
 
-def test_nr_gmres_step_4096_reference_scenarios(gb, golden):
-    g = golden("scale_nr_gb2224")
-    model, base = gb
+@pytest.mark.parametrize("name", list(NR_CASES))
+def test_nr_gmres_step_4096_reference_scenarios(name, golden):
+    g = golden(f"scale_nr_{name}")
+    model, base = _tx(name)
     plan = model.plan()
     plan.set_fd(model.y.csr, model.part.theta_block, model.part.q_block, 1e-6)
     p, q = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), 0.2)
     out = plan.solve_gmres(p, q, 1e-8, 20)
-    _nr_check(g, out, "NR gb2224 (GMRES step)")
+    _nr_check(g, out, f"NR {name} (GMRES step)")
     np.testing.assert_array_equal(out["gmres_steps"].sum(1), g["gmres_total"])
 
 
