@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 
 import paper_2605_14103_b200 as pf
-from paper_2605_14103_b200.fixtures import load_transmission
+from paper_2605_14103_b200.fixtures import load_distribution, load_transmission
 from paper_2605_14103_b200.transmission import results_from_arrays
 
 from tiebands import check_iterations, classify, margins
@@ -97,3 +97,29 @@ def test_stress_batch_lu_step(golden):
     g = golden("stress_nr_case118")
     model, plan, p, q = _inputs(g)
     _check("NR case118 stress (LU step)", g, plan.solve(p, q, 1e-8, 20), exact_step=True)
+
+
+def test_stress_batch_zbus_ieee13(golden):
+    """16,384 IEEE13 scenarios at spread 0.9 scaled by factors in [1, 2.2): ~78%
+    converge after 9-100 sweeps, the rest run to max_iter = 100 (reference-run,
+    tools/make_golden_stress.py). Flags, sweep counts (stop-rule ties reported),
+    final deltas and, for the kept rows, v within 1e-8."""
+    from paper_2605_14103_b200 import engine
+    g = golden("stress_zb_ieee13")
+    model = pf.build_zbus_model(load_distribution("ieee13"))
+    base = pf.distribution_base(model)
+    plan = engine.zbus_plan_for(model)
+    sw, sd = plan.scenarios(base, int(g["seed"]), 0, int(g["count"]), float(g["spread"]))
+    f = np.asarray(g["factor"])[:, None]
+    sw, sd = np.ascontiguousarray(sw * f), np.ascontiguousarray(np.asarray(sd) * f)
+    out = plan.solve(sw, sd, 1e-9, 100)
+    np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
+    ties = check_iterations("Z-Bus ieee13 stress", g["iterations"], out["iterations"], g["sweep_delta"], 1e-9,
+                            first=1)
+    ok = np.setdiff1d(np.arange(g["iterations"].size), ties)
+    conv = g["converged"].astype(bool)
+    cok = ok[conv[ok]]
+    assert np.abs(out["final_delta"][cok] - g["final_delta"][cok]).max() <= 1e-10
+    k = np.setdiff1d(g["keep"], ties)
+    sel = np.searchsorted(g["keep"], k)
+    assert np.abs(out["v"][k] - g["v"][sel]).max() <= 1e-8

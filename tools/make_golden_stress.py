@@ -12,6 +12,12 @@ batch has to keep every scenario's own exit while its groups run on
 (tests/test_gpu_stress.py). Recorded: flags, iterations, diagnostics, final
 norms, the norm at every Newton check (stop-rule tie bands) and full states of
 every 32nd scenario.
+
+Z-Bus: 16,384 IEEE13 scenarios at spread 0.9 (seed 2606) scaled by factors in
+[1, 2.2): ~80% converge after 11-60+ sweeps, the rest run to max_iter = 100 --
+long runs with many stop decisions (recorded: |sum|v_k| - sum|v_k-1|| of every
+sweep, as tools/make_golden_scale.py), flags, iterations, final deltas and v
+of every 64th scenario.
 """
 
 from __future__ import annotations
@@ -76,7 +82,44 @@ def main() -> int:
     import collections
     print("converged", collections.Counter(conv), "iterations", sorted(collections.Counter(its).items()))
     print("diagnostics", collections.Counter(d[:40] for d in diag).most_common(5))
+    _zbus(ac)
     return 0
+
+
+def _zbus(ac) -> None:
+    from acpflow import distribution as dm
+    sys.path.insert(0, str(ROOT / "tools"))
+    from make_golden_failures import _DeltaRecorder
+    count, seed, spread, lo, hi = 16384, 2606, 0.9, 1.0, 2.2
+    txt = gzip.open(ROOT / "fixtures" / "ieee13.json.gz", "rt").read()
+    model = ac.build_zbus_model(ac.parse_distribution_json(txt))
+    base = ac.distribution_base(model)
+    mult = ac.generate_load_multipliers(ac.ScenarioSpec(count=count, seed=seed, spread=spread,
+                                                        target="distribution"), base.n_elements)
+    factor = lo + (hi - lo) * np.random.default_rng(seed).random(count)
+    conv, its, fdel, resid, vs, deltas = [], [], [], [], [], []
+    with _DeltaRecorder(dm) as rec:
+        for i in range(count):
+            sc = ac.apply_multipliers(base, mult[i])
+            sc = dm.DistributionScenario(sc.wye_s * factor[i], sc.delta_s * factor[i])
+            r, d = rec.run(ac, model, sc)
+            conv.append(r.converged)
+            its.append(r.iterations)
+            fdel.append(r.final_delta)
+            resid.append(r.residual_inf)
+            vs.append(r.v)
+            deltas.append(d)
+    m = max(len(x) for x in deltas)
+    sweep = np.full((count, m), np.nan)
+    for k, x in enumerate(deltas):
+        sweep[k, :len(x)] = x
+    keep = np.arange(0, count, 64)
+    np.savez_compressed(OUT / "stress_zb_ieee13.npz", seed=seed, spread=spread, count=count, factor=factor,
+                        converged=np.array(conv), iterations=np.array(its), final_delta=np.array(fdel),
+                        residual=np.array(resid), sweep_delta=sweep, keep=keep, v=np.array(vs)[keep])
+    import collections
+    print("Z-Bus converged", collections.Counter(conv), "iterations (min, max, #100)",
+          min(its), max(its), sum(1 for x in its if x == 100))
 
 
 if __name__ == "__main__":
