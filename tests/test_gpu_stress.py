@@ -123,3 +123,31 @@ def test_stress_batch_zbus_ieee13(golden):
     k = np.setdiff1d(g["keep"], ties)
     sel = np.searchsorted(g["keep"], k)
     assert np.abs(out["v"][k] - g["v"][sel]).max() <= 1e-8
+
+
+def test_warm_start_4096_reference_scenarios(golden):
+    """4,096 case1354 scenarios warm-started (newton_solve start=, flat_start=False,
+    transmission.py:306-330) from the base case's solution perturbed per
+    scenario (tools/make_golden_warm.py): flags, iterations (ties reported),
+    states of every 64th scenario within 1e-8."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    from make_golden_warm import warm_starts
+    g = golden("warm_nr_case1354")
+    net = load_transmission("case1354pegase")
+    model = pf.build_transmission_model(net)
+    base = pf.transmission_base(net, model.part)
+    plan = model.plan()
+    n = int(g["count"])
+    th0, vm0 = warm_starts(g["base_theta"], g["base_vmag"], model.part.slack, model.part.pq, n, int(g["wseed"]))
+    p, q = plan.scenarios(base, int(g["seed"]), 0, n, 0.2)
+    out = plan.solve(p, q, 1e-8, 20, theta_start=np.ascontiguousarray(th0), vmag_start=np.ascontiguousarray(vm0))
+    np.testing.assert_array_equal(out["converged"].astype(bool), g["converged"])
+    ties = check_iterations("NR case1354 warm starts", g["iterations"], out["iterations"], g["step_fnorm"], 1e-8,
+                            first=0)
+    assert (out["final_mismatch_inf"] <= 1e-8).all()
+    k = np.setdiff1d(g["keep"], ties)
+    sel = np.searchsorted(g["keep"], k)
+    assert np.abs(out["theta"][k] - g["theta"][sel]).max() <= 1e-8
+    assert np.abs(out["vmag"][k] - g["vmag"][sel]).max() <= 1e-8
