@@ -74,7 +74,10 @@ constexpr int kMaxKsPerStage = ACPF_ZB_STAGE_KS;  // k-steps (of 4) per Z stage
 #define ACPF_ZB_VIRT 4
 #endif
 constexpr int kZbVirt = ACPF_ZB_VIRT;
-constexpr int kZbBuf = 2;            // Z stage buffers (TMA ring; 4 x half-K stages measured 2% slower)
+#ifndef ACPF_ZB_BUF
+#define ACPF_ZB_BUF 2
+#endif
+constexpr int kZbBuf = ACPF_ZB_BUF;  // Z stage buffers (TMA ring; 4 x half-K stages measured 2% slower)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
