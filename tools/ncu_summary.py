@@ -5,7 +5,8 @@ import csv, io, subprocess, sys
 def raw(rep):
     out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return [dict(zip(rows[0], r)) for r in rows[2:]]
+    units = dict(zip(rows[0], rows[1]))  # ncu scales each metric's unit per report (ms/us, GB/MB, ...)
+    return [dict(zip(rows[0], r), _units=units) for r in rows[2:]]
 
 KEYS = ['gpu__time_duration.sum', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
         'gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed',
@@ -20,7 +21,7 @@ for d in raw(sys.argv[1]):
     print(d.get('Kernel Name', '')[:90])
     for k in KEYS:
         if k in d:
-            print(f'  {k:70s} {d[k]}')
+            print(f'  {k:70s} {d[k]} {d["_units"].get(k, "")}')
     st = {k: float(d[k]) for k in d if k.startswith('smsp__average_warps_issue_stalled_') and k.endswith('_per_issue_active.ratio')
           and d[k] not in ('', 'n/a')}
     for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:8]:
