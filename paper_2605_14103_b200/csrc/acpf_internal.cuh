@@ -6,6 +6,16 @@
 #include <string>
 
 #include "../../include/acpf.h"
+
+// ACPF_DEBUG_BOUNDS builds (never shipped) turn the index checks at the hot
+// gather/scatter sites into device asserts: compute-sanitizer is not
+// available on the GPU pool, so bad accesses are caught by our own checks
+#ifdef ACPF_DEBUG_BOUNDS
+#include <cassert>
+#define ACPF_CHECK(cond) assert(cond)
+#else
+#define ACPF_CHECK(cond) ((void)0)
+#endif
 #include "nr_symbolic.h"
 
 namespace acpf {

@@ -122,6 +122,7 @@ struct PipeLdgsts {
   static_assert((kRingN & (kRingN - 1)) == 0, "ring size must be a power of two");
   const uint32_t* stream;
   const double* src;  // this lane's copy source: its group's block region + chunk
+  uint32_t n_elem;    // block elements per group (bounds checks)
   bool cp_ok;         // this lane's group is live (NG = 2: lanes 16-31 copy group 1)
   int nlive;          // live groups of the unit
   uint32_t ring;      // smem [kRingN] slots
@@ -161,6 +162,7 @@ struct PipeLdgsts {
         for (int j = 0; j < CH; j += 2) {
           const int jj = j + half;
           const uint32_t w = __shfl_sync(kFull, wcur, (jw + jj) & 31);
+          ACPF_CHECK(jj >= lim || (w & 0x3fffffu) < n_elem);
           if (jj < lim) cp_async16(ring + (slot + jj) * kSlot + chunk * 16, src + (size_t)(w & 0x3fffffu) * kBlk);
         }
       } else {
@@ -168,6 +170,7 @@ struct PipeLdgsts {
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const uint32_t w = __shfl_sync(kFull, wcur, (jw + j) & 31);
+          ACPF_CHECK(j >= lim || (w & 0x3fffffu) < n_elem);
           if (j < lim && cp_ok) cp_async16(ring + (slot + j) * kSlot + lane * 16, src + (size_t)(w & 0x3fffffu) * kBlk);
         }
       }
@@ -569,6 +572,7 @@ __device__ __forceinline__ void pipe_setup(P& pp, const NrDeviceModel& m, const 
   const int half = lane >> 4, chunk = lane & 15;
   const int h = P::NG == 1 ? 0 : half;
   pp.src = w.arena + (size_t)(g0 + h) * gstride + chunk * 2;
+  pp.n_elem = (uint32_t)m.n_block;
   pp.cp_ok = (live >> h) & 1u;
   pp.nlive = __popc(live);
   pp.ring = ring;
@@ -721,6 +725,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         // tail row, tail column: A_pt minus the non-tail updates, stored raw
         // for the dense tail factorisation (nr_tail_kernel)
         const size_t st = (size_t)(uint32_t)stv * kBlk;
+        ACPF_CHECK(st < (size_t)m.n_block * kBlk);
 #pragma unroll
         for (int h = 0; h < NG; ++h)
           if ((live >> h) & 1u) luw[h * gstride + st] = a[h];
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
             // U^_pt = inv(U_pp) A'_pt: column j of A' from the other row's lane
             const double o = __shfl_xor_sync(kFull, a[h], 16);  // entry (1-i, j)
             const double c0 = bi ? o : a[h], c1 = bi ? a[h] : o;
+            ACPF_CHECK(st < (size_t)m.n_block * kBlk);
             if ((live >> h) & 1u) luw[h * gstride + st] = ir0[h] * c0 + ir1[h] * c1;
           }
         }
@@ -750,6 +756,7 @@ __global__ void __launch_bounds__(32) nr_factor_kernel(NrDeviceModel m, NrWorksp
         break;
       }
     }
+    ACPF_CHECK(p >= 0 && p < m.n_rows);
     if (p >= m.tail_row0) {  // tail row: b_p - sum over non-tail t of L^_pt y_t, raw
 #pragma unroll
       for (int h = 0; h < NG; ++h)
@@ -1156,6 +1163,7 @@ __global__ void __launch_bounds__(kTW * 32, ACPF_TAIL_MINB) nr_tail_kernel(NrDev
   for (int r = n2 + tid; r < 8 * np; r += kTW * 32) U[r * kTLd + r] = 1.0;
   for (int k = tid; k < m.n_tail_slot; k += kTW * 32) {
     const int2 e = __ldg(m.tail_slot + k);
+    ACPF_CHECK(e.x >= 0 && e.x < m.n_block && e.y >= 0 && e.y < T * T);
     const double* src = gsrc + (size_t)e.x * kBlk;  // column j of the block at +16 j
     const double2 c0 = *reinterpret_cast<const double2*>(src);
     const double2 c1 = *reinterpret_cast<const double2*>(src + 2 * kGroup);

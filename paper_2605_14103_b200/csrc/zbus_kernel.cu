@@ -377,6 +377,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
             if (MODE == kIterate) {
               if (in) {
                 contrib = sqrt(vr * vr + vi * vi);
+                ACPF_CHECK(!st.run[col] || (tile_col0 + col < io.batch && row < m.n));
                 if (st.run[col]) io.v_out[(tile_col0 + col) * m.n + row] = make_double2(vr, vi);
               }
               acc[b][j] = acc[b][j] + contrib;
@@ -385,6 +386,7 @@ __device__ void zb_pass(const ZbDeviceModel& m, const ZbBatchIO& io, int64_t til
               acc[b][j] = acc[b][j] + contrib;
             } else {  // certificate: |v_final - (Z i(v_final) + v0)|
               if (in && st.cert[col]) {
+                ACPF_CHECK(tile_col0 + col < io.batch && row < m.n);
                 const double2 vf = io.v_out[(tile_col0 + col) * m.n + row];
                 const double dr = vf.x - vr, di = vf.y - vi;
                 contrib = sqrt(dr * dr + di * di);
