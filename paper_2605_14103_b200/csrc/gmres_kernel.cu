@@ -183,7 +183,7 @@ cudaError_t fd_gemm(int M, int N, int K, const double* A, int lda, const double*
 __global__ void gm_phasor(GmModel m, GmWork w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)m.n_bus * w.bc) return;
-  const int i = (int)(t / w.bc), s = (int)(t % w.bc);
+  const int s = (int)(t % w.bc);  // [bus][scenario] layout: t = bus * Bc + s
   if (!w.nactive[s]) return;
   const double th = w.th[t], v = w.vm[t];
   double sn, cs;
